@@ -1,0 +1,643 @@
+/*
+ * ORACLE — test infrastructure only.
+ * Restatement of proj/src/constraints.cpp: contact rows (volume ratio Eq. 10-11,
+ * gap Eq. 12), edge-length rows (Eq. 13), diag, linearize_all, and the
+ * randomized smallest-last coloring; plus the product's deterministic
+ * Jones-Plassmann "device" coloring (defined in DESIGN.md) so that the GPU
+ * performance mode has a bit-exact CPU twin.
+ */
+#include <stdlib.h>
+#include <string.h>
+
+#include "or_internal.h"
+
+static const double kMinRefVolume = 6.0 * 1e-18; /* constraints.cpp:15 */
+static const double kDiagFloor = 1e-10;          /* constraints.cpp:16 */
+
+void or_rowvec_push(or_rowvec* v, const or_row* r) {
+    if (v->n == v->cap) {
+        v->cap = v->cap ? v->cap * 2 : 256;
+        v->rows = (or_row*)or_xrealloc(v->rows, (size_t)v->cap * sizeof(or_row));
+    }
+    v->rows[v->n++] = *r;
+}
+void or_rowvec_free(or_rowvec* v) {
+    free(v->rows);
+    v->rows = NULL;
+    v->n = v->cap = 0;
+}
+
+static void row_init(or_row* c) {
+    memset(c, 0, sizeof *c);
+    c->kind = OR_ROW_VV;
+    c->verts[0] = c->verts[1] = c->verts[2] = c->verts[3] = -1;
+    c->color = -1;
+    c->pair_index = -1;
+    c->edge_index = -1;
+    c->flavor = OR_FLAVOR_GAP;
+}
+
+/* stencil_det, constraints.cpp:19-21 */
+static double stencil_det(v3 p0, v3 p1, v3 p2, v3 p3) {
+    return v3_dot(v3_sub(p1, p0), v3_cross(v3_sub(p2, p0), v3_sub(p3, p0)));
+}
+/* stencil_det_gradient, constraints.cpp:23-27 */
+static void stencil_grad(v3 p0, v3 p1, v3 p2, v3 p3, v3 g[4]) {
+    g[1] = v3_cross(v3_sub(p2, p0), v3_sub(p3, p0));
+    g[2] = v3_cross(v3_sub(p3, p0), v3_sub(p1, p0));
+    g[3] = v3_cross(v3_sub(p1, p0), v3_sub(p2, p0));
+    g[0] = v3_neg(v3_add(v3_add(g[1], g[2]), g[3]));
+}
+
+static int kind_of_pair(const or_pair* p) { /* constraints.cpp:29-35 */
+    if (p->a.kind == OR_KIND_V && p->b.kind == OR_KIND_T) return OR_ROW_VT;
+    if (p->a.kind == OR_KIND_E && p->b.kind == OR_KIND_E) return OR_ROW_EE;
+    if (p->a.kind == OR_KIND_V && p->b.kind == OR_KIND_E) return OR_ROW_VE;
+    return OR_ROW_VV;
+}
+
+#define X(i) v3_load(x + 3 * (size_t)(i))
+
+/* constraint_value_at, constraints.cpp:39-54 */
+double or_constraint_value_at(int flavor, int nverts, const int32_t* verts, double ref_volume,
+                              const double* gap_weights, double denom, double sigma,
+                              const double* x) {
+    switch (flavor) {
+        case OR_FLAVOR_VOLUME:
+            return stencil_det(X(verts[0]), X(verts[1]), X(verts[2]), X(verts[3])) / ref_volume - 1.0;
+        case OR_FLAVOR_GAP: {
+            v3 g = v3_zero();
+            for (int m = 0; m < nverts; ++m) g = v3_add(g, v3_scale(gap_weights[m], X(verts[m])));
+            return v3_norm(g) / denom - 1.0;
+        }
+        default:
+            return sigma - v3_norm(v3_sub(X(verts[0]), X(verts[1]))) / denom;
+    }
+}
+
+/* build_gap_constraint, constraints.cpp:56-76 */
+static void build_gap(const or_pair* p, double delta, int kind, or_row* c) {
+    row_init(c);
+    c->kind = kind;
+    c->flavor = OR_FLAVOR_GAP;
+    c->denom = delta;
+    int n = 0;
+    for (int i = 0; i < or_simplex_size(&p->a); ++i, ++n) {
+        c->verts[n] = p->a.idx[i];
+        c->gap_weights[n] = p->c.wa[i];
+    }
+    for (int i = 0; i < or_simplex_size(&p->b); ++i, ++n) {
+        c->verts[n] = p->b.idx[i];
+        c->gap_weights[n] = -p->c.wb[i];
+    }
+    c->nverts = n;
+    c->value = p->c.distance / delta - 1.0;
+    const v3 dir = p->c.dir;
+    for (int m = 0; m < n; ++m) c->jac[m] = v3_scale(c->gap_weights[m] / delta, dir);
+}
+
+/* build_vt_constraint, constraints.cpp:86-115 */
+static void build_vt(const or_pair* p, const double* x, double delta, or_row* c) {
+    const int va = p->a.idx[0];
+    const int i = p->b.idx[0], j = p->b.idx[1], k = p->b.idx[2];
+    v3 n = v3_cross(v3_sub(X(j), X(i)), v3_sub(X(k), X(i)));
+    const double n_len = v3_norm(n);
+    if (n_len < 1e-20) {
+        build_gap(p, delta, OR_ROW_VT, c);
+        return;
+    }
+    n = v3_div(n, n_len);
+    if (v3_dot(n, p->c.dir) < 0.0) n = v3_neg(n);
+
+    const double h = 0.5 * (delta - p->c.distance);
+    const v3 ra = v3_add(X(va), v3_scale(h, n));
+    const v3 ri = v3_sub(X(i), v3_scale(h, n)), rj = v3_sub(X(j), v3_scale(h, n)),
+             rk = v3_sub(X(k), v3_scale(h, n));
+    const double wr = stencil_det(ra, ri, rj, rk);
+    if (fabs(wr) < kMinRefVolume) {
+        build_gap(p, delta, OR_ROW_VT, c);
+        return;
+    }
+    row_init(c);
+    c->kind = OR_ROW_VT;
+    c->flavor = OR_FLAVOR_VOLUME;
+    c->nverts = 4;
+    c->verts[0] = va, c->verts[1] = i, c->verts[2] = j, c->verts[3] = k;
+    c->ref_volume = wr;
+    c->value = stencil_det(X(va), X(i), X(j), X(k)) / wr - 1.0;
+    v3 g[4];
+    stencil_grad(X(va), X(i), X(j), X(k), g);
+    for (int m = 0; m < 4; ++m) c->jac[m] = v3_div(g[m], wr);
+}
+
+/* build_ee_constraint, constraints.cpp:117-142 */
+static void build_ee(const or_pair* p, const double* x, double delta, or_row* c) {
+    const int p1 = p->a.idx[0], p2 = p->a.idx[1];
+    const int q1 = p->b.idx[0], q2 = p->b.idx[1];
+    const v3 dir = p->c.dir;
+    if (v3_is_zero(dir)) {
+        build_gap(p, delta, OR_ROW_EE, c);
+        return;
+    }
+    const double h = 0.5 * (delta - p->c.distance);
+    const v3 rp1 = v3_add(X(p1), v3_scale(h, dir)), rp2 = v3_add(X(p2), v3_scale(h, dir));
+    const v3 rq1 = v3_sub(X(q1), v3_scale(h, dir)), rq2 = v3_sub(X(q2), v3_scale(h, dir));
+    const double wr = stencil_det(rp1, rp2, rq1, rq2);
+    if (fabs(wr) < kMinRefVolume) {
+        build_gap(p, delta, OR_ROW_EE, c);
+        return;
+    }
+    row_init(c);
+    c->kind = OR_ROW_EE;
+    c->flavor = OR_FLAVOR_VOLUME;
+    c->nverts = 4;
+    c->verts[0] = p1, c->verts[1] = p2, c->verts[2] = q1, c->verts[3] = q2;
+    c->ref_volume = wr;
+    c->value = stencil_det(X(p1), X(p2), X(q1), X(q2)) / wr - 1.0;
+    v3 g[4];
+    stencil_grad(X(p1), X(p2), X(q1), X(q2), g);
+    for (int m = 0; m < 4; ++m) c->jac[m] = v3_div(g[m], wr);
+}
+
+/* fill_diag, constraints.cpp:175-179 */
+void or_fill_diag(or_row* c, const double* inv_mass) {
+    double d = 0.0;
+    for (int m = 0; m < c->nverts; ++m) d += inv_mass[c->verts[m]] * v3_sqn(c->jac[m]);
+    c->diag = or_max(d, kDiagFloor);
+}
+
+/* linearize_all, constraints.cpp:181-220 (edge rows: 144-173) */
+void or_linearize_all(const or_pairset* set, const double* x, const or_mesh* m,
+                      const double* edge_targets, double delta, double sigma, int family,
+                      int edge_constraints, or_rowvec* out) {
+    or_linearize_window(set, x, m, edge_targets, delta, delta, sigma, family, edge_constraints, out);
+}
+
+/* window = activation threshold (linearize_all uses delta; tests may widen it
+ * to build rows outside the window like build_*_constraint does) */
+void or_linearize_window(const or_pairset* set, const double* x, const or_mesh* m,
+                         const double* edge_targets, double delta, double window, double sigma,
+                         int family, int edge_constraints, or_rowvec* out) {
+    out->n = 0;
+    for (int64_t pi = 0; pi < set->n; ++pi) {
+        const or_pair* p = &set->pairs[pi];
+        if (!p->active || p->all_static) continue;
+        if (p->c.distance >= window) continue; /* activation window */
+        or_row c;
+        const int kind = kind_of_pair(p);
+        if (family == OR_FAMILY_GAP) {
+            build_gap(p, delta, kind, &c);
+        } else {
+            switch (kind) {
+                case OR_ROW_VT: build_vt(p, x, delta, &c); break;
+                case OR_ROW_EE: build_ee(p, x, delta, &c); break;
+                case OR_ROW_VE: build_gap(p, delta, OR_ROW_VE, &c); break;
+                default: build_gap(p, delta, OR_ROW_VV, &c); break;
+            }
+        }
+        double jnorm = 0.0;
+        for (int k = 0; k < c.nverts; ++k) jnorm += v3_sqn(c.jac[k]);
+        if (jnorm < 1e-28) continue; /* fully degenerate row */
+        c.pair_index = pi;
+        c.pair_key = p->key;
+        or_fill_diag(&c, m->inv_mass);
+        or_rowvec_push(out, &c);
+    }
+    if (edge_constraints) {
+        for (int e = 0; e < m->ne; ++e) {
+            const int i = m->edges[2 * e], j = m->edges[2 * e + 1];
+            const double ly = edge_targets[e];
+            if (ly <= 1e-12) continue;
+            if (m->inv_mass[i] == 0.0 && m->inv_mass[j] == 0.0) continue;
+            or_row c;
+            row_init(&c);
+            c.kind = OR_ROW_EDGE;
+            c.flavor = OR_FLAVOR_LENGTH;
+            c.nverts = 2;
+            c.verts[0] = i, c.verts[1] = j;
+            c.denom = ly;
+            c.sigma = sigma;
+            c.edge_index = e;
+            const v3 d = v3_sub(X(i), X(j));
+            const double len = v3_norm(d);
+            c.value = sigma - len / ly;
+            if (len > 1e-12) {
+                const v3 u = v3_div(d, len);
+                c.jac[0] = v3_div(v3_neg(u), ly);
+                c.jac[1] = v3_div(u, ly);
+            }
+            or_fill_diag(&c, m->inv_mass);
+            or_rowvec_push(out, &c);
+        }
+    }
+}
+#undef X
+
+/* ---------------------------------------------------------------- RNG */
+
+void or_mt64_seed(or_mt64* g, uint64_t seed) {
+    g->mt[0] = seed;
+    for (int i = 1; i < 312; ++i)
+        g->mt[i] = 6364136223846793005ull * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+    g->idx = 312;
+}
+
+uint64_t or_mt64_next(or_mt64* g) {
+    if (g->idx >= 312) {
+        const uint64_t upper = ~0ull << 31, lower = ~upper;
+        for (int k = 0; k < 312; ++k) {
+            const uint64_t y = (g->mt[k] & upper) | (g->mt[(k + 1) % 312] & lower);
+            g->mt[k] = g->mt[(k + 156) % 312] ^ (y >> 1) ^ ((y & 1) ? 0xB5026F5AA96619E9ull : 0ull);
+        }
+        g->idx = 0;
+    }
+    uint64_t z = g->mt[g->idx++];
+    z ^= (z >> 29) & 0x5555555555555555ull;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+    z ^= (z << 37) & 0xFFF7EEE000000000ull;
+    z ^= z >> 43;
+    return z;
+}
+
+/* libstdc++ 13 uniform_int_distribution<size_t>(0, range-1) with a 64-bit
+ * engine: Lemire's nearly-divisionless _S_nd over unsigned __int128
+ * (/usr/include/c++/13/bits/uniform_int_dist.h:252-328). */
+uint64_t or_uniform_below(or_mt64* g, uint64_t range) {
+    unsigned __int128 product = (unsigned __int128)or_mt64_next(g) * range;
+    uint64_t low = (uint64_t)product;
+    if (low < range) {
+        const uint64_t threshold = (0ull - range) % range;
+        while (low < threshold) {
+            product = (unsigned __int128)or_mt64_next(g) * range;
+            low = (uint64_t)product;
+        }
+    }
+    return (uint64_t)(product >> 64);
+}
+
+uint64_t or_mt19937_64_nth(uint64_t seed, int64_t n) {
+    or_mt64 g;
+    or_mt64_seed(&g, seed);
+    uint64_t v = 0;
+    for (int64_t i = 0; i < n; ++i) v = or_mt64_next(&g);
+    return v;
+}
+
+uint64_t or_uniform_index(uint64_t seed, int64_t draws, uint64_t size) {
+    or_mt64 g;
+    or_mt64_seed(&g, seed);
+    uint64_t v = 0;
+    for (int64_t i = 0; i < draws; ++i) v = or_uniform_below(&g, size);
+    return v;
+}
+
+/* ------------------------------------------------- reference coloring */
+
+typedef struct {
+    int* d;
+    int64_t n, cap;
+} ivec;
+static void ivec_push(ivec* v, int x) {
+    if (v->n == v->cap) {
+        v->cap = v->cap ? v->cap * 2 : 4;
+        v->d = (int*)or_xrealloc(v->d, (size_t)v->cap * sizeof(int));
+    }
+    v->d[v->n++] = x;
+}
+static int cmp_int(const void* a, const void* b) {
+    const int x = *(const int*)a, y = *(const int*)b;
+    return x < y ? -1 : (x > y);
+}
+
+/* conflict adjacency through shared dynamic vertices (constraints.cpp:228-244):
+ * CSR adj_off/adj with sorted, unique neighbor lists */
+static void build_adjacency(const or_row* rows, int64_t n, const double* inv_mass, int nv,
+                            int64_t** adj_off_out, int** adj_out) {
+    /* vertex -> rows (rows in increasing order, one entry per occurrence) */
+    int64_t* voff = (int64_t*)or_xcalloc((size_t)nv + 1, sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i)
+        for (int m = 0; m < rows[i].nverts; ++m) {
+            const int v = rows[i].verts[m];
+            if (inv_mass[v] > 0.0) ++voff[v + 1];
+        }
+    for (int v = 0; v < nv; ++v) voff[v + 1] += voff[v];
+    int* vrows = (int*)or_xmalloc((size_t)(voff[nv] + 1) * sizeof(int));
+    int64_t* fill = (int64_t*)or_xmalloc(((size_t)nv + 1) * sizeof(int64_t));
+    memcpy(fill, voff, ((size_t)nv + 1) * sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i)
+        for (int m = 0; m < rows[i].nverts; ++m) {
+            const int v = rows[i].verts[m];
+            if (inv_mass[v] > 0.0) vrows[fill[v]++] = (int)i;
+        }
+    /* per-row neighbor counts (with multiplicity), then fill */
+    int64_t* off = (int64_t*)or_xcalloc((size_t)n + 1, sizeof(int64_t));
+    for (int v = 0; v < nv; ++v) {
+        const int64_t k = voff[v + 1] - voff[v];
+        for (int64_t a = voff[v]; a < voff[v + 1]; ++a) off[vrows[a] + 1] += k - 1;
+    }
+    for (int64_t i = 0; i < n; ++i) off[i + 1] += off[i];
+    int* adj = (int*)or_xmalloc((size_t)(off[n] + 1) * sizeof(int));
+    int64_t* afill = (int64_t*)or_xmalloc(((size_t)n + 1) * sizeof(int64_t));
+    memcpy(afill, off, ((size_t)n + 1) * sizeof(int64_t));
+    for (int v = 0; v < nv; ++v)
+        for (int64_t a = voff[v]; a < voff[v + 1]; ++a)
+            for (int64_t b = a + 1; b < voff[v + 1]; ++b) {
+                adj[afill[vrows[a]]++] = vrows[b];
+                adj[afill[vrows[b]]++] = vrows[a];
+            }
+    /* sort + unique in place, compact */
+    int64_t w = 0;
+    int64_t* noff = (int64_t*)or_xmalloc(((size_t)n + 1) * sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t s = off[i], e = off[i + 1];
+        qsort(adj + s, (size_t)(e - s), sizeof(int), cmp_int);
+        noff[i] = w;
+        for (int64_t k = s; k < e; ++k)
+            if (k == s || adj[k] != adj[k - 1]) adj[w++] = adj[k];
+    }
+    noff[n] = w;
+    free(off);
+    free(afill);
+    free(voff);
+    free(vrows);
+    free(fill);
+    *adj_off_out = noff;
+    *adj_out = adj;
+}
+
+/* color_constraints, constraints.cpp:222-288 */
+int or_color_reference(or_row* rows, int64_t n, const double* inv_mass, int nv, uint64_t seed) {
+    if (n == 0) return 0;
+    int64_t* off;
+    int* adj;
+    build_adjacency(rows, n, inv_mass, nv, &off, &adj);
+
+    or_mt64 rng;
+    or_mt64_seed(&rng, seed);
+    int* degree = (int*)or_xmalloc((size_t)n * sizeof(int));
+    int* order = (int*)or_xmalloc((size_t)n * sizeof(int));
+    uint8_t* removed = (uint8_t*)or_xcalloc((size_t)n, 1);
+    int max_deg = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        degree[i] = (int)(off[i + 1] - off[i]);
+        if (degree[i] > max_deg) max_deg = degree[i];
+    }
+    ivec* buckets = (ivec*)or_xcalloc((size_t)max_deg + 1, sizeof(ivec));
+    for (int64_t i = 0; i < n; ++i) ivec_push(&buckets[degree[i]], (int)i);
+    for (int64_t picked = 0; picked < n; ++picked) {
+        int d = 0, cand = -1;
+        while (cand < 0) {
+            while (buckets[d].n == 0) ++d;
+            ivec* bkt = &buckets[d];
+            const uint64_t at = or_uniform_below(&rng, (uint64_t)bkt->n); /* random tie-break */
+            const int c = bkt->d[at];
+            bkt->d[at] = bkt->d[bkt->n - 1];
+            --bkt->n;
+            if (!removed[c] && degree[c] == d) cand = c; /* else stale, drop it */
+        }
+        removed[cand] = 1;
+        order[picked] = cand;
+        for (int64_t k = off[cand]; k < off[cand + 1]; ++k) {
+            const int nb = adj[k];
+            if (!removed[nb]) ivec_push(&buckets[--degree[nb]], nb);
+        }
+    }
+
+    int ncolors = 0;
+    int* used = (int*)or_xmalloc(((size_t)n + 1) * sizeof(int));
+    for (int64_t i = 0; i <= n; ++i) used[i] = -1;
+    for (int64_t it = n - 1; it >= 0; --it) {
+        const int i = order[it];
+        for (int64_t k = off[i]; k < off[i + 1]; ++k) {
+            const int nb = adj[k];
+            if (rows[nb].color >= 0) used[rows[nb].color] = i;
+        }
+        int col = 0;
+        while (used[col] == i) ++col;
+        rows[i].color = col;
+        if (col + 1 > ncolors) ncolors = col + 1;
+    }
+    for (int d = 0; d <= max_deg; ++d) free(buckets[d].d);
+    free(buckets);
+    free(used);
+    free(degree);
+    free(order);
+    free(removed);
+    free(off);
+    free(adj);
+    return ncolors;
+}
+
+/* ---------------------------------------------------- device coloring */
+
+/* Priority order of the Jones-Plassmann rounds: larger (prio, index) wins. */
+static inline int jp_beats(uint64_t pa, int64_t ia, uint64_t pb, int64_t ib) {
+    return pa > pb || (pa == pb && ia > ib);
+}
+static inline uint64_t edge_prio(int e) { return or_mix64((uint64_t)(uint32_t)e + 0x5851F42D4C957F2Dull); }
+static inline uint64_t contact_prio(uint64_t key, uint64_t seed) {
+    return or_mix64(key ^ (seed * 0x9E3779B97F4A7C15ull));
+}
+
+/* smallest color not in the (unsorted) list */
+static int smallest_free(const int* cols, int k) {
+    for (int c = 0;; ++c) {
+        int hit = 0;
+        for (int i = 0; i < k; ++i)
+            if (cols[i] == c) {
+                hit = 1;
+                break;
+            }
+        if (!hit) return c;
+    }
+}
+
+/* Edge-row precoloring (once per mesh): Jones-Plassmann rounds over the
+ * edges that are not both-static; conflict = shared vertex with inv_mass > 0;
+ * a round's winners take the smallest color unused by neighbors colored in
+ * earlier rounds. */
+int or_color_edges_impl(int nv, const double* inv_mass, int ne, const int* edges, int32_t* color) {
+    int64_t* voff = (int64_t*)or_xcalloc((size_t)nv + 1, sizeof(int64_t));
+    for (int e = 0; e < ne; ++e)
+        for (int k = 0; k < 2; ++k) ++voff[edges[2 * e + k] + 1];
+    for (int v = 0; v < nv; ++v) voff[v + 1] += voff[v];
+    int* vedges = (int*)or_xmalloc((size_t)(voff[nv] + 1) * sizeof(int));
+    int64_t* fill = (int64_t*)or_xmalloc(((size_t)nv + 1) * sizeof(int64_t));
+    memcpy(fill, voff, ((size_t)nv + 1) * sizeof(int64_t));
+    for (int e = 0; e < ne; ++e)
+        for (int k = 0; k < 2; ++k) vedges[fill[edges[2 * e + k]]++] = e;
+    free(fill);
+
+    int* round = (int*)or_xcalloc((size_t)ne + 1, sizeof(int)); /* 0 = uncolored */
+    int remaining = 0;
+    for (int e = 0; e < ne; ++e) {
+        const int i = edges[2 * e], j = edges[2 * e + 1];
+        if (inv_mass[i] == 0.0 && inv_mass[j] == 0.0) {
+            color[e] = -1;
+            round[e] = -1;
+        } else {
+            color[e] = -1;
+            ++remaining;
+        }
+    }
+    int ncolors = 0;
+    int cap = 64;
+    int* cols = (int*)or_xmalloc((size_t)cap * sizeof(int));
+    int* winners = (int*)or_xmalloc(((size_t)ne + 1) * sizeof(int));
+    for (int r = 1; remaining > 0; ++r) {
+        int nw = 0;
+        for (int e = 0; e < ne; ++e) {
+            if (round[e] != 0) continue;
+            const uint64_t pe = edge_prio(e);
+            int is_max = 1;
+            for (int k = 0; k < 2 && is_max; ++k) {
+                const int v = edges[2 * e + k];
+                if (!(inv_mass[v] > 0.0)) continue;
+                for (int64_t a = voff[v]; a < voff[v + 1]; ++a) {
+                    const int f = vedges[a];
+                    if (f == e || round[f] != 0) continue; /* only uncolored-at-round-start */
+                    if (!jp_beats(pe, e, edge_prio(f), f)) {
+                        is_max = 0;
+                        break;
+                    }
+                }
+            }
+            if (is_max) winners[nw++] = e;
+        }
+        for (int w = 0; w < nw; ++w) {
+            const int e = winners[w];
+            int k = 0;
+            for (int q = 0; q < 2; ++q) {
+                const int v = edges[2 * e + q];
+                if (!(inv_mass[v] > 0.0)) continue;
+                for (int64_t a = voff[v]; a < voff[v + 1]; ++a) {
+                    const int f = vedges[a];
+                    if (f == e || round[f] <= 0) continue;
+                    if (k == cap) cols = (int*)or_xrealloc(cols, (size_t)(cap *= 2) * sizeof(int));
+                    cols[k++] = color[f];
+                }
+            }
+            color[e] = smallest_free(cols, k);
+            if (color[e] + 1 > ncolors) ncolors = color[e] + 1;
+        }
+        for (int w = 0; w < nw; ++w) round[winners[w]] = r;
+        remaining -= nw;
+    }
+    free(cols);
+    free(winners);
+    free(round);
+    free(vedges);
+    free(voff);
+    return ncolors;
+}
+
+int or_color_edges(int nv, const double* inv_mass, int ne, const int* edges, int32_t* edge_color) {
+    return or_color_edges_impl(nv, inv_mass, ne, edges, edge_color);
+}
+
+/* Per-step device coloring: edge rows take the precomputed edge color;
+ * contact rows run Jones-Plassmann rounds among themselves, avoiding the
+ * colors of every non-static mesh edge incident to one of their dynamic
+ * vertices (when edge rows are enabled). */
+int or_color_device(or_row* rows, int64_t n, const double* inv_mass, int nv, uint64_t seed,
+                    const int32_t* edge_color, int ne, const int* edges, int edge_constraints) {
+    int64_t nc = 0;
+    while (nc < n && rows[nc].kind != OR_ROW_EDGE) ++nc;
+    int ncolors = 0;
+    for (int64_t i = nc; i < n; ++i) {
+        rows[i].color = edge_color[rows[i].edge_index];
+        if (rows[i].color + 1 > ncolors) ncolors = rows[i].color + 1;
+    }
+    /* vertex -> contact rows, vertex -> edges */
+    int64_t* voff = (int64_t*)or_xcalloc((size_t)nv + 1, sizeof(int64_t));
+    for (int64_t i = 0; i < nc; ++i)
+        for (int m = 0; m < rows[i].nverts; ++m) ++voff[rows[i].verts[m] + 1];
+    for (int v = 0; v < nv; ++v) voff[v + 1] += voff[v];
+    int* vrows = (int*)or_xmalloc((size_t)(voff[nv] + 1) * sizeof(int));
+    int64_t* fill = (int64_t*)or_xmalloc(((size_t)nv + 1) * sizeof(int64_t));
+    memcpy(fill, voff, ((size_t)nv + 1) * sizeof(int64_t));
+    for (int64_t i = 0; i < nc; ++i)
+        for (int m = 0; m < rows[i].nverts; ++m) vrows[fill[rows[i].verts[m]]++] = (int)i;
+    int64_t* eoff = (int64_t*)or_xcalloc((size_t)nv + 1, sizeof(int64_t));
+    for (int e = 0; e < ne; ++e)
+        for (int k = 0; k < 2; ++k) ++eoff[edges[2 * e + k] + 1];
+    for (int v = 0; v < nv; ++v) eoff[v + 1] += eoff[v];
+    int* vedges = (int*)or_xmalloc((size_t)(eoff[nv] + 1) * sizeof(int));
+    memcpy(fill, eoff, ((size_t)nv + 1) * sizeof(int64_t));
+    for (int e = 0; e < ne; ++e)
+        for (int k = 0; k < 2; ++k) vedges[fill[edges[2 * e + k]]++] = e;
+    free(fill);
+
+    uint64_t* prio = (uint64_t*)or_xmalloc(((size_t)nc + 1) * sizeof(uint64_t));
+    int* round = (int*)or_xcalloc((size_t)nc + 1, sizeof(int));
+    int* winners = (int*)or_xmalloc(((size_t)nc + 1) * sizeof(int));
+    /* largest-(approximate)-degree first, hashed tie-break: the conflict
+     * degree counts, with multiplicity, the other contact rows at each
+     * dynamic vertex */
+    for (int64_t i = 0; i < nc; ++i) {
+        uint64_t deg = 0;
+        for (int m = 0; m < rows[i].nverts; ++m) {
+            const int v = rows[i].verts[m];
+            if (inv_mass[v] > 0.0) deg += (uint64_t)(voff[v + 1] - voff[v] - 1);
+        }
+        if (deg > 0xFFFFF) deg = 0xFFFFF;
+        prio[i] = (deg << 44) | (contact_prio(rows[i].pair_key, seed) >> 20);
+    }
+    int cap = 64;
+    int* cols = (int*)or_xmalloc((size_t)cap * sizeof(int));
+    int64_t remaining = nc;
+    for (int r = 1; remaining > 0; ++r) {
+        int nw = 0;
+        for (int64_t i = 0; i < nc; ++i) {
+            if (round[i] != 0) continue;
+            int is_max = 1;
+            for (int m = 0; m < rows[i].nverts && is_max; ++m) {
+                const int v = rows[i].verts[m];
+                if (!(inv_mass[v] > 0.0)) continue;
+                for (int64_t a = voff[v]; a < voff[v + 1]; ++a) {
+                    const int j = vrows[a];
+                    if (j == i || round[j] != 0) continue;
+                    if (!jp_beats(prio[i], i, prio[j], j)) {
+                        is_max = 0;
+                        break;
+                    }
+                }
+            }
+            if (is_max) winners[nw++] = (int)i;
+        }
+        for (int w = 0; w < nw; ++w) {
+            const int i = winners[w];
+            int k = 0;
+            for (int m = 0; m < rows[i].nverts; ++m) {
+                const int v = rows[i].verts[m];
+                if (!(inv_mass[v] > 0.0)) continue;
+                for (int64_t a = voff[v]; a < voff[v + 1]; ++a) {
+                    const int j = vrows[a];
+                    if (j == i || round[j] <= 0) continue;
+                    if (k == cap) cols = (int*)or_xrealloc(cols, (size_t)(cap *= 2) * sizeof(int));
+                    cols[k++] = rows[j].color;
+                }
+                if (edge_constraints)
+                    for (int64_t a = eoff[v]; a < eoff[v + 1]; ++a) {
+                        const int e = vedges[a];
+                        if (edge_color[e] < 0) continue;
+                        if (k == cap) cols = (int*)or_xrealloc(cols, (size_t)(cap *= 2) * sizeof(int));
+                        cols[k++] = edge_color[e];
+                    }
+            }
+            rows[i].color = smallest_free(cols, k);
+            if (rows[i].color + 1 > ncolors) ncolors = rows[i].color + 1;
+        }
+        for (int w = 0; w < nw; ++w) round[winners[w]] = r;
+        remaining -= nw;
+    }
+    free(cols);
+    free(prio);
+    free(round);
+    free(winners);
+    free(voff);
+    free(vrows);
+    free(eoff);
+    free(vedges);
+    return ncolors;
+}
