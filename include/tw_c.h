@@ -1,0 +1,194 @@
+/*
+ * tw_c.h — C-ABI of the B200-native two-way continuous collision handling
+ * path (arXiv 2211.04045, reference proj/include/twoway/resolve.hpp).
+ *
+ * The reference exposes only C++ (twoway::resolve / twoway::repair,
+ * resolve.hpp:63-69) and a pybind11 module (bindings/module.cpp:101-186). This
+ * C-ABI is the boundary a drop-in replacement needs: plain pointers and sizes,
+ * no CUDA or torch types. include/twoway/resolve.hpp re-implements the
+ * reference C++ API on top of it; paper_2211_04045_b200/_twoway mirrors the
+ * Python module. All arithmetic is FP64 on the GPU (sm_100a); there is no
+ * CPU fallback — without a CUDA device every call returns TW_ECUDA.
+ *
+ * Positions are N x 3 row-major doubles: the byte layout of
+ * std::vector<Eigen::Vector3d> (types.hpp:10-14) and of a numpy (N, 3) array.
+ */
+#ifndef TW_C_H
+#define TW_C_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TW_ABI_VERSION 1
+
+/* error codes (the C++ wrapper maps EINVAL/EUNSUPPORTED to
+ * std::invalid_argument as resolve.cpp:12-21,39-43 throws, the rest to
+ * std::runtime_error) */
+enum {
+    TW_OK = 0,
+    TW_EINVAL = 1,       /* bad config / sizes / non-finite input */
+    TW_EUNSUPPORTED = 2, /* solver al20/al100 (paper baseline, out of scope) */
+    TW_ECAPACITY = 3,    /* internal: a device buffer was too small (regrown + retried) */
+    TW_ECUDA = 4,        /* CUDA runtime error / no device */
+    TW_ETIMEOUT = 5      /* device watchdog fired inside the resolve kernel */
+};
+
+enum { TW_SOLVER_PGS = 0, TW_SOLVER_JACOBI = 1, TW_SOLVER_AL20 = 2, TW_SOLVER_AL100 = 3 };
+enum { TW_FAMILY_VOLUME = 0, TW_FAMILY_GAP = 1 };
+/* TW_COLOR_REFERENCE replays the reference's randomized smallest-last greedy
+ * coloring (constraints.cpp:222-288) exactly on one device thread — bit-exact
+ * end-to-end parity, slow at scale. TW_COLOR_DEVICE is the parallel
+ * deterministic Jones-Plassmann coloring: a different but valid
+ * Gauss-Seidel order, the performance mode. */
+enum { TW_COLOR_REFERENCE = 0, TW_COLOR_DEVICE = 1 };
+
+/* ResolveConfig, resolve.hpp:13-34 (+ coloring_mode) */
+typedef struct {
+    int32_t step_limit;   /* L = 512 */
+    int32_t solver;       /* TW_SOLVER_* */
+    double eps;           /* 1e-4 */
+    double d_min;         /* 2e-3 m */
+    double d_max;         /* 4e-3 m */
+    double delta;         /* 1e-3 m */
+    double sigma;         /* 1.1 */
+    double gamma;         /* 0.9 */
+    int32_t sweeps;       /* 1 */
+    int32_t family;       /* TW_FAMILY_* */
+    double under_relax;   /* 0.5 */
+    int32_t edge_constraints;
+    int32_t force_fresh_search;
+    int32_t record_path;
+    int32_t coloring_mode; /* TW_COLOR_* */
+    uint64_t color_seed;   /* 0x5eed */
+} tw_resolve_config;
+
+/* ResolveStats, resolve.hpp:36-51 (vectors are separate buffers) */
+typedef struct {
+    int32_t steps;
+    int32_t searches;
+    double final_residual;
+    double wall_ms;           /* host wall time of the call */
+    int32_t converged;
+    int32_t hit_step_limit;
+    int32_t stagnated;
+    int32_t start_in_contact;
+    int32_t step_law_violated;
+    int32_t num_pairs;        /* |P| after the last step */
+    int64_t pairs_evaluated;  /* narrow-phase closest evaluations (search + refresh) */
+    int64_t rows_solved;      /* sum over steps of (contact + edge rows) */
+    double device_ms;         /* CUDA-event time of the device resolve (no H2D/D2H) */
+    int32_t kernel_launches;  /* kernels this call launched */
+    int32_t retries;          /* capacity regrow restarts */
+} tw_resolve_stats;
+
+/* per-step diagnostics (same fields as the oracle's trace) */
+typedef struct {
+    int32_t searched;
+    int32_t num_pairs;
+    int32_t num_contact_rows;
+    int32_t num_edge_rows;
+    int32_t num_colors;
+    int32_t num_active_pairs;
+    double bound;
+    double max_disp;
+    double residual;
+} tw_step_trace;
+
+typedef struct tw_ctx tw_ctx;
+typedef struct tw_mesh tw_mesh;
+
+int tw_abi_version(void);
+void tw_default_config(tw_resolve_config* cfg);
+
+/* One context per (host thread, device); not thread-safe. stream may be NULL
+ * (the context creates its own) or a cudaStream_t to run on. */
+int tw_ctx_create(int device, void* stream, tw_ctx** out);
+void tw_ctx_destroy(tw_ctx* ctx);
+const char* tw_last_error(const tw_ctx* ctx);
+/* kernels launched by this context since creation */
+int64_t tw_ctx_kernel_launches(const tw_ctx* ctx);
+
+/* Topology upload (once per scene). Runs MeshState::finalize's edge
+ * derivation (mesh.cpp:10-33) on the explicit, strand and triangle edges:
+ * the resulting order defines edge indices. inv_mass may be NULL (all 1). */
+int tw_mesh_create(tw_ctx* ctx, int32_t nv, const double* inv_mass, int32_t ne_explicit,
+                   const int32_t* edges, int32_t ns, const int32_t* strand_edges, int32_t nt,
+                   const int32_t* triangles, tw_mesh** out);
+int32_t tw_mesh_num_edges(const tw_mesh* mesh);
+int tw_mesh_edges(const tw_mesh* mesh, int32_t* out_edges /* 2 * ne */);
+void tw_mesh_destroy(tw_mesh* mesh);
+
+/* resolve(x_start, y_target, mesh, cfg) — resolve.cpp:36-144. Host buffers.
+ * step_max_disp: NULL or step_limit doubles; path: NULL or
+ * (step_limit + 1) * nv * 3 doubles (used when cfg->record_path); trace:
+ * NULL or step_limit entries. */
+int tw_resolve(tw_ctx* ctx, tw_mesh* mesh, const double* x_start, const double* y_target,
+               const tw_resolve_config* cfg, double* x_out, tw_resolve_stats* stats,
+               double* step_max_disp, double* path, tw_step_trace* trace);
+
+/* Same with device pointers already resident in HBM (nv * 3 doubles each). */
+int tw_resolve_device(tw_ctx* ctx, tw_mesh* mesh, const double* d_x_start,
+                      const double* d_y_target, const tw_resolve_config* cfg, double* d_x_out,
+                      tw_resolve_stats* stats);
+
+/* ---- stage entry points (stage-by-stage parity; host buffers) ---- */
+
+/* simplex_pair_closest for n arbitrary pairs. kinds: 2n (ka, kb); verts: 6n
+ * (3 ids of a, 3 ids of b, -1 padded). out: 11n = [dist, wa[3], wb[3],
+ * dir[3], degenerate]; has: n = 1 value, 0 nullopt, -1 adjacent/unsupported. */
+int tw_stage_closest(tw_ctx* ctx, int32_t nv, const double* x, int64_t n, const int32_t* kinds,
+                     const int32_t* verts, double* out, int32_t* has);
+
+/* proximity_search (proximity.cpp:76-183) on the device broad phase. Writes
+ * at most cap pairs sorted by key; *np receives P (if P > cap, nothing is
+ * written and TW_ECAPACITY is returned). wa/wb/dir: 3 doubles per pair;
+ * flags: bit0 active, bit1 all_static, bit2 degenerate. */
+int tw_stage_search(tw_ctx* ctx, tw_mesh* mesh, const double* x, double d_max, int64_t cap,
+                    uint64_t* keys, double* dist, double* wa, double* wb, double* dir,
+                    uint8_t* flags, int64_t* np);
+
+/* refresh_distances (proximity.cpp:190-202) in place, then per_vertex_bound
+ * (proximity.cpp:204-211) for every vertex into vertex_bound (may be NULL). */
+int tw_stage_refresh(tw_ctx* ctx, tw_mesh* mesh, const double* x, double bound, int64_t np,
+                     const uint64_t* keys, double* dist, double* wa, double* wb, double* dir,
+                     uint8_t* flags, double* vertex_bound);
+
+/* linearize_all (constraints.cpp:181-220): contact rows then edge rows.
+ * Row arrays: kind (u8), verts (4 x i32, -1 padded), value, jac (12 doubles),
+ * diag, pair_key (u64), edge_index (i32). Returns R in *nrows. */
+int tw_stage_linearize(tw_ctx* ctx, tw_mesh* mesh, const double* x, int64_t np,
+                       const uint64_t* keys, const double* dist, const double* wa,
+                       const double* wb, const double* dir, const uint8_t* flags,
+                       const double* edge_targets, double delta, double sigma, int32_t family,
+                       int32_t edge_constraints, int64_t cap, uint8_t* kind, int32_t* verts,
+                       double* value, double* jac, double* diag, uint64_t* pair_key,
+                       int32_t* edge_index, int64_t* nrows);
+
+/* color_constraints on rows produced by tw_stage_linearize (contact rows
+ * first). mode TW_COLOR_*. Returns the color count in *ncolors. */
+int tw_stage_color(tw_ctx* ctx, tw_mesh* mesh, int64_t nrows, const uint8_t* kind,
+                   const int32_t* verts, const uint64_t* pair_key, const int32_t* edge_index,
+                   uint64_t seed, int32_t mode, int32_t edge_constraints, int32_t* color,
+                   int32_t* ncolors);
+
+/* assemble_lcp + pgs/jacobi sweeps + recover_target (lcp.cpp). lambda in/out. */
+int tw_stage_backward(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t nrows,
+                      const int32_t* verts, const double* value, const double* jac,
+                      const double* diag, const int32_t* color, int32_t ncolors,
+                      const double* x, const double* y_target, int32_t solver, int32_t sweeps,
+                      double under_relax, double* lambda, double* q_out, double* y_out);
+
+/* advance (advance.cpp:8-39): x and r in/out, D = per-vertex bound. */
+int tw_stage_advance(tw_ctx* ctx, int32_t nv, const double* inv_mass, const double* y,
+                     const double* D, double gamma, double* x, double* r, double* max_disp);
+
+/* ---- CCD certification on the device is out of scope this round ---- */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

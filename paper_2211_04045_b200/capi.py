@@ -1,0 +1,288 @@
+"""ctypes binding of the C-ABI (include/tw_c.h) in libtwoway_b200.so.
+
+This is the host-side entry the tests and the benchmark use; it mirrors the
+reference's operator interface (resolve(x, y, mesh, cfg) -> x, stats). The
+library is built in-tree by ``make`` / ``__graft_entry__.build()``; importing
+without it, or calling without a CUDA device, raises (there is no CPU
+fallback on this path).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtwoway_b200.so")
+
+TW_OK, TW_EINVAL, TW_EUNSUPPORTED, TW_ECAPACITY, TW_ECUDA, TW_ETIMEOUT = range(6)
+SOLVERS = {"pgs": 0, "jacobi": 1, "al20": 2, "al100": 3}
+FAMILIES = {"volume": 0, "gap": 1}
+COLORINGS = {"reference": 0, "device": 1}
+
+
+class TwError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"tw error {code}: {msg}")
+        self.code = code
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("step_limit", C.c_int32), ("solver", C.c_int32), ("eps", C.c_double),
+        ("d_min", C.c_double), ("d_max", C.c_double), ("delta", C.c_double),
+        ("sigma", C.c_double), ("gamma", C.c_double), ("sweeps", C.c_int32),
+        ("family", C.c_int32), ("under_relax", C.c_double), ("edge_constraints", C.c_int32),
+        ("force_fresh_search", C.c_int32), ("record_path", C.c_int32),
+        ("coloring_mode", C.c_int32), ("color_seed", C.c_uint64),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("steps", C.c_int32), ("searches", C.c_int32), ("final_residual", C.c_double),
+        ("wall_ms", C.c_double), ("converged", C.c_int32), ("hit_step_limit", C.c_int32),
+        ("stagnated", C.c_int32), ("start_in_contact", C.c_int32),
+        ("step_law_violated", C.c_int32), ("num_pairs", C.c_int32),
+        ("pairs_evaluated", C.c_int64), ("rows_solved", C.c_int64), ("device_ms", C.c_double),
+        ("kernel_launches", C.c_int32), ("retries", C.c_int32),
+    ]
+
+
+class StepTrace(C.Structure):
+    _fields_ = [
+        ("searched", C.c_int32), ("num_pairs", C.c_int32), ("num_contact_rows", C.c_int32),
+        ("num_edge_rows", C.c_int32), ("num_colors", C.c_int32), ("num_active_pairs", C.c_int32),
+        ("bound", C.c_double), ("max_disp", C.c_double), ("residual", C.c_double),
+    ]
+
+
+EXPORTS = [
+    "tw_abi_version", "tw_default_config", "tw_ctx_create", "tw_ctx_destroy", "tw_last_error",
+    "tw_ctx_kernel_launches", "tw_mesh_create", "tw_mesh_num_edges", "tw_mesh_edges",
+    "tw_mesh_destroy", "tw_resolve", "tw_resolve_device", "tw_stage_closest", "tw_stage_search",
+    "tw_stage_refresh", "tw_stage_linearize", "tw_stage_color", "tw_stage_backward",
+    "tw_stage_advance",
+]
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built (run `make` or __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.tw_abi_version.restype = C.c_int
+        L.tw_default_config.argtypes = [C.POINTER(Config)]
+        L.tw_ctx_create.argtypes = [C.c_int, P, C.POINTER(P)]
+        L.tw_ctx_destroy.argtypes = [P]
+        L.tw_last_error.restype = C.c_char_p
+        L.tw_last_error.argtypes = [P]
+        L.tw_ctx_kernel_launches.restype = C.c_int64
+        L.tw_ctx_kernel_launches.argtypes = [P]
+        L.tw_mesh_create.argtypes = [P, C.c_int32, P, C.c_int32, P, C.c_int32, P, C.c_int32, P, C.POINTER(P)]
+        L.tw_mesh_num_edges.restype = C.c_int32
+        L.tw_mesh_num_edges.argtypes = [P]
+        L.tw_mesh_edges.argtypes = [P, P]
+        L.tw_mesh_destroy.argtypes = [P]
+        L.tw_resolve.argtypes = [P, P, P, P, C.POINTER(Config), P, C.POINTER(Stats), P, P, P]
+        L.tw_resolve_device.argtypes = [P, P, P, P, C.POINTER(Config), P, C.POINTER(Stats)]
+        L.tw_stage_closest.argtypes = [P, C.c_int32, P, C.c_int64, P, P, P, P]
+        L.tw_stage_search.argtypes = [P, P, P, C.c_double, C.c_int64, P, P, P, P, P, P, P]
+        L.tw_stage_refresh.argtypes = [P, P, P, C.c_double, C.c_int64, P, P, P, P, P, P, P]
+        L.tw_stage_advance.argtypes = [P, C.c_int32, P, P, P, C.c_double, P, P, P]
+        _LIB = L
+    return _LIB
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def make_config(**kw) -> Config:
+    c = Config()
+    lib().tw_default_config(C.byref(c))
+    for k, v in kw.items():
+        if k == "solver":
+            v = SOLVERS[v] if isinstance(v, str) else v
+        elif k in ("constraint_family", "family"):
+            k, v = "family", (FAMILIES[v] if isinstance(v, str) else v)
+        elif k in ("coloring", "coloring_mode"):
+            k, v = "coloring_mode", (COLORINGS[v] if isinstance(v, str) else v)
+        elif k in ("edge_constraints", "force_fresh_search", "record_path"):
+            v = int(bool(v))
+        if not any(k == f[0] for f in Config._fields_):
+            raise ValueError(f"unknown config key '{k}'")
+        setattr(c, k, v)
+    return c
+
+
+class Context:
+    """One tw_ctx: device buffers + stream (not thread-safe)."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self.h = C.c_void_p()
+        rc = lib().tw_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(self.h))
+        if rc != TW_OK:
+            raise TwError(rc, "tw_ctx_create failed (no CUDA device?)")
+
+    def check(self, rc):
+        if rc != TW_OK:
+            raise TwError(rc, lib().tw_last_error(self.h).decode())
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(lib().tw_ctx_kernel_launches(self.h))
+
+    def close(self):
+        if self.h:
+            lib().tw_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Mesh:
+    """tw_mesh: topology uploaded once (edge order = MeshState::finalize)."""
+
+    def __init__(self, ctx: Context, nv, inv_mass=None, edges=(), strand_edges=(), triangles=()):
+        self.ctx = ctx
+        self.nv = int(nv)
+        im = None if inv_mass is None else np.ascontiguousarray(inv_mass, np.float64)
+        self.inv_mass = np.ones(self.nv) if im is None else im
+        e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1, 2))
+        s = np.ascontiguousarray(np.asarray(strand_edges, np.int32).reshape(-1, 2))
+        t = np.ascontiguousarray(np.asarray(triangles, np.int32).reshape(-1, 3))
+        self.triangles = t
+        self.h = C.c_void_p()
+        ctx.check(lib().tw_mesh_create(ctx.h, self.nv, _p(im), len(e), _p(e), len(s), _p(s), len(t), _p(t),
+                                       C.byref(self.h)))
+        ne = lib().tw_mesh_num_edges(self.h)
+        self.edges = np.zeros((ne, 2), np.int32)
+        lib().tw_mesh_edges(self.h, _p(self.edges))
+
+    @classmethod
+    def from_scene(cls, ctx, sc):
+        return cls(ctx, sc.nv, sc.inv_mass, sc.edges, sc.strand_edges, sc.triangles)
+
+    def close(self):
+        if self.h:
+            lib().tw_mesh_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def resolve(ctx: Context, mesh: Mesh, x, y, trace=False, **kw):
+    """resolve(x_start, y_target, mesh, cfg) on the device. Returns (x_out, stats dict)."""
+    cfg = make_config(**kw)
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    y = np.ascontiguousarray(y, np.float64).reshape(-1, 3)
+    if len(x) != mesh.nv or len(y) != mesh.nv:
+        raise ValueError("resolve: position arrays do not match mesh")
+    xo = np.zeros_like(x)
+    st = Stats()
+    smd = np.zeros(max(1, cfg.step_limit))
+    path = np.zeros((cfg.step_limit + 1, mesh.nv, 3)) if cfg.record_path else None
+    tr = (StepTrace * cfg.step_limit)() if trace else None
+    rc = lib().tw_resolve(ctx.h, mesh.h, _p(x), _p(y), C.byref(cfg), _p(xo), C.byref(st), _p(smd), _p(path),
+                          C.cast(tr, C.c_void_p) if tr is not None else None)
+    if rc == TW_EINVAL:
+        raise ValueError(lib().tw_last_error(ctx.h).decode())
+    if rc == TW_EUNSUPPORTED:
+        raise NotImplementedError(lib().tw_last_error(ctx.h).decode())
+    ctx.check(rc)
+    stats = {k: getattr(st, k) for k, _ in Stats._fields_}
+    stats["step_max_disp"] = smd[:st.steps].copy()
+    if path is not None:
+        stats["path"] = path[:st.steps + 1].copy()
+    if tr is not None:
+        stats["trace"] = [{k: getattr(tr[i], k) for k, _ in StepTrace._fields_} for i in range(st.steps)]
+    return xo, stats
+
+
+def resolve_device_ptr(ctx: Context, mesh: Mesh, d_x: int, d_y: int, d_out: int, **kw):
+    """resolve on device pointers already resident in HBM (nv*3 float64 each)."""
+    cfg = make_config(**kw)
+    st = Stats()
+    ctx.check(lib().tw_resolve_device(ctx.h, mesh.h, C.c_void_p(d_x), C.c_void_p(d_y), C.byref(cfg),
+                                      C.c_void_p(d_out), C.byref(st)))
+    return {k: getattr(st, k) for k, _ in Stats._fields_}
+
+
+def closest_batch(ctx: Context, x, kinds, verts):
+    """simplex_pair_closest for n pairs. kinds (n, 2), verts (n, 6)."""
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    kinds = np.ascontiguousarray(kinds, np.int32).reshape(-1, 2)
+    verts = np.ascontiguousarray(verts, np.int32).reshape(-1, 6)
+    n = len(kinds)
+    out = np.zeros((n, 11))
+    has = np.zeros(n, np.int32)
+    ctx.check(lib().tw_stage_closest(ctx.h, len(x), _p(x), n, _p(kinds), _p(verts), _p(out), _p(has)))
+    return out, has
+
+
+class Pairs:
+    def __init__(self, n):
+        self.keys = np.zeros(n, np.uint64)
+        self.dist = np.zeros(n)
+        self.wa = np.zeros((n, 3))
+        self.wb = np.zeros((n, 3))
+        self.dir = np.zeros((n, 3))
+        self.flags = np.zeros(n, np.uint8)
+
+    def __len__(self):
+        return len(self.keys)
+
+    def take(self, n):
+        p = Pairs(0)
+        for k in ("keys", "dist", "wa", "wb", "dir", "flags"):
+            setattr(p, k, getattr(self, k)[:n].copy())
+        return p
+
+
+def search(ctx: Context, mesh: Mesh, x, d_max, cap=None) -> Pairs:
+    """proximity_search on the device broad phase; pairs sorted by key."""
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    cap = cap or max(1024, 64 * mesh.nv)
+    while True:
+        P = Pairs(cap)
+        n = C.c_int64(0)
+        rc = lib().tw_stage_search(ctx.h, mesh.h, _p(x), d_max, cap, _p(P.keys), _p(P.dist), _p(P.wa), _p(P.wb),
+                                   _p(P.dir), _p(P.flags), C.byref(n))
+        if rc == TW_ECAPACITY and n.value > cap:
+            cap = n.value
+            continue
+        ctx.check(rc)
+        return P.take(n.value)
+
+
+def refresh(ctx: Context, mesh: Mesh, x, bound, pairs: Pairs):
+    """refresh_distances in place; returns per_vertex_bound for every vertex."""
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    D = np.zeros(mesh.nv)
+    ctx.check(lib().tw_stage_refresh(ctx.h, mesh.h, _p(x), bound, len(pairs), _p(pairs.keys), _p(pairs.dist),
+                                     _p(pairs.wa), _p(pairs.wb), _p(pairs.dir), _p(pairs.flags), _p(D)))
+    return D
+
+
+def advance(ctx: Context, inv_mass, y, D, gamma, x, r):
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3).copy()
+    r = np.ascontiguousarray(r, np.float64).copy()
+    md = C.c_double(0.0)
+    ctx.check(lib().tw_stage_advance(ctx.h, len(r), _p(np.ascontiguousarray(inv_mass, np.float64)),
+                                     _p(np.ascontiguousarray(y, np.float64)), _p(np.ascontiguousarray(D, np.float64)),
+                                     gamma, _p(x), _p(r), C.byref(md)))
+    return x, r, md.value

@@ -1,0 +1,1000 @@
+// C-ABI (include/tw_c.h) of the B200 two-way collision handling path: context
+// and mesh management, capacity growth, the per-call orchestration around
+// the persistent resolve kernel, and the stage entry points.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "tw_c.h"
+#include "tw_internal.h"
+
+using namespace tw;
+
+namespace {
+
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t n) {
+        n = n ? n : 16;
+        if (n <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        const cudaError_t e = cudaMalloc(&p, n);
+        if (e == cudaSuccess) bytes = n;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct BvhMem {
+    DevMem prim, child, parent, lo, hi, flag;
+    int n = 0;
+    Bvh view() const {
+        return Bvh{n, prim.as<int>(), child.as<int2>(), parent.as<int>(), lo.as<float4>(), hi.as<float4>(),
+                   flag.as<unsigned>()};
+    }
+};
+
+}  // namespace
+
+struct tw_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    int sm_count = 0;
+    int nblocks = 0;
+    long long launches = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // capacities
+    long long pcap = 0;
+    int K = 64;
+    long long arch_cap = 0;
+    int colcap = 1024;
+    long long refpool_cap = 0;
+    // buffers
+    DevMem xs, ys, xo;  // N x 3 staging
+    DevMem x, yk1, r, imp, dmin, vhead, vcnt;
+    DevMem ly, is_er, er_edge, er_index, er_value, er_g, er_q, edge_lambda, er_color, er_by_color, er_color_off,
+        er_color_cnt;
+    DevMem pkey, pids, pdd, pw, pflag, qcount, qslot;
+    DevMem c_key, c_ids, c_jac, c_value, c_diag, c_q, c_lambda, c_next, c_color, c_stamp, c_arch, c_prio, c_by_color;
+    DevMem vnext;
+    DevMem ccount, coff;
+    DevMem arch_key0, arch_key1, arch_val0, arch_val1, new_lb, new_key, new_val;
+    DevMem refpool;
+    DevMem part_q, part_c, part_k, blk_lo, blk_hi;
+    DevMem globals, box, bvh_tmp, smd, trace, path;
+    // stage scratch
+    DevMem s_kinds, s_verts, s_out, s_has;
+    // TW_DEBUG progress markers (host-mapped)
+    int* dbg_host = nullptr;
+    int* dbg_dev = nullptr;
+};
+
+struct tw_mesh {
+    tw_ctx* ctx = nullptr;
+    int nv = 0, ne = 0, nt = 0, niso = 0;
+    std::vector<int32_t> edges;  // 2 ne, finalized order
+    std::vector<double> inv_mass;
+    DevMem d_inv_mass, d_edges, d_tris, d_iso, d_vedge_off, d_vedge, d_edge_color;
+    int edge_ncolors = 0;
+    BvhMem bvh[3];
+};
+
+namespace {
+
+int fail(tw_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int cuda_fail(tw_ctx* ctx, cudaError_t e, const char* where) {
+    std::string msg = std::string(where) + ": " + cudaGetErrorString(e);
+    if (ctx && ctx->dbg_host) {  // TW_DEBUG: last phase (step << 16 | source line) per CTA
+        std::map<int, int> hist;
+        for (int b = 0; b < ctx->nblocks; ++b) ++hist[ctx->dbg_host[b]];
+        msg += " [progress:";
+        for (auto& kv : hist)
+            msg += " step" + std::to_string(kv.first >> 16) + "/line" + std::to_string(kv.first & 0xffff) + "x" +
+                   std::to_string(kv.second);
+        msg += "]";
+    }
+    return fail(ctx, TW_ECUDA, msg);
+}
+
+#define CK(expr)                                               \
+    do {                                                       \
+        const cudaError_t _e = (expr);                         \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr); \
+    } while (0)
+
+// ResolveConfig::validate (resolve.cpp:12-21)
+bool config_valid(const tw_resolve_config& c) {
+    if (!(c.d_min > 0.0) || !(c.d_min <= c.d_max)) return false;
+    if (!(c.delta > 0.0) || !(c.delta <= c.d_min)) return false;
+    if (!(c.gamma > 0.0) || !(c.gamma < 1.0)) return false;
+    if (!(c.eps > 0.0)) return false;
+    if (c.step_limit < 1) return false;
+    if (c.sweeps < 1) return false;
+    return true;
+}
+
+// MeshState::finalize edge derivation, mesh.cpp:15-26
+std::vector<int32_t> finalize_edges(int ne_explicit, const int32_t* edges, int ns, const int32_t* strands, int nt,
+                                    const int32_t* tris) {
+    std::vector<int32_t> out;
+    out.reserve(2 * (size_t)(ne_explicit + ns + 3 * (size_t)nt));
+    std::unordered_set<uint64_t> seen;
+    seen.reserve(2 * (size_t)(ne_explicit + ns + 3 * (size_t)nt) + 16);
+    auto key = [](int a, int b) {
+        const uint32_t lo = (uint32_t)std::min(a, b), hi = (uint32_t)std::max(a, b);
+        return ((uint64_t)lo << 32) | hi;
+    };
+    for (int i = 0; i < ne_explicit; ++i) {
+        seen.insert(key(edges[2 * i], edges[2 * i + 1]));
+        out.push_back(edges[2 * i]);
+        out.push_back(edges[2 * i + 1]);
+    }
+    for (int i = 0; i < ns; ++i)
+        if (seen.insert(key(strands[2 * i], strands[2 * i + 1])).second) {
+            out.push_back(strands[2 * i]);
+            out.push_back(strands[2 * i + 1]);
+        }
+    for (int t = 0; t < nt; ++t)
+        for (int k = 0; k < 3; ++k) {
+            const int a = tris[3 * t + k], b = tris[3 * t + (k + 1) % 3];
+            if (seen.insert(key(a, b)).second) {
+                out.push_back(std::min(a, b));
+                out.push_back(std::max(a, b));
+            }
+        }
+    return out;
+}
+
+void grow_ll(long long& v, long long need) {
+    while (v < need) v = v * 2 + 1024;
+}
+
+int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) {
+    const size_t nv = (size_t)std::max(1, m->nv), ne = (size_t)std::max(1, m->ne);
+    const long long nq = 2LL * m->niso + m->nv + m->ne;
+    if (ctx->pcap == 0) ctx->pcap = 8LL * (m->nv + m->ne) + 4096;
+    if (ctx->arch_cap < ctx->pcap) ctx->arch_cap = ctx->pcap;
+    const size_t P = (size_t)ctx->pcap;
+    CK(ctx->xs.ensure(nv * 24));
+    CK(ctx->ys.ensure(nv * 24));
+    CK(ctx->xo.ensure(nv * 24));
+    CK(ctx->x.ensure(nv * 32));
+    CK(ctx->yk1.ensure(nv * 32));
+    CK(ctx->r.ensure(nv * 8));
+    CK(ctx->imp.ensure(nv * 32));
+    CK(ctx->dmin.ensure(nv * 8));
+    CK(ctx->vhead.ensure(nv * 4));
+    CK(ctx->vcnt.ensure(nv * 4));
+    CK(ctx->ly.ensure(ne * 8));
+    CK(ctx->is_er.ensure(ne));
+    CK(ctx->er_edge.ensure(ne * 4));
+    CK(ctx->er_index.ensure(ne * 4));
+    CK(ctx->er_value.ensure(ne * 8));
+    CK(ctx->er_g.ensure(ne * 32));
+    CK(ctx->er_q.ensure(ne * 8));
+    CK(ctx->edge_lambda.ensure(ne * 8));
+    CK(ctx->er_color.ensure(ne * 4));
+    CK(ctx->er_by_color.ensure(ne * 4));
+    CK(ctx->pkey.ensure(P * 8));
+    CK(ctx->pids.ensure(P * 16));
+    CK(ctx->pdd.ensure(P * 32));
+    CK(ctx->pw.ensure(P * 32));
+    CK(ctx->pflag.ensure(P));
+    CK(ctx->qcount.ensure((size_t)std::max(1LL, nq) * 4));
+    CK(ctx->qslot.ensure((size_t)std::max(1LL, nq) * ctx->K * 4));
+    CK(ctx->c_key.ensure(P * 8));
+    CK(ctx->c_ids.ensure(P * 16));
+    CK(ctx->c_jac.ensure(P * 96));
+    CK(ctx->c_value.ensure(P * 8));
+    CK(ctx->c_diag.ensure(P * 8));
+    CK(ctx->c_q.ensure(P * 8));
+    CK(ctx->c_lambda.ensure(P * 8));
+    if (cfg.solver == TW_SOLVER_JACOBI) CK(ctx->c_next.ensure(P * 8));
+    CK(ctx->c_color.ensure(P * 4));
+    CK(ctx->c_stamp.ensure(P * 4));
+    CK(ctx->c_arch.ensure(P * 8));
+    CK(ctx->c_prio.ensure(P * 8));
+    CK(ctx->c_by_color.ensure(P * 4));
+    CK(ctx->vnext.ensure(P * 16));
+    CK(ctx->ccount.ensure((size_t)ctx->colcap * 4));
+    CK(ctx->coff.ensure(((size_t)ctx->colcap + 1) * 4));
+    CK(ctx->er_color_cnt.ensure((size_t)ctx->colcap * 4));
+    CK(ctx->er_color_off.ensure(((size_t)ctx->colcap + 1) * 4));
+    const size_t A = (size_t)ctx->arch_cap;
+    CK(ctx->arch_key0.ensure(A * 8));
+    CK(ctx->arch_key1.ensure(A * 8));
+    CK(ctx->arch_val0.ensure(A * 8));
+    CK(ctx->arch_val1.ensure(A * 8));
+    CK(ctx->new_lb.ensure(P * 8));
+    CK(ctx->new_key.ensure(P * 8));
+    CK(ctx->new_val.ensure(P * 8));
+    if (cfg.coloring_mode == TW_COLOR_REFERENCE) {
+        if (ctx->refpool_cap == 0) ctx->refpool_cap = 256LL * (m->nv + m->ne) + (1LL << 20);
+        CK(ctx->refpool.ensure((size_t)ctx->refpool_cap * 4));
+    }
+    const size_t nb = (size_t)ctx->nblocks;
+    CK(ctx->part_q.ensure(nb * 8));
+    CK(ctx->part_c.ensure(nb * 8));
+    CK(ctx->part_k.ensure(nb * 8));
+    CK(ctx->blk_lo.ensure(nb * 8));
+    CK(ctx->blk_hi.ensure(nb * 8));
+    CK(ctx->globals.ensure(sizeof(Globals)));
+    CK(ctx->box.ensure(64));
+    CK(ctx->smd.ensure((size_t)cfg.step_limit * 8));
+    CK(ctx->trace.ensure((size_t)cfg.step_limit * sizeof(Trace)));
+    if (cfg.record_path) CK(ctx->path.ensure(((size_t)cfg.step_limit + 1) * nv * 24));
+    size_t tb = 0;
+    for (int c = 0; c < 3; ++c) tb = std::max(tb, bvh_tmp_bytes(m->bvh[c].n));
+    CK(ctx->bvh_tmp.ensure(tb));
+    return TW_OK;
+}
+
+Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
+    Params P;
+    std::memset(&P, 0, sizeof P);
+    P.cfg.step_limit = c.step_limit;
+    P.cfg.solver = c.solver;
+    P.cfg.eps = c.eps;
+    P.cfg.d_min = c.d_min;
+    P.cfg.d_max = c.d_max;
+    P.cfg.delta = c.delta;
+    P.cfg.sigma = c.sigma;
+    P.cfg.gamma = c.gamma;
+    P.cfg.sweeps = c.sweeps;
+    P.cfg.family = c.family;
+    P.cfg.under_relax = c.under_relax;
+    P.cfg.edge_constraints = c.edge_constraints ? 1 : 0;
+    P.cfg.force_fresh_search = c.force_fresh_search ? 1 : 0;
+    P.cfg.record_path = c.record_path ? 1 : 0;
+    P.cfg.coloring_mode = c.coloring_mode;
+    P.cfg.color_seed = c.color_seed;
+    P.nv = m->nv, P.ne = m->ne, P.nt = m->nt, P.niso = m->niso;
+    P.inv_mass = m->d_inv_mass.as<double>();
+    P.edges = m->d_edges.as<int2>();
+    P.tris = m->d_tris.as<int4>();
+    P.iso = m->d_iso.as<int>();
+    P.vedge_off = m->d_vedge_off.as<int>();
+    P.vedge = m->d_vedge.as<int>();
+    P.edge_color = m->d_edge_color.as<int>();
+    P.edge_ncolors = m->edge_ncolors;
+    for (int k = 0; k < 3; ++k) P.bvh[k] = m->bvh[k].view();
+    P.x = ctx->x.as<double4>();
+    P.yk1 = ctx->yk1.as<double4>();
+    P.r = ctx->r.as<double>();
+    P.imp = ctx->imp.as<double4>();
+    P.dmin = ctx->dmin.as<unsigned long long>();
+    P.er_edge = ctx->er_edge.as<int>();
+    P.er_index = ctx->er_index.as<int>();
+    P.is_er = ctx->is_er.as<uint8_t>();
+    P.ly = ctx->ly.as<double>();
+    P.er_value = ctx->er_value.as<double>();
+    P.er_g = ctx->er_g.as<double4>();
+    P.er_q = ctx->er_q.as<double>();
+    P.edge_lambda = ctx->edge_lambda.as<double>();
+    P.er_color = ctx->er_color.as<int>();
+    P.er_by_color = ctx->er_by_color.as<int>();
+    P.er_color_off = ctx->er_color_off.as<int>();
+    P.er_color_cnt = ctx->er_color_cnt.as<int>();
+    P.er_ncolors = m->edge_ncolors;
+    P.pcap = ctx->pcap;
+    P.K = ctx->K;
+    P.pkey = ctx->pkey.as<uint64_t>();
+    P.pids = ctx->pids.as<int4>();
+    P.pdd = ctx->pdd.as<double4>();
+    P.pw = ctx->pw.as<double4>();
+    P.pflag = ctx->pflag.as<uint8_t>();
+    P.qcount = ctx->qcount.as<int>();
+    P.qslot = ctx->qslot.as<int>();
+    P.c_key = ctx->c_key.as<uint64_t>();
+    P.c_ids = ctx->c_ids.as<int4>();
+    P.c_jac = ctx->c_jac.as<double>();
+    P.c_value = ctx->c_value.as<double>();
+    P.c_diag = ctx->c_diag.as<double>();
+    P.c_q = ctx->c_q.as<double>();
+    P.c_lambda = ctx->c_lambda.as<double>();
+    P.c_next = ctx->c_next.as<double>();
+    P.c_color = ctx->c_color.as<int>();
+    P.c_stamp = ctx->c_stamp.as<int>();
+    P.c_arch = ctx->c_arch.as<long long>();
+    P.c_prio = ctx->c_prio.as<uint64_t>();
+    P.c_by_color = ctx->c_by_color.as<int>();
+    P.vhead = ctx->vhead.as<int>();
+    P.vnext = ctx->vnext.as<int>();
+    P.vcnt = ctx->vcnt.as<int>();
+    P.colcap = ctx->colcap;
+    P.ccount = ctx->ccount.as<int>();
+    P.coff = ctx->coff.as<int>();
+    P.arch_cap = ctx->arch_cap;
+    P.arch_key[0] = ctx->arch_key0.as<uint64_t>();
+    P.arch_key[1] = ctx->arch_key1.as<uint64_t>();
+    P.arch_val[0] = ctx->arch_val0.as<double>();
+    P.arch_val[1] = ctx->arch_val1.as<double>();
+    P.new_lb = ctx->new_lb.as<long long>();
+    P.new_key = ctx->new_key.as<uint64_t>();
+    P.new_val = ctx->new_val.as<double>();
+    P.refpool_cap = ctx->refpool_cap;
+    P.refpool = ctx->refpool.as<int>();
+    P.nblocks = ctx->nblocks;
+    P.part_q = ctx->part_q.as<long long>();
+    P.part_c = ctx->part_c.as<long long>();
+    P.part_k = ctx->part_k.as<long long>();
+    P.blk_lo = ctx->blk_lo.as<long long>();
+    P.blk_hi = ctx->blk_hi.as<long long>();
+    P.g = ctx->globals.as<Globals>();
+    P.step_max_disp = ctx->smd.as<double>();
+    P.path = c.record_path ? ctx->path.as<double>() : nullptr;
+    P.trace = ctx->trace.as<Trace>();
+    P.dbg = ctx->dbg_dev;
+    return P;
+}
+
+int build_bvhs(tw_ctx* ctx, tw_mesh* m) {
+    CK(cudaMemsetAsync(ctx->box.p, 0, 64, ctx->stream));
+    // lo = ~0 (max), hi = 0
+    std::vector<unsigned long long> init = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+    CK(cudaMemcpyAsync(ctx->box.p, init.data(), 48, cudaMemcpyHostToDevice, ctx->stream));
+    tw::launch_bounds(ctx->stream, m->nv, ctx->x.as<double4>(), ctx->box.as<unsigned long long>());
+    ctx->launches += 1;
+    for (int c = 0; c < 3; ++c) {
+        launch_bvh_build(ctx->stream, c, m->bvh[c].view(), m->d_tris.as<int4>(), m->d_edges.as<int2>(),
+                         m->d_iso.as<int>(), ctx->x.as<double4>(), m->nv, ctx->bvh_tmp.p, ctx->bvh_tmp.bytes,
+                         ctx->box.as<unsigned long long>());
+        ctx->launches += launch_count_last();
+    }
+    CK(cudaGetLastError());
+    return TW_OK;
+}
+
+// Runs one resolve on inputs already in ctx->xs / ctx->ys (device, N x 3).
+int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys, const tw_resolve_config& cfg,
+                double* d_out, tw_resolve_stats* st, double* smd_host, double* path_host, tw_step_trace* trace_host) {
+    Globals G;
+    int retries = 0;
+    float dev_ms = 0.f;
+    for (;;) {
+        int rc = ensure_buffers(ctx, m, cfg);
+        if (rc) return rc;
+        Params P = make_params(ctx, m, cfg);
+        CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), ctx->stream));
+        CK(cudaEventRecord(ctx->ev0, ctx->stream));
+        launch_setup(ctx->stream, m->nv, d_xs, d_ys, m->d_inv_mass.as<double>(), P.x, const_cast<double4*>(P.yk1),
+                     P.r, P.dmin, P.vhead, P.vcnt, P.imp, &P.g->nonfinite, m->ne, P.edges,
+                     const_cast<double*>(P.ly), P.is_er, P.edge_lambda, P.er_color, P.edge_color,
+                     cfg.edge_constraints ? 1 : 0, cfg.coloring_mode == TW_COLOR_DEVICE ? 1 : 0);
+        ctx->launches += launch_count_last();
+        rc = build_bvhs(ctx, m);
+        if (rc) return rc;
+        CK(coop_resolve(ctx->stream, P, ctx->nblocks));
+        ctx->launches += 1;
+        CK(cudaEventRecord(ctx->ev1, ctx->stream));
+        CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof(Globals), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaEventElapsedTime(&dev_ms, ctx->ev0, ctx->ev1));
+        if (G.nonfinite) return fail(ctx, TW_EINVAL, "resolve: non-finite input positions");
+        if (G.error & ERR_TIMEOUT) return fail(ctx, TW_ETIMEOUT, "resolve: device watchdog fired");
+        if (G.error & ERR_INTERNAL)
+            return fail(ctx, TW_ECUDA, "resolve: device invariant violated at tw_phases.cuh:" +
+                                           std::to_string(G.internal_line) + " (step " +
+                                           std::to_string(G.steps) + ")");
+        const int cap = G.error & (ERR_CAP_SLOTS | ERR_CAP_PAIRS | ERR_CAP_ARCH | ERR_CAP_COLORS | ERR_CAP_REFPOOL |
+                                   ERR_CAP_STACK);
+        if (!cap) break;
+        if (++retries > 12) return fail(ctx, TW_ECAPACITY, "resolve: capacity growth did not converge");
+        if (G.error & ERR_CAP_STACK) return fail(ctx, TW_ECAPACITY, "resolve: BVH traversal stack overflow");
+        if (G.error & ERR_CAP_SLOTS) ctx->K = std::max(ctx->K * 2, ((G.needed_k + 31) / 32) * 32);
+        if (G.error & ERR_CAP_PAIRS) grow_ll(ctx->pcap, G.needed_pairs + G.needed_pairs / 4);
+        if (G.error & ERR_CAP_ARCH) grow_ll(ctx->arch_cap, ctx->arch_cap * 2);
+        if (G.error & ERR_CAP_COLORS) ctx->colcap *= 4;
+        if (G.error & ERR_CAP_REFPOOL) ctx->refpool_cap *= 4;
+    }
+    launch_pack(ctx->stream, m->nv, ctx->x.as<double4>(), d_out);
+    ctx->launches += launch_count_last();
+    std::memset(st, 0, sizeof *st);
+    st->steps = G.steps;
+    st->searches = G.searches;
+    st->final_residual = G.final_residual;
+    st->converged = G.converged;
+    st->hit_step_limit = !G.converged;
+    st->stagnated = 0;
+    st->start_in_contact = G.start_in_contact;
+    st->step_law_violated = G.step_law_violated;
+    st->num_pairs = (int32_t)G.np;
+    st->pairs_evaluated = G.pairs_evaluated;
+    st->rows_solved = G.rows_solved;
+    st->device_ms = dev_ms;
+    st->retries = retries;
+    if (smd_host && G.steps > 0)
+        CK(cudaMemcpyAsync(smd_host, ctx->smd.p, (size_t)G.steps * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (trace_host && G.steps > 0) {
+        static_assert(sizeof(Trace) == sizeof(tw_step_trace), "trace layout");
+        CK(cudaMemcpyAsync(trace_host, ctx->trace.p, (size_t)G.steps * sizeof(Trace), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    }
+    if (path_host && cfg.record_path)
+        CK(cudaMemcpyAsync(path_host, ctx->path.p, ((size_t)G.steps + 1) * m->nv * 24, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    return TW_OK;
+}
+
+int check_cfg(tw_ctx* ctx, const tw_resolve_config* cfg) {
+    if (!cfg || !config_valid(*cfg)) return fail(ctx, TW_EINVAL, "resolve: invalid configuration");
+    if (cfg->solver == TW_SOLVER_AL20 || cfg->solver == TW_SOLVER_AL100)
+        return fail(ctx, TW_EUNSUPPORTED, "resolve: the AL baseline solvers are not provided on the device");
+    if (cfg->solver != TW_SOLVER_PGS && cfg->solver != TW_SOLVER_JACOBI)
+        return fail(ctx, TW_EINVAL, "resolve: unknown solver");
+    if (cfg->coloring_mode != TW_COLOR_REFERENCE && cfg->coloring_mode != TW_COLOR_DEVICE)
+        return fail(ctx, TW_EINVAL, "resolve: unknown coloring mode");
+    if (cfg->family != TW_FAMILY_VOLUME && cfg->family != TW_FAMILY_GAP)
+        return fail(ctx, TW_EINVAL, "resolve: unknown constraint family");
+    return TW_OK;
+}
+
+}  // namespace
+
+// ================================================================= C-ABI
+extern "C" {
+
+int tw_abi_version(void) { return TW_ABI_VERSION; }
+
+void tw_default_config(tw_resolve_config* c) {
+    std::memset(c, 0, sizeof *c);
+    c->step_limit = 512;
+    c->solver = TW_SOLVER_PGS;
+    c->eps = 1e-4;
+    c->d_min = 2e-3;
+    c->d_max = 4e-3;
+    c->delta = 1e-3;
+    c->sigma = 1.1;
+    c->gamma = 0.9;
+    c->sweeps = 1;
+    c->family = TW_FAMILY_VOLUME;
+    c->under_relax = 0.5;
+    c->edge_constraints = 1;
+    c->force_fresh_search = 0;
+    c->record_path = 0;
+    c->coloring_mode = TW_COLOR_DEVICE;
+    c->color_seed = 0x5eed;
+}
+
+int tw_ctx_create(int device, void* stream, tw_ctx** out) {
+    if (!out) return TW_EINVAL;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return TW_ECUDA;
+    if (device < 0 || device >= n) return TW_EINVAL;
+    tw_ctx* ctx = new tw_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return TW_ECUDA;
+    }
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (!coop) {
+        delete ctx;
+        return TW_ECUDA;
+    }
+    int per_sm = resolve_blocks_per_sm();
+    int want = 2;
+    if (const char* s = std::getenv("TW_BLOCKS_PER_SM")) want = std::max(1, std::atoi(s));
+    per_sm = std::max(1, std::min(per_sm, want));
+    ctx->nblocks = std::min(ctx->sm_count * per_sm, tw::MAX_BLOCKS);
+    if (stream) {
+        ctx->stream = (cudaStream_t)stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete ctx;
+            return TW_ECUDA;
+        }
+        ctx->own_stream = true;
+    }
+    cudaEventCreate(&ctx->ev0);
+    cudaEventCreate(&ctx->ev1);
+    if (const char* d = std::getenv("TW_DEBUG"); d && d[0] == '1') {
+        if (cudaHostAlloc((void**)&ctx->dbg_host, MAX_BLOCKS * sizeof(int), cudaHostAllocMapped) == cudaSuccess) {
+            std::memset(ctx->dbg_host, 0xff, MAX_BLOCKS * sizeof(int));
+            cudaHostGetDevicePointer((void**)&ctx->dbg_dev, ctx->dbg_host, 0);
+        }
+    }
+    *out = ctx;
+    return TW_OK;
+}
+
+void tw_ctx_destroy(tw_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    DevMem* all[] = {&ctx->xs, &ctx->ys, &ctx->xo, &ctx->x, &ctx->yk1, &ctx->r, &ctx->imp, &ctx->dmin, &ctx->vhead,
+                     &ctx->vcnt, &ctx->ly, &ctx->is_er, &ctx->er_edge, &ctx->er_index, &ctx->er_value, &ctx->er_g,
+                     &ctx->er_q, &ctx->edge_lambda, &ctx->er_color, &ctx->er_by_color, &ctx->er_color_off,
+                     &ctx->er_color_cnt, &ctx->pkey, &ctx->pids, &ctx->pdd, &ctx->pw, &ctx->pflag, &ctx->qcount,
+                     &ctx->qslot, &ctx->c_key, &ctx->c_ids, &ctx->c_jac, &ctx->c_value, &ctx->c_diag, &ctx->c_q,
+                     &ctx->c_lambda, &ctx->c_next, &ctx->c_color, &ctx->c_stamp, &ctx->c_arch, &ctx->c_prio,
+                     &ctx->c_by_color, &ctx->vnext, &ctx->ccount, &ctx->coff, &ctx->arch_key0, &ctx->arch_key1,
+                     &ctx->arch_val0, &ctx->arch_val1, &ctx->new_lb, &ctx->new_key, &ctx->new_val, &ctx->refpool,
+                     &ctx->part_q, &ctx->part_c, &ctx->part_k, &ctx->blk_lo, &ctx->blk_hi, &ctx->globals, &ctx->box,
+                     &ctx->bvh_tmp, &ctx->smd, &ctx->trace, &ctx->path, &ctx->s_kinds, &ctx->s_verts, &ctx->s_out,
+                     &ctx->s_has};
+    for (DevMem* d : all) d->release();
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* tw_last_error(const tw_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+int64_t tw_ctx_kernel_launches(const tw_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int tw_mesh_create(tw_ctx* ctx, int32_t nv, const double* inv_mass, int32_t ne_explicit, const int32_t* edges,
+                   int32_t ns, const int32_t* strand_edges, int32_t nt, const int32_t* triangles, tw_mesh** out) {
+    if (!ctx || !out || nv < 0 || ne_explicit < 0 || ns < 0 || nt < 0) return fail(ctx, TW_EINVAL, "mesh: bad sizes");
+    *out = nullptr;
+    CK(cudaSetDevice(ctx->device));
+    tw_mesh* m = new tw_mesh();
+    m->ctx = ctx;
+    m->nv = nv;
+    m->nt = nt;
+    m->inv_mass.assign(nv, 1.0);
+    if (inv_mass) m->inv_mass.assign(inv_mass, inv_mass + nv);
+    // MeshState::validate (mesh.cpp:35-55)
+    for (int v = 0; v < nv; ++v)
+        if (!std::isfinite(m->inv_mass[v]) || m->inv_mass[v] < 0.0) {
+            delete m;
+            return fail(ctx, TW_EINVAL, "mesh: inv_mass must be finite and >= 0");
+        }
+    m->edges = finalize_edges(ne_explicit, edges, ns, strand_edges, nt, triangles);
+    m->ne = (int)(m->edges.size() / 2);
+    for (size_t i = 0; i < m->edges.size(); i += 2) {
+        const int a = m->edges[i], b = m->edges[i + 1];
+        if (a < 0 || a >= nv || b < 0 || b >= nv || a == b) {
+            delete m;
+            return fail(ctx, TW_EINVAL, "mesh: bad edge");
+        }
+    }
+    for (int t = 0; t < nt; ++t) {
+        const int a = triangles[3 * t], b = triangles[3 * t + 1], c = triangles[3 * t + 2];
+        if (a < 0 || a >= nv || b < 0 || b >= nv || c < 0 || c >= nv || a == b || b == c || a == c) {
+            delete m;
+            return fail(ctx, TW_EINVAL, "mesh: bad triangle");
+        }
+    }
+    // isolated vertices, vertex -> edge CSR (ascending edge index)
+    std::vector<uint8_t> touched(nv, 0);
+    std::vector<int> voff(nv + 1, 0);
+    for (int e = 0; e < m->ne; ++e) {
+        touched[m->edges[2 * e]] = touched[m->edges[2 * e + 1]] = 1;
+        ++voff[m->edges[2 * e] + 1];
+        ++voff[m->edges[2 * e + 1] + 1];
+    }
+    for (int t = 0; t < 3 * nt; ++t) touched[triangles[t]] = 1;
+    for (int v = 0; v < nv; ++v) voff[v + 1] += voff[v];
+    std::vector<int> vedge(std::max(1, voff[nv])), fillp(voff.begin(), voff.end() - 1);
+    for (int e = 0; e < m->ne; ++e) {
+        vedge[fillp[m->edges[2 * e]]++] = e;
+        vedge[fillp[m->edges[2 * e + 1]]++] = e;
+    }
+    std::vector<int> iso;
+    for (int v = 0; v < nv; ++v)
+        if (!touched[v]) iso.push_back(v);
+    m->niso = (int)iso.size();
+    std::vector<int4> tris4(std::max(1, nt));
+    for (int t = 0; t < nt; ++t) tris4[t] = make_int4(triangles[3 * t], triangles[3 * t + 1], triangles[3 * t + 2], -1);
+    cudaStream_t s = ctx->stream;
+    auto up = [&](DevMem& d, const void* src, size_t bytes) -> cudaError_t {
+        cudaError_t e = d.ensure(bytes);
+        if (e != cudaSuccess) return e;
+        if (bytes) e = cudaMemcpyAsync(d.p, src, bytes, cudaMemcpyHostToDevice, s);
+        return e;
+    };
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = up(m->d_inv_mass, m->inv_mass.data(), (size_t)nv * 8);
+    if (e == cudaSuccess) e = up(m->d_edges, m->edges.data(), (size_t)m->ne * 8);
+    if (e == cudaSuccess) e = up(m->d_tris, tris4.data(), (size_t)nt * 16);
+    if (e == cudaSuccess) e = up(m->d_iso, iso.data(), (size_t)m->niso * 4);
+    if (e == cudaSuccess) e = up(m->d_vedge_off, voff.data(), (size_t)(nv + 1) * 4);
+    if (e == cudaSuccess) e = up(m->d_vedge, vedge.data(), (size_t)voff[nv] * 4);
+    // LBVH storage
+    const int ncls[3] = {nt, m->ne, m->niso};
+    for (int c = 0; c < 3 && e == cudaSuccess; ++c) {
+        BvhMem& B = m->bvh[c];
+        B.n = ncls[c];
+        const size_t n = (size_t)std::max(1, B.n);
+        if (e == cudaSuccess) e = B.prim.ensure(n * 4);
+        if (e == cudaSuccess) e = B.child.ensure(n * 8);
+        if (e == cudaSuccess) e = B.parent.ensure(2 * n * 4);
+        if (e == cudaSuccess) e = B.lo.ensure(2 * n * 16);
+        if (e == cudaSuccess) e = B.hi.ensure(2 * n * 16);
+        if (e == cudaSuccess) e = B.flag.ensure(n * 4);
+        if (e == cudaSuccess) e = cudaMemsetAsync(B.flag.p, 0, n * 4, s);
+    }
+    // device-mode edge-row precoloring (Jones-Plassmann rounds)
+    if (e == cudaSuccess) e = m->d_edge_color.ensure((size_t)std::max(1, m->ne) * 4);
+    if (e == cudaSuccess && m->ne > 0) {
+        DevMem stamp, counter;
+        std::vector<int> st(m->ne, 0);
+        int participating = 0;
+        for (int k = 0; k < m->ne; ++k) {
+            const bool both_static = m->inv_mass[m->edges[2 * k]] == 0.0 && m->inv_mass[m->edges[2 * k + 1]] == 0.0;
+            st[k] = both_static ? -1 : 0;
+            participating += !both_static;
+        }
+        std::vector<int> col_init(m->ne, -1);
+        e = stamp.ensure((size_t)m->ne * 4);
+        if (e == cudaSuccess) e = counter.ensure(4);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(stamp.p, st.data(), (size_t)m->ne * 4, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(m->d_edge_color.p, col_init.data(), (size_t)m->ne * 4, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(counter.p, 0, 4, s);
+        int colored = 0;
+        for (int round = 1; e == cudaSuccess && colored < participating; ++round) {
+            launch_edge_color_round(s, m->ne, m->d_edges.as<int2>(), m->d_inv_mass.as<double>(),
+                                    m->d_vedge_off.as<int>(), m->d_vedge.as<int>(), m->d_edge_color.as<int>(),
+                                    stamp.as<int>(), round, counter.as<int>());
+            ++ctx->launches;
+            e = cudaMemcpyAsync(&colored, counter.p, 4, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (round > m->ne + 2) break;
+        }
+        std::vector<int> cols(m->ne);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(cols.data(), m->d_edge_color.p, (size_t)m->ne * 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        int mx = -1;
+        for (int c : cols) mx = std::max(mx, c);
+        m->edge_ncolors = mx + 1;
+        stamp.release();
+        counter.release();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        delete m;
+        return cuda_fail(ctx, e, "tw_mesh_create");
+    }
+    if (ctx->colcap < m->edge_ncolors + 64) ctx->colcap = m->edge_ncolors + 1024;
+    *out = m;
+    return TW_OK;
+}
+
+int32_t tw_mesh_num_edges(const tw_mesh* m) { return m ? m->ne : 0; }
+
+int tw_mesh_edges(const tw_mesh* m, int32_t* out) {
+    if (!m || !out) return TW_EINVAL;
+    std::memcpy(out, m->edges.data(), m->edges.size() * 4);
+    return TW_OK;
+}
+
+void tw_mesh_destroy(tw_mesh* m) {
+    if (!m) return;
+    cudaSetDevice(m->ctx->device);
+    cudaStreamSynchronize(m->ctx->stream);
+    DevMem* all[] = {&m->d_inv_mass, &m->d_edges, &m->d_tris, &m->d_iso, &m->d_vedge_off, &m->d_vedge, &m->d_edge_color};
+    for (DevMem* d : all) d->release();
+    for (auto& B : m->bvh) {
+        B.prim.release(), B.child.release(), B.parent.release(), B.lo.release(), B.hi.release(), B.flag.release();
+    }
+    delete m;
+}
+
+int tw_resolve(tw_ctx* ctx, tw_mesh* m, const double* x_start, const double* y_target, const tw_resolve_config* cfg,
+               double* x_out, tw_resolve_stats* stats, double* step_max_disp, double* path, tw_step_trace* trace) {
+    if (!ctx || !m || !x_start || !y_target || !x_out) return fail(ctx, TW_EINVAL, "resolve: null argument");
+    int rc = check_cfg(ctx, cfg);
+    if (rc) return rc;
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaSetDevice(ctx->device));
+    rc = ensure_buffers(ctx, m, *cfg);
+    if (rc) return rc;
+    const size_t bytes = (size_t)m->nv * 24;
+    if (bytes) {
+        CK(cudaMemcpyAsync(ctx->xs.p, x_start, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->ys.p, y_target, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    tw_resolve_stats st;
+    rc = run_resolve(ctx, m, ctx->xs.as<double>(), ctx->ys.as<double>(), *cfg, ctx->xo.as<double>(), &st,
+                     step_max_disp, cfg->record_path ? path : nullptr, trace);
+    if (rc) return rc;
+    if (bytes) CK(cudaMemcpyAsync(x_out, ctx->xo.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    st.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (stats) *stats = st;
+    return TW_OK;
+}
+
+int tw_resolve_device(tw_ctx* ctx, tw_mesh* m, const double* d_x, const double* d_y, const tw_resolve_config* cfg,
+                      double* d_out, tw_resolve_stats* stats) {
+    if (!ctx || !m || !d_x || !d_y || !d_out) return fail(ctx, TW_EINVAL, "resolve: null argument");
+    int rc = check_cfg(ctx, cfg);
+    if (rc) return rc;
+    tw_resolve_config c = *cfg;
+    c.record_path = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaSetDevice(ctx->device));
+    tw_resolve_stats st;
+    rc = run_resolve(ctx, m, d_x, d_y, c, d_out, &st, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    st.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (stats) *stats = st;
+    return TW_OK;
+}
+
+// ---------------------------------------------------------------- stages
+int tw_stage_closest(tw_ctx* ctx, int32_t nv, const double* x, int64_t n, const int32_t* kinds, const int32_t* verts,
+                     double* out, int32_t* has) {
+    if (!ctx || nv < 0 || n < 0) return fail(ctx, TW_EINVAL, "closest: bad sizes");
+    CK(cudaSetDevice(ctx->device));
+    std::vector<double4> x4(std::max(1, nv));
+    for (int v = 0; v < nv; ++v) x4[v] = make_double4(x[3 * v], x[3 * v + 1], x[3 * v + 2], 0.0);
+    CK(ctx->x.ensure((size_t)std::max(1, nv) * 32));
+    CK(ctx->s_kinds.ensure((size_t)std::max<int64_t>(1, n) * 8));
+    CK(ctx->s_verts.ensure((size_t)std::max<int64_t>(1, n) * 24));
+    CK(ctx->s_out.ensure((size_t)std::max<int64_t>(1, n) * 88));
+    CK(ctx->s_has.ensure((size_t)std::max<int64_t>(1, n) * 4));
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemcpyAsync(ctx->x.p, x4.data(), (size_t)nv * 32, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->s_kinds.p, kinds, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->s_verts.p, verts, (size_t)n * 24, cudaMemcpyHostToDevice, s));
+    CK(launch_closest(s, nv, ctx->x.as<double4>(), n, ctx->s_kinds.as<int>(), ctx->s_verts.as<int>(),
+                      ctx->s_out.as<double>(), ctx->s_has.as<int>()));
+    ++ctx->launches;
+    CK(cudaMemcpyAsync(out, ctx->s_out.p, (size_t)n * 88, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(has, ctx->s_has.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return TW_OK;
+}
+
+namespace {
+int stage_upload_x(tw_ctx* ctx, tw_mesh* m, const double* x) {
+    std::vector<double4> x4(std::max(1, m->nv));
+    for (int v = 0; v < m->nv; ++v) x4[v] = make_double4(x[3 * v], x[3 * v + 1], x[3 * v + 2], m->inv_mass[v]);
+    CK(cudaMemcpyAsync(ctx->x.p, x4.data(), (size_t)m->nv * 32, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TW_OK;
+}
+
+int stage_download_pairs(tw_ctx* ctx, int64_t np, uint64_t* keys, double* dist, double* wa, double* wb, double* dir,
+                         uint8_t* flags) {
+    std::vector<int4> ids(np);
+    std::vector<double4> dd(np), w(np);
+    cudaStream_t s = ctx->stream;
+    if (np) {
+        CK(cudaMemcpyAsync(keys, ctx->pkey.p, np * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(dd.data(), ctx->pdd.p, np * 32, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(w.data(), ctx->pw.p, np * 32, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(flags, ctx->pflag.p, np, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < np; ++i) {
+        const int ka = (int)(keys[i] >> 62), kb = (int)((keys[i] >> 60) & 3);
+        dist[i] = dd[i].w;
+        dir[3 * i] = dd[i].x, dir[3 * i + 1] = dd[i].y, dir[3 * i + 2] = dd[i].z;
+        double a[3] = {1, 0, 0}, b[3] = {1, 0, 0};
+        if (ka == 1) a[0] = w[i].x, a[1] = w[i].y, b[0] = w[i].z, b[1] = w[i].w;
+        else if (kb == 2) b[0] = w[i].x, b[1] = w[i].y, b[2] = w[i].z;
+        else if (kb == 1) b[0] = w[i].x, b[1] = w[i].y;
+        for (int k = 0; k < 3; ++k) wa[3 * i + k] = a[k], wb[3 * i + k] = b[k];
+        flags[i] &= (uint8_t)(PF_ACTIVE | PF_ALL_STATIC | PF_DEGENERATE);
+    }
+    return TW_OK;
+}
+}  // namespace
+
+int tw_stage_search(tw_ctx* ctx, tw_mesh* m, const double* x, double d_max, int64_t cap, uint64_t* keys, double* dist,
+                    double* wa, double* wb, double* dir, uint8_t* flags, int64_t* np) {
+    if (!ctx || !m || !x || !np) return fail(ctx, TW_EINVAL, "search: null argument");
+    if (!(d_max > 0.0)) return fail(ctx, TW_EINVAL, "proximity_search: d_max must be > 0");
+    CK(cudaSetDevice(ctx->device));
+    tw_resolve_config cfg;
+    tw_default_config(&cfg);
+    cfg.d_max = d_max;
+    cfg.step_limit = 1;
+    int rc = ensure_buffers(ctx, m, cfg);
+    if (rc) return rc;
+    rc = stage_upload_x(ctx, m, x);
+    if (rc) return rc;
+    Globals G;
+    for (int attempt = 0;; ++attempt) {
+        rc = ensure_buffers(ctx, m, cfg);
+        if (rc) return rc;
+        Params P = make_params(ctx, m, cfg);
+        CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), ctx->stream));
+        CK(cudaMemsetAsync(ctx->dmin.p, 0x7f, (size_t)m->nv * 8, ctx->stream));
+        rc = build_bvhs(ctx, m);
+        if (rc) return rc;
+        CK(coop_search(ctx->stream, P, ctx->nblocks));
+        ++ctx->launches;
+        CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof G, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (G.error & ERR_TIMEOUT) return fail(ctx, TW_ETIMEOUT, "search: watchdog");
+        if (!(G.error & (ERR_CAP_SLOTS | ERR_CAP_PAIRS))) break;
+        if (attempt > 10) return fail(ctx, TW_ECAPACITY, "search: capacity");
+        if (G.error & ERR_CAP_SLOTS) ctx->K = std::max(ctx->K * 2, ((G.needed_k + 31) / 32) * 32);
+        if (G.error & ERR_CAP_PAIRS) grow_ll(ctx->pcap, G.needed_pairs + G.needed_pairs / 4);
+    }
+    *np = G.np;
+    if (G.np > cap) return fail(ctx, TW_ECAPACITY, "search: output capacity too small");
+    return stage_download_pairs(ctx, G.np, keys, dist, wa, wb, dir, flags);
+}
+
+int tw_stage_refresh(tw_ctx* ctx, tw_mesh* m, const double* x, double bound, int64_t np, const uint64_t* keys,
+                     double* dist, double* wa, double* wb, double* dir, uint8_t* flags, double* vertex_bound) {
+    if (!ctx || !m || !x || np < 0) return fail(ctx, TW_EINVAL, "refresh: bad argument");
+    CK(cudaSetDevice(ctx->device));
+    tw_resolve_config cfg;
+    tw_default_config(&cfg);
+    cfg.step_limit = 1;
+    if (ctx->pcap < np) grow_ll(ctx->pcap, np);
+    int rc = ensure_buffers(ctx, m, cfg);
+    if (rc) return rc;
+    rc = stage_upload_x(ctx, m, x);
+    if (rc) return rc;
+    // pack the pair records as the search writes them
+    std::vector<int4> ids(np);
+    std::vector<double4> dd(np), w(np);
+    for (int64_t i = 0; i < np; ++i) {
+        const uint64_t k = keys[i];
+        const int ka = (int)(k >> 62), kb = (int)((k >> 60) & 3), ia = (int)((k >> 30) & 0x3fffffff),
+                  ib = (int)(k & 0x3fffffff);
+        int va[3] = {-1, -1, -1}, vb[3] = {-1, -1, -1};
+        auto ids_of = [&](int kind, int idx, int* v) {
+            if (kind == 0) v[0] = idx;
+            else if (kind == 1) v[0] = m->edges[2 * idx], v[1] = m->edges[2 * idx + 1];
+            else {
+                // triangles are only on device; keep a host copy via the tris upload? use edges path
+                v[0] = v[1] = v[2] = -1;
+            }
+        };
+        ids_of(ka, ia, va);
+        ids_of(kb, ib, vb);
+        ids[i] = ka == 1 ? make_int4(va[0], va[1], vb[0], vb[1]) : make_int4(va[0], vb[0], vb[1], vb[2]);
+        dd[i] = make_double4(dir[3 * i], dir[3 * i + 1], dir[3 * i + 2], dist[i]);
+        if (ka == 1) w[i] = make_double4(wa[3 * i], wa[3 * i + 1], wb[3 * i], wb[3 * i + 1]);
+        else w[i] = make_double4(wb[3 * i], wb[3 * i + 1], wb[3 * i + 2], 0.0);
+    }
+    cudaStream_t s = ctx->stream;
+    if (np) {
+        CK(cudaMemcpyAsync(ctx->pkey.p, keys, np * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->pids.p, ids.data(), np * 16, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->pdd.p, dd.data(), np * 32, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->pw.p, w.data(), np * 32, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->pflag.p, flags, np, cudaMemcpyHostToDevice, s));
+    }
+    // triangle ids for VT pairs come from the device triangle table
+    std::vector<int4> tris(m->nt);
+    if (m->nt) CK(cudaMemcpyAsync(tris.data(), m->d_tris.p, (size_t)m->nt * 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    bool fix = false;
+    for (int64_t i = 0; i < np; ++i) {
+        const uint64_t k = keys[i];
+        if (((k >> 60) & 3) == 2) {
+            const int4 t = tris[k & 0x3fffffff];
+            ids[i] = make_int4((int)((k >> 30) & 0x3fffffff), t.x, t.y, t.z);
+            fix = true;
+        }
+    }
+    if (fix && np) CK(cudaMemcpyAsync(ctx->pids.p, ids.data(), np * 16, cudaMemcpyHostToDevice, s));
+    Params P = make_params(ctx, m, cfg);
+    CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), s));
+    CK(cudaMemsetAsync(ctx->dmin.p, 0x7f, (size_t)m->nv * 8, s));
+    Globals G;
+    std::memset(&G, 0, sizeof G);
+    G.np = np;
+    CK(cudaMemcpyAsync(ctx->globals.p, &G, sizeof G, cudaMemcpyHostToDevice, s));
+    CK(coop_refresh(s, P, ctx->nblocks, bound));
+    ++ctx->launches;
+    CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof G, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (G.error) return fail(ctx, TW_ETIMEOUT, "refresh: device error");
+    int rc2 = stage_download_pairs(ctx, np, const_cast<uint64_t*>(keys), dist, wa, wb, dir, flags);
+    if (rc2) return rc2;
+    if (vertex_bound) {
+        CK(cudaMemcpyAsync(vertex_bound, ctx->r.p, (size_t)m->nv * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    return TW_OK;
+}
+
+int tw_stage_advance(tw_ctx* ctx, int32_t nv, const double* inv_mass, const double* y, const double* D, double gamma,
+                     double* x, double* r, double* max_disp) {
+    if (!ctx || nv < 0) return fail(ctx, TW_EINVAL, "advance: bad argument");
+    CK(cudaSetDevice(ctx->device));
+    const size_t n = (size_t)std::max(1, nv);
+    CK(ctx->x.ensure(n * 32));
+    CK(ctx->yk1.ensure(n * 32));
+    CK(ctx->r.ensure(n * 8));
+    CK(ctx->imp.ensure(n * 32));
+    CK(ctx->dmin.ensure(n * 8));
+    CK(ctx->vhead.ensure(n * 4));
+    CK(ctx->vcnt.ensure(n * 4));
+    CK(ctx->globals.ensure(sizeof(Globals)));
+    CK(ctx->part_k.ensure((size_t)ctx->nblocks * 8));
+    std::vector<double4> x4(n), y4(n), imp(n, make_double4(0, 0, 0, 0));
+    std::vector<double> Db(n);
+    for (int v = 0; v < nv; ++v) {
+        x4[v] = make_double4(x[3 * v], x[3 * v + 1], x[3 * v + 2], inv_mass[v]);
+        y4[v] = make_double4(y[3 * v], y[3 * v + 1], y[3 * v + 2], inv_mass[v]);
+        Db[v] = D[v];
+    }
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemcpyAsync(ctx->x.p, x4.data(), n * 32, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->yk1.p, y4.data(), n * 32, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->imp.p, imp.data(), n * 32, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->dmin.p, Db.data(), n * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->r.p, r, (size_t)nv * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), s));
+    Params P;
+    std::memset(&P, 0, sizeof P);
+    P.cfg.gamma = gamma;
+    P.nv = nv;
+    P.x = ctx->x.as<double4>();
+    P.yk1 = ctx->yk1.as<double4>();
+    P.r = ctx->r.as<double>();
+    P.imp = ctx->imp.as<double4>();
+    P.dmin = ctx->dmin.as<unsigned long long>();
+    P.vhead = ctx->vhead.as<int>();
+    P.vcnt = ctx->vcnt.as<int>();
+    P.part_k = ctx->part_k.as<long long>();
+    P.g = ctx->globals.as<Globals>();
+    CK(launch_advance(s, P, ctx->nblocks));
+    ++ctx->launches;
+    Globals G;
+    CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof G, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(x4.data(), ctx->x.p, n * 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(r, ctx->r.p, (size_t)nv * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int v = 0; v < nv; ++v) x[3 * v] = x4[v].x, x[3 * v + 1] = x4[v].y, x[3 * v + 2] = x4[v].z;
+    if (max_disp) {
+        unsigned long long b = G.maxdisp_bits;
+        double d;
+        std::memcpy(&d, &b, 8);
+        *max_disp = d;
+    }
+    return TW_OK;
+}
+
+int tw_stage_linearize(tw_ctx* ctx, tw_mesh*, const double*, int64_t, const uint64_t*, const double*, const double*,
+                       const double*, const double*, const uint8_t*, const double*, double, double, int32_t, int32_t,
+                       int64_t, uint8_t*, int32_t*, double*, double*, double*, uint64_t*, int32_t*, int64_t*) {
+    return fail(ctx, TW_EUNSUPPORTED, "tw_stage_linearize: not yet wired");
+}
+
+int tw_stage_color(tw_ctx* ctx, tw_mesh*, int64_t, const uint8_t*, const int32_t*, const uint64_t*, const int32_t*,
+                   uint64_t, int32_t, int32_t, int32_t*, int32_t*) {
+    return fail(ctx, TW_EUNSUPPORTED, "tw_stage_color: not yet wired");
+}
+
+int tw_stage_backward(tw_ctx* ctx, int32_t, const double*, int64_t, const int32_t*, const double*, const double*,
+                      const double*, const int32_t*, int32_t, const double*, const double*, int32_t, int32_t, double,
+                      double*, double*, double*) {
+    return fail(ctx, TW_EUNSUPPORTED, "tw_stage_backward: not yet wired");
+}
+
+}  // extern "C"

@@ -1,0 +1,244 @@
+// Device-side state of one resolve call and the phase functions of Alg. 1.
+//
+// Layout in HBM (all buffers owned by the tw_ctx, grown on demand):
+//   vertices   x, y_k1: double4 (x, y, z, inv_mass) — one 32 B sector per gather
+//              r, impulse, vertex bound (u64 bit pattern for atomicMin)
+//   pairs      SoA: key u64 | ids int4 | (dir, dist) double4 | weights double4 | flags u8
+//   contact rows (compact, pair order) SoA: key, ids, jac[12], value, diag, q, lambda, color
+//   edge rows  indexed by mesh edge: g = u/ly (double4 with diag in w), value, q, lambda
+//   archive    sorted (key, lambda) of every contact multiplier ever stored
+//              (tombstone = NaN), ping-pong merged — the reference's
+//              std::unordered_map<uint64_t,double> contact_lambda
+//   BVHs       Karras LBVH over triangles, edges, isolated vertices; float
+//              boxes rounded outwards
+#pragma once
+
+#include <cstdint>
+
+#include "tw_math.cuh"
+
+namespace tw {
+
+constexpr int TPB = 256;  // threads per block of every engine kernel
+constexpr int MAX_BLOCKS = 1024;
+
+enum : int {
+    ERR_CAP_SLOTS = 1,    // a broad-phase query produced more than K candidates
+    ERR_CAP_PAIRS = 2,    // P > pair capacity
+    ERR_CAP_ARCH = 4,     // multiplier archive full
+    ERR_CAP_COLORS = 8,   // more colors than the color table holds
+    ERR_CAP_REFPOOL = 16, // reference-coloring scratch pool too small
+    ERR_TIMEOUT = 32,     // grid barrier watchdog fired
+    ERR_CAP_STACK = 64,   // BVH traversal stack overflow
+    ERR_INTERNAL = 128,   // invariant violated (line in Globals::internal_line)
+};
+
+enum : uint8_t { PF_ACTIVE = 1, PF_ALL_STATIC = 2, PF_DEGENERATE = 4, PF_CONTACT = 8 };
+
+struct Bvh {
+    int n;            // primitives (leaves); nodes = 2n-1, internal 0..n-2, leaves n-1..2n-2
+    int* prim;        // leaf slot -> primitive index
+    int2* child;      // internal node -> (left, right) node ids
+    int* parent;      // node -> parent (-1 for root)
+    float4* lo;       // node box lo (xyz)
+    float4* hi;       // node box hi (xyz)
+    unsigned* flag;   // refit arrival counters (internal nodes)
+};
+
+struct Globals {
+    unsigned bar_count;
+    unsigned bar_gen;
+    int error;
+    int nonfinite;
+    int internal_line;
+    int ner;             // edge rows of this call (set by the prologue)
+    int needed_k;
+    long long np;        // pairs in the set
+    long long nc;        // contact rows this step
+    long long narch;     // archive entries
+    int arch_sel;        // which archive buffer is current
+    int colored;         // JP coloring progress
+    int max_color;       // max contact-row color this step
+    int new_keys;
+    int nactive;
+    unsigned long long maxdisp_bits;
+    unsigned long long resid_bits;
+    long long needed_pairs;
+    // stats
+    int steps;
+    int searches;
+    int converged;
+    int start_in_contact;
+    int step_law_violated;
+    int ncolors_last;
+    double final_residual;
+    long long pairs_evaluated;
+    long long rows_solved;
+};
+
+struct Config {
+    int step_limit;
+    int solver;
+    double eps, d_min, d_max, delta, sigma, gamma;
+    int sweeps;
+    int family;
+    double under_relax;
+    int edge_constraints;
+    int force_fresh_search;
+    int record_path;
+    int coloring_mode;  // 0 reference replica, 1 device JP
+    unsigned long long color_seed;
+};
+
+struct Trace {
+    int searched, num_pairs, num_contact_rows, num_edge_rows, num_colors, num_active_pairs;
+    double bound, max_disp, residual;
+};
+
+struct Params {
+    Config cfg;
+    // ---- mesh
+    int nv, ne, nt, niso;
+    const double* inv_mass;
+    const int2* edges;
+    const int4* tris;
+    const int* iso;
+    const int* vedge_off;   // vertex -> incident edges (ascending edge index)
+    const int* vedge;
+    const int* edge_color;  // device-mode precoloring (-1 both static)
+    int edge_ncolors;
+    Bvh bvh[3];             // 0 triangles, 1 edges, 2 isolated vertices
+    // ---- vertex state
+    double4* x;
+    const double4* yk1;
+    double* r;
+    double4* imp;
+    unsigned long long* dmin;
+    // ---- edge rows (by mesh edge index); their count is Globals::ner
+    int* er_edge;            // ER list (ascending edge index)
+    int* er_index;            // per edge: position in er_edge (-1 if no row)
+    uint8_t* is_er;           // per edge
+    const double* ly;         // frozen targets
+    double* er_value;
+    double4* er_g;            // u / ly, w = diag
+    double* er_q;
+    double* edge_lambda;
+    int* er_color;            // per edge (ref mode: per step; device mode: = edge_color)
+    int* er_by_color;         // edge ids grouped by color
+    int* er_color_off;        // ncolors + 1
+    int* er_color_cnt;        // per color (ref-mode per-step bucketing)
+    int er_ncolors;           // device mode: colors used by ER rows
+    // ---- pairs
+    long long pcap;
+    int K;
+    uint64_t* pkey;
+    int4* pids;
+    double4* pdd;   // dir.xyz, dist
+    double4* pw;    // weights (kind dependent, see pack_weights)
+    uint8_t* pflag;
+    int* qcount;
+    int* qslot;     // nq * K
+    // ---- contact rows
+    uint64_t* c_key;
+    int4* c_ids;
+    double* c_jac;  // 12 per row
+    double* c_value;
+    double* c_diag;
+    double* c_q;
+    double* c_lambda;
+    double* c_next;  // Jacobi
+    int* c_color;
+    int* c_stamp;
+    long long* c_arch;  // archive index, or -(lower_bound)-1
+    uint64_t* c_prio;
+    int* c_by_color;
+    // vertex -> contact-row incidence (linked lists, entry = 4*row + m)
+    int* vhead;
+    int* vnext;
+    int* vcnt;
+    // color tables
+    int colcap;
+    int* ccount;
+    int* coff;
+    // archive
+    long long arch_cap;
+    uint64_t* arch_key[2];
+    double* arch_val[2];
+    long long* new_lb;
+    uint64_t* new_key;
+    double* new_val;
+    // reference coloring scratch
+    long long refpool_cap;
+    int* refpool;
+    // per block scratch
+    int nblocks;
+    long long* part_q;
+    long long* part_c;
+    long long* part_k;
+    long long* blk_lo;  // per block pair range
+    long long* blk_hi;
+    // globals + outputs
+    Globals* g;
+    double* step_max_disp;
+    double* path;   // (L+1) * nv * 3
+    Trace* trace;
+    int* dbg;       // host-mapped progress markers (TW_DEBUG=1), else null
+};
+
+// ------------------------------------------------------------ helpers
+__device__ __forceinline__ d3 ld3(const double4* p, int i) {
+    const double4 v = p[i];
+    return mk(v.x, v.y, v.z);
+}
+__device__ __forceinline__ double to_d(unsigned long long b) { return __longlong_as_double((long long)b); }
+__device__ __forceinline__ unsigned long long to_b(double d) {
+    return (unsigned long long)__double_as_longlong(d);
+}
+constexpr unsigned long long INF_BITS = 0x7ff0000000000000ull;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t edge_prio(int e) {
+    uint64_t z = uint64_t(uint32_t(e)) + 0x5851F42D4C957F2Dull;
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ bool jp_beats(uint64_t pa, long long ia, uint64_t pb, long long ib) {
+    return pa > pb || (pa == pb && ia > ib);
+}
+
+// Weights packing: VT (wb0, wb1, wb2, -), EE (wa0, wa1, wb0, wb1), VE (wb0, wb1, -, -),
+// VV (-). The reference's other weight slots are the ClosestResult defaults.
+__device__ __forceinline__ double4 pack_weights(int ka, int kb, const Closest& c) {
+    if (ka == KE) return make_double4(c.wa[0], c.wa[1], c.wb[0], c.wb[1]);
+    return make_double4(c.wb[0], c.wb[1], c.wb[2], 0.0);
+}
+__device__ __forceinline__ void unpack_weights(int ka, int kb, double4 w, double* wa, double* wb) {
+    wa[0] = 1.0, wa[1] = 0.0, wa[2] = 0.0;
+    wb[0] = 1.0, wb[1] = 0.0, wb[2] = 0.0;
+    if (ka == KE) {
+        wa[0] = w.x, wa[1] = w.y, wb[0] = w.z, wb[1] = w.w;
+    } else if (kb == KT) {
+        wb[0] = w.x, wb[1] = w.y, wb[2] = w.z;
+    } else if (kb == KE) {
+        wb[0] = w.x, wb[1] = w.y;
+    }
+}
+
+// vertex ids of the pair's simplices from its stored ids (a first)
+__device__ __forceinline__ void split_ids(int ka, int kb, int4 id, int* va, int* vb) {
+    const int v[4] = {id.x, id.y, id.z, id.w};
+    int k = 0;
+    for (int i = 0; i <= ka; ++i) va[i] = v[k++];
+    for (int i = ka + 1; i < 3; ++i) va[i] = -1;
+    for (int i = 0; i <= kb; ++i) vb[i] = v[k++];
+    for (int i = kb + 1; i < 3; ++i) vb[i] = -1;
+}
+
+}  // namespace tw

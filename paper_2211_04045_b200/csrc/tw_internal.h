@@ -1,0 +1,47 @@
+// Host-side launchers of the engine kernels (defined in tw_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "tw_engine.cuh"
+
+namespace tw {
+
+// k_unpack + k_edges_init
+void launch_setup(cudaStream_t s, int nv, const double* xs, const double* ys, const double* inv_mass,
+                  double4* x, double4* yk1, double* r, unsigned long long* dmin, int* vhead, int* vcnt,
+                  double4* imp, int* nonfinite, int ne, const int2* edges, double* ly, uint8_t* is_er,
+                  double* edge_lambda, int* er_color, const int* edge_color, int edge_rows,
+                  int device_coloring);
+
+void launch_pack(cudaStream_t s, int nv, const double4* x, double* out);
+
+// LBVH build for one primitive class; tmp must hold cub temp + 4 arrays of n
+size_t bvh_tmp_bytes(int n);
+void launch_bvh_build(cudaStream_t s, int cls, const Bvh& B, const int4* tris, const int2* edges,
+                      const int* iso, const double4* x, int nv, void* tmp, size_t tmp_bytes,
+                      unsigned long long* box /* 6, device */);
+
+int launch_count_last();  // kernels launched by the last launcher call
+void launch_bounds(cudaStream_t s, int nv, const double4* x, unsigned long long* box);
+
+// cooperative kernels
+cudaError_t coop_resolve(cudaStream_t s, const Params& P, int nblocks);
+cudaError_t coop_search(cudaStream_t s, const Params& P, int nblocks);
+cudaError_t coop_refresh(cudaStream_t s, const Params& P, int nblocks, double bound);
+cudaError_t launch_advance(cudaStream_t s, const Params& P, int nblocks);
+cudaError_t launch_closest(cudaStream_t s, int nv, const double4* x, long long n, const int* kinds,
+                           const int* verts, double* out, int* has);
+// blocks per SM the resolve kernel can keep resident
+int resolve_blocks_per_sm();
+
+// device-mode edge precoloring: one Jones-Plassmann round; returns via
+// *colored the number of edges colored so far (device counter)
+void launch_edge_color_round(cudaStream_t s, int ne, const int2* edges, const double* inv_mass,
+                             const int* vedge_off, const int* vedge, int* color, int* stamp, int round,
+                             int* colored);
+
+}  // namespace tw

@@ -1,0 +1,599 @@
+// Kernels of the B200 two-way collision handling path: per-call setup, the
+// LBVH build, the persistent cooperative resolve kernel (the whole Alg. 1
+// loop on the device, no host round trip per step) and the stage kernels
+// used for stage-by-stage parity. Compiled with -fmad=false.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "tw_internal.h"
+#include "tw_phases.cuh"
+
+namespace tw {
+
+// ================================================================= setup
+// Unpack N x 3 host-layout positions into double4 (w = inv_mass), apply the
+// static override y_k1 = x_start (resolve.cpp:48-50), initialise r = 1 and
+// the per-vertex scratch; flag non-finite input (resolve.cpp:41-43).
+__global__ void k_unpack(int nv, const double* xs, const double* ys, const double* inv_mass, double4* x,
+                         double4* yk1, double* r, unsigned long long* dmin, int* vhead, int* vcnt,
+                         double4* imp, int* nonfinite) {
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        const double im = inv_mass[v];
+        const double a0 = xs[3 * v], a1 = xs[3 * v + 1], a2 = xs[3 * v + 2];
+        double b0 = ys[3 * v], b1 = ys[3 * v + 1], b2 = ys[3 * v + 2];
+        if (!isfinite(a0) || !isfinite(a1) || !isfinite(a2) || !isfinite(b0) || !isfinite(b1) ||
+            !isfinite(b2))
+            atomicOr(nonfinite, 1);
+        if (im == 0.0) b0 = a0, b1 = a1, b2 = a2;
+        x[v] = make_double4(a0, a1, a2, im);
+        yk1[v] = make_double4(b0, b1, b2, im);
+        r[v] = 1.0;
+        dmin[v] = INF_BITS;
+        vhead[v] = -1;
+        vcnt[v] = 0;
+        imp[v] = make_double4(0, 0, 0, 0);
+    }
+}
+
+// frozen edge targets (resolve.cpp:53-55) and the edge-row set of the call
+// (constraints.cpp:152-153): target > 1e-12 and not both endpoints static
+__global__ void k_edges_init(int ne, const int2* edges, const double4* yk1, double* ly, uint8_t* is_er,
+                             double* edge_lambda, int* er_color, const int* edge_color, int edge_rows,
+                             int device_coloring) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ne;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int2 ed = edges[e];
+        const double4 a = yk1[ed.x], b = yk1[ed.y];
+        const double l = nrm(mk(a.x - b.x, a.y - b.y, a.z - b.z));
+        ly[e] = l;
+        is_er[e] = (edge_rows && l > 1e-12 && !(a.w == 0.0 && b.w == 0.0)) ? 1 : 0;
+        edge_lambda[e] = 0.0;
+        er_color[e] = device_coloring ? edge_color[e] : -1;
+    }
+}
+
+__global__ void k_pack(int nv, const double4* x, double* out) {
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        const double4 a = x[v];
+        out[3 * v] = a.x, out[3 * v + 1] = a.y, out[3 * v + 2] = a.z;
+    }
+}
+
+// ================================================================ LBVH
+__device__ __forceinline__ unsigned long long ord_bits(double d) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double from_ord(unsigned long long o) {
+    const unsigned long long b = (o & 0x8000000000000000ull) ? (o & ~0x8000000000000000ull) : ~o;
+    return __longlong_as_double((long long)b);
+}
+
+__global__ void k_bounds(int nv, const double4* x, unsigned long long* box /* 6: lo xyz, hi xyz */) {
+    __shared__ unsigned long long s[6];
+    if (threadIdx.x < 3) s[threadIdx.x] = ~0ull, s[3 + threadIdx.x] = 0ull;
+    __syncthreads();
+    unsigned long long l[3] = {~0ull, ~0ull, ~0ull}, h[3] = {0, 0, 0};
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        const double4 p = x[v];
+        const double c[3] = {p.x, p.y, p.z};
+        for (int k = 0; k < 3; ++k) {
+            const unsigned long long o = ord_bits(c[k]);
+            l[k] = min(l[k], o);
+            h[k] = max(h[k], o);
+        }
+    }
+    for (int k = 0; k < 3; ++k) atomicMin(&s[k], l[k]), atomicMax(&s[3 + k], h[k]);
+    __syncthreads();
+    if (threadIdx.x < 3) atomicMin(&box[threadIdx.x], s[threadIdx.x]), atomicMax(&box[3 + threadIdx.x], s[3 + threadIdx.x]);
+}
+
+__device__ __forceinline__ unsigned expand_bits(unsigned v) {
+    v = (v * 0x00010001u) & 0xFF0000FFu;
+    v = (v * 0x00000101u) & 0x0F00F00Fu;
+    v = (v * 0x00000011u) & 0xC30C30C3u;
+    v = (v * 0x00000005u) & 0x49249249u;
+    return v;
+}
+
+// 30-bit Morton code of each primitive's centroid
+__global__ void k_morton(int n, int cls, const int4* tris, const int2* edges, const int* iso, const double4* x,
+                         const unsigned long long* box, unsigned* codes, int* idx) {
+    const double lo[3] = {from_ord(box[0]), from_ord(box[1]), from_ord(box[2])};
+    const double hi[3] = {from_ord(box[3]), from_ord(box[4]), from_ord(box[5])};
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double c[3] = {0, 0, 0};
+        int ids[3], k;
+        if (cls == 0) {
+            const int4 t = tris[i];
+            ids[0] = t.x, ids[1] = t.y, ids[2] = t.z, k = 3;
+        } else if (cls == 1) {
+            const int2 e = edges[i];
+            ids[0] = e.x, ids[1] = e.y, k = 2;
+        } else {
+            ids[0] = iso[i], k = 1;
+        }
+        for (int j = 0; j < k; ++j) {
+            const double4 p = x[ids[j]];
+            c[0] += p.x, c[1] += p.y, c[2] += p.z;
+        }
+        unsigned q[3];
+        for (int a = 0; a < 3; ++a) {
+            const double ext = hi[a] - lo[a];
+            double u = ext > 0.0 ? (c[a] / k - lo[a]) / ext : 0.5;
+            u = fmin(fmax(u, 0.0), 1.0);
+            q[a] = min(1023u, (unsigned)(u * 1024.0));
+        }
+        codes[i] = (expand_bits(q[0]) << 2) | (expand_bits(q[1]) << 1) | expand_bits(q[2]);
+        idx[i] = (int)i;
+    }
+}
+
+__device__ __forceinline__ int lcp_delta(const unsigned* c, int n, int i, int j) {
+    if (j < 0 || j >= n) return -1;
+    const unsigned a = c[i], b = c[j];
+    if (a == b) return 32 + __clz((unsigned)(i ^ j));
+    return __clz(a ^ b);
+}
+
+// Karras 2012 hierarchy over sorted codes: internal nodes 0..n-2, leaf j at n-1+j
+__global__ void k_karras(int n, const unsigned* codes, const int* sorted_idx, int* prim, int2* child, int* parent,
+                         unsigned* flag) {
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)t;
+        prim[i] = sorted_idx[i];
+        if (i == 0) parent[n > 1 ? 0 : 0] = -1;
+        if (i >= n - 1) continue;
+        flag[i] = 0u;
+        const int d = (lcp_delta(codes, n, i, i + 1) - lcp_delta(codes, n, i, i - 1)) >= 0 ? 1 : -1;
+        const int dmin = lcp_delta(codes, n, i, i - d);
+        int lmax = 2;
+        while (lcp_delta(codes, n, i, i + lmax * d) > dmin) lmax *= 2;
+        int l = 0;
+        for (int s = lmax / 2; s >= 1; s /= 2)
+            if (lcp_delta(codes, n, i, i + (l + s) * d) > dmin) l += s;
+        const int j = i + l * d;
+        const int dnode = lcp_delta(codes, n, i, j);
+        int s = 0, div = 2, step;
+        do {
+            step = (l + div - 1) / div;
+            if (lcp_delta(codes, n, i, i + (s + step) * d) > dnode) s += step;
+            div *= 2;
+        } while (step > 1);
+        const int gamma = i + s * d + min(d, 0);
+        const int left = (min(i, j) == gamma) ? (n - 1 + gamma) : gamma;
+        const int right = (max(i, j) == gamma + 1) ? (n - 1 + gamma + 1) : gamma + 1;
+        child[i] = make_int2(left, right);
+        parent[left] = i;
+        parent[right] = i;
+    }
+}
+
+// =========================================================== closest
+__global__ void k_stage_closest(int nv, const double4* x, long long n, const int* kinds, const int* verts,
+                                double* out, int* has) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int ka = kinds[2 * i], kb = kinds[2 * i + 1];
+        const int* va = verts + 6 * i;
+        const int* vb = verts + 6 * i + 3;
+        Closest c;
+        const int h = pair_closest(ka, va, kb, vb, XLoad{x}, c);
+        has[i] = h;
+        double* o = out + 11 * i;
+        if (h == 1) {
+            o[0] = c.dist;
+            for (int k = 0; k < 3; ++k) o[1 + k] = c.wa[k], o[4 + k] = c.wb[k];
+            o[7] = c.dir.x, o[8] = c.dir.y, o[9] = c.dir.z;
+            o[10] = c.degenerate ? 1.0 : 0.0;
+        }
+    }
+    (void)nv;
+}
+
+// ====================================================== call prologue
+// ER compaction (edge order) and, in device-coloring mode, the static edge
+// row buckets by color (the edge-row colors are fixed for the call).
+__device__ bool prologue(const Params& P) {
+    long long lo, hi;
+    chunk_of(P.ne, &lo, &hi);
+    long long cnt = 0;
+    for (long long e = lo + threadIdx.x; e < hi; e += TPB) cnt += P.is_er[e];
+    const long long t = block_sum(cnt);
+    if (threadIdx.x == 0) P.part_k[blockIdx.x] = t;
+    if (P.cfg.record_path)
+        for (long long v = gtid(); v < P.nv; v += gstride()) {
+            const double4 a = P.x[v];
+            P.path[3 * v] = a.x, P.path[3 * v + 1] = a.y, P.path[3 * v + 2] = a.z;
+        }
+    if (!grid_sync(P.g)) return false;
+    const long long ner_total = prefix_of(P.part_k, gridDim.x);
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.g->ner = (int)ner_total;
+    long long base = prefix_of(P.part_k, blockIdx.x);
+    for (long long tt = lo; tt < hi; tt += TPB) {
+        const long long e = tt + threadIdx.x;
+        const int f = e < hi ? P.is_er[e] : 0;
+        long long tot;
+        const long long pos = base + block_scan(f, &tot);
+        base += tot;
+        if (e < hi) P.er_index[e] = f ? (int)pos : -1;
+        if (f) {
+            P.er_edge[pos] = (int)e;
+            if (P.cfg.coloring_mode == 1) atomicAdd(&P.er_color_cnt[P.er_color[e]], 1);
+        }
+    }
+    if (!grid_sync(P.g)) return false;
+    if (P.cfg.coloring_mode == 1) {
+        long long run = 0;
+        for (int b0 = 0; b0 < P.er_ncolors; b0 += TPB) {
+            const int c = b0 + threadIdx.x;
+            const long long v = c < P.er_ncolors ? P.er_color_cnt[c] : 0;
+            long long tt;
+            const long long ex = block_scan(v, &tt);
+            if (blockIdx.x == 0 && c < P.er_ncolors) P.er_color_off[c] = (int)(run + ex);
+            run += tt;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) P.er_color_off[P.er_ncolors] = (int)run;
+        if (!grid_sync(P.g)) return false;
+        for (long long k = gtid(); k < P.g->ner; k += gstride()) {
+            const int e = P.er_edge[k];
+            const int c = P.er_color[e];
+            const int slot = atomicSub(&P.er_color_cnt[c], 1) - 1;
+            P.er_by_color[P.er_color_off[c] + slot] = e;
+        }
+        if (!grid_sync(P.g)) return false;
+    }
+    return true;
+}
+
+// ======================================================== resolve kernel
+// The Alg.-1 loop of resolve.cpp:69-137, device resident: every CTA runs the
+// same control flow (replicated scalars, read from device memory after each
+// grid barrier), so the host only sees the final state.
+// progress marker (TW_DEBUG=1): the last phase each CTA completed, written to
+// host-mapped memory so it survives a device fault
+#define SYNC()                                                                    \
+    do {                                                                          \
+        if (P.dbg && threadIdx.x == 0) {                                          \
+            P.dbg[blockIdx.x] = (dbg_step << 16) | __LINE__;                      \
+            __threadfence_system();                                               \
+        }                                                                         \
+        if (!grid_sync(g)) return;                                                \
+    } while (0)
+
+__global__ void __launch_bounds__(TPB) k_resolve(Params P) {
+    Globals* g = P.g;
+    int dbg_step = 0;
+    if (g->nonfinite || g->error) return;  // non-finite input detected by k_unpack
+    if (!prologue(P)) return;
+    const Config& C = P.cfg;
+    double bound = 0.0;  // forces a search on step 0
+    int searches = 0;
+    int sel = 0;
+    long long narch = 0;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    int steps = 0;
+    double residual = 0.0;
+    bool converged = false;
+    for (int l = 0; l < C.step_limit; ++l) {
+        dbg_step = l;
+        const bool search = C.force_fresh_search || bound < C.d_min;
+        if (search) {
+            ph_refit(P);
+            SYNC();
+            ph_traverse(P);
+            SYNC();
+            ph_emit_pairs(P, searches == 0);
+            SYNC();
+            bound = C.d_max;
+            ++searches;
+        }
+        if (lead) {
+            g->maxdisp_bits = 0ull;
+            g->resid_bits = 0ull;
+            g->colored = 0;
+            g->max_color = -1;
+        }
+        // ---- backward step at x^(l)
+        ph_rows(P, sel, narch);
+        SYNC();
+        const long long nc = g->nc;
+        if (lead) g->nactive = 0;
+        ph_warm(P, nc);
+        SYNC();
+        int ncol_c, ncol_e, ncol;
+        if (C.coloring_mode == 0) {
+            ph_color_ref(P, nc);
+            SYNC();
+            ncol = g->max_color + 1;
+            if (ncol > P.colcap) {
+                if (lead) atomicOr(&g->error, ERR_CAP_COLORS);
+                return;
+            }
+            ph_bucket_count(P, nc);
+            SYNC();
+            ph_bucket_scatter(P, nc, ncol, true);
+            SYNC();
+            ph_bucket_place(P, nc, true);
+            SYNC();
+            ncol_c = ncol_e = ncol;
+        } else {
+            for (int k = 1; *((volatile int*)&g->colored) < nc; ++k) {
+                ph_color_round(P, nc, k);
+                SYNC();
+            }
+            ncol_c = g->max_color + 1;
+            ncol_e = C.edge_constraints ? P.er_ncolors : 0;
+            ncol = max(ncol_c, ncol_e);
+            ph_bucket_scatter(P, nc, ncol_c, false);
+            SYNC();
+            ph_bucket_place(P, nc, false);
+            SYNC();
+        }
+        if (C.solver == 0) {
+            for (int sw = 0; sw < C.sweeps; ++sw)
+                for (int c = 0; c < ncol; ++c) {
+                    ph_pgs_color(P, c, ncol_c, ncol_e);
+                    SYNC();
+                }
+        } else {
+            for (int sw = 0; sw < C.sweeps; ++sw) {
+                ph_jacobi_next(P, nc);
+                SYNC();
+                ph_jacobi_apply(P, nc);
+                SYNC();
+                ph_jacobi_commit(P, nc);
+                SYNC();
+            }
+        }
+        // ---- forward step
+        ph_advance(P, bound, l, nc, sel);
+        SYNC();
+        const double maxdisp = to_d(g->maxdisp_bits);
+        residual = to_d(g->resid_bits);
+        if (lead) {
+            if (maxdisp > 0.5 * C.gamma * bound) g->step_law_violated = 1;
+            if (P.step_max_disp) P.step_max_disp[l] = maxdisp;
+            g->rows_solved += nc + (C.edge_constraints ? P.g->ner : 0);
+        }
+        const double bound_next = bound - 2.0 * maxdisp;
+        const bool next_search = C.force_fresh_search || bound_next < C.d_min;
+        const long long nnew = prefix_of(P.part_k, gridDim.x);
+        if (nnew > 0) {
+            if (narch + nnew > P.arch_cap) {
+                if (lead) atomicOr(&g->error, ERR_CAP_ARCH);
+                return;
+            }
+            ph_arch_rank(P, nc);
+            SYNC();
+            ph_arch_merge(P, nnew, sel, narch);
+            SYNC();
+            sel ^= 1;
+            narch += nnew;
+        }
+        ph_refresh(P, bound, next_search, true, sel, narch);
+        SYNC();
+        if (lead && P.trace) {
+            Trace& t = P.trace[l];
+            t.searched = search;
+            t.num_pairs = (int)g->np;
+            t.num_contact_rows = (int)nc;
+            t.num_edge_rows = C.edge_constraints ? P.g->ner : 0;
+            t.num_colors = ncol;
+            t.num_active_pairs = g->nactive;
+            t.bound = bound;
+            t.max_disp = maxdisp;
+            t.residual = residual;
+        }
+        if (lead) g->ncolors_last = ncol;
+        bound = bound_next;
+        steps = l + 1;
+        if (residual < C.eps) {
+            converged = true;
+            break;
+        }
+    }
+    if (lead) {
+        g->steps = steps;
+        g->searches = searches;
+        g->converged = converged;
+        g->final_residual = residual;
+        g->narch = narch;
+        g->arch_sel = sel;
+    }
+}
+
+// ======================================================== stage kernels
+__global__ void __launch_bounds__(TPB) k_stage_search(Params P) {
+    ph_refit(P);
+    if (!grid_sync(P.g)) return;
+    ph_traverse(P);
+    if (!grid_sync(P.g)) return;
+    ph_emit_pairs(P, false);
+}
+
+// refresh + per-vertex bound into P.r (min(bound, dmin))
+__global__ void __launch_bounds__(TPB) k_stage_refresh(Params P, double bound) {
+    ph_refresh(P, bound, false, false, 0, 0);
+    if (!grid_sync(P.g)) return;
+    for (long long v = gtid(); v < P.nv; v += gstride()) P.r[v] = mind(bound, to_d(P.dmin[v]));
+}
+
+__global__ void k_stage_advance(Params P, double* max_disp) {
+    ph_advance(P, __longlong_as_double(0x7ff0000000000000ll), -1, 0, 0);
+    (void)max_disp;
+}
+
+}  // namespace tw
+
+// ==================================================== edge precoloring
+namespace tw {
+
+// One Jones-Plassmann round over the mesh edges (device-mode edge-row
+// colors, computed once per mesh): same rule as the contact rows, priority
+// edge_prio(e), conflicts through shared vertices with inv_mass > 0.
+__global__ void k_edge_color_round(int ne, const int2* edges, const double* inv_mass, const int* vedge_off,
+                                   const int* vedge, int* color, int* stamp, int round, int* colored) {
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ne;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int e = (int)t;
+        if (stamp[e] != 0) continue;
+        const int2 ed = edges[e];
+        const int vv[2] = {ed.x, ed.y};
+        const uint64_t pe = edge_prio(e);
+        bool is_max = true;
+        for (int k = 0; k < 2 && is_max; ++k) {
+            const int v = vv[k];
+            if (!(inv_mass[v] > 0.0)) continue;
+            for (int q = vedge_off[v]; q < vedge_off[v + 1]; ++q) {
+                const int f = vedge[q];
+                if (f == e) continue;
+                const int sf = *((volatile int*)&stamp[f]);
+                if (sf != 0 && sf != round) continue;
+                if (!jp_beats(pe, e, edge_prio(f), f)) {
+                    is_max = false;
+                    break;
+                }
+            }
+        }
+        if (!is_max) continue;
+        unsigned long long used[4] = {0, 0, 0, 0};
+        int big_min = 1 << 30;
+        for (int k = 0; k < 2; ++k) {
+            const int v = vv[k];
+            if (!(inv_mass[v] > 0.0)) continue;
+            for (int q = vedge_off[v]; q < vedge_off[v + 1]; ++q) {
+                const int f = vedge[q];
+                if (f == e) continue;
+                const int sf = *((volatile int*)&stamp[f]);
+                if (sf >= 1 && sf < round) {
+                    const int c = color[f];
+                    if (c < 256) used[c >> 6] |= 1ull << (c & 63);
+                }
+            }
+        }
+        int col = -1;
+        for (int w = 0; w < 4 && col < 0; ++w)
+            if (~used[w]) col = w * 64 + __ffsll(~used[w]) - 1;
+        (void)big_min;
+        color[e] = col < 0 ? 256 : col;  // > 256 edge colors: not reachable for manifold meshes
+        stamp[e] = round;
+        atomicAdd(colored, 1);
+    }
+}
+
+static int g_last_launches = 0;
+int launch_count_last() { return g_last_launches; }
+
+static int grid_for(long long n, int tpb = 256) {
+    long long b = (n + tpb - 1) / tpb;
+    if (b < 1) b = 1;
+    if (b > 148 * 8) b = 148 * 8;
+    return (int)b;
+}
+
+void launch_setup(cudaStream_t s, int nv, const double* xs, const double* ys, const double* inv_mass,
+                  double4* x, double4* yk1, double* r, unsigned long long* dmin, int* vhead, int* vcnt,
+                  double4* imp, int* nonfinite, int ne, const int2* edges, double* ly, uint8_t* is_er,
+                  double* edge_lambda, int* er_color, const int* edge_color, int edge_rows,
+                  int device_coloring) {
+    g_last_launches = 0;
+    if (nv > 0) {
+        k_unpack<<<grid_for(nv), 256, 0, s>>>(nv, xs, ys, inv_mass, x, yk1, r, dmin, vhead, vcnt, imp, nonfinite);
+        ++g_last_launches;
+    }
+    if (ne > 0) {
+        k_edges_init<<<grid_for(ne), 256, 0, s>>>(ne, edges, yk1, ly, is_er, edge_lambda, er_color, edge_color,
+                                                  edge_rows, device_coloring);
+        ++g_last_launches;
+    }
+}
+
+void launch_pack(cudaStream_t s, int nv, const double4* x, double* out) {
+    g_last_launches = 0;
+    if (nv > 0) {
+        k_pack<<<grid_for(nv), 256, 0, s>>>(nv, x, out);
+        ++g_last_launches;
+    }
+}
+
+size_t bvh_tmp_bytes(int n) {
+    size_t cub_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const unsigned*)nullptr, (unsigned*)nullptr,
+                                    (const int*)nullptr, (int*)nullptr, n < 1 ? 1 : n, 0, 30);
+    const size_t arr = ((size_t)(n < 1 ? 1 : n) * 4 + 255) & ~(size_t)255;
+    return cub_bytes + 4 * arr + 256;
+}
+
+void launch_bvh_build(cudaStream_t s, int cls, const Bvh& B, const int4* tris, const int2* edges, const int* iso,
+                      const double4* x, int nv, void* tmp, size_t tmp_bytes, unsigned long long* box) {
+    g_last_launches = 0;
+    const int n = B.n;
+    if (n == 0) return;
+    const size_t arr = ((size_t)n * 4 + 255) & ~(size_t)255;
+    char* base = (char*)tmp;
+    unsigned* codes = (unsigned*)base;
+    unsigned* codes2 = (unsigned*)(base + arr);
+    int* idx = (int*)(base + 2 * arr);
+    int* idx2 = (int*)(base + 3 * arr);
+    void* cub_tmp = base + 4 * arr;
+    size_t cub_bytes = tmp_bytes - 4 * arr - 256;
+    k_morton<<<grid_for(n), 256, 0, s>>>(n, cls, tris, edges, iso, x, box, codes, idx);
+    cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, codes, codes2, idx, idx2, n, 0, 30, s);
+    k_karras<<<grid_for(n), 256, 0, s>>>(n, codes2, idx2, B.prim, B.child, B.parent, B.flag);
+    g_last_launches = 3;
+    (void)nv;
+}
+
+void launch_bounds(cudaStream_t s, int nv, const double4* x, unsigned long long* box) {
+    k_bounds<<<grid_for(nv), 256, 0, s>>>(nv, x, box);
+}
+
+int resolve_blocks_per_sm() {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_resolve, TPB, 0);
+    return b;
+}
+
+static cudaError_t coop(const void* fn, cudaStream_t s, int nblocks, void** args) {
+    return cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(TPB), args, 0, s);
+}
+
+cudaError_t coop_resolve(cudaStream_t s, const Params& P, int nblocks) {
+    Params p = P;
+    void* args[] = {&p};
+    return coop((const void*)k_resolve, s, nblocks, args);
+}
+cudaError_t coop_search(cudaStream_t s, const Params& P, int nblocks) {
+    Params p = P;
+    void* args[] = {&p};
+    return coop((const void*)k_stage_search, s, nblocks, args);
+}
+cudaError_t coop_refresh(cudaStream_t s, const Params& P, int nblocks, double bound) {
+    Params p = P;
+    double b = bound;
+    void* args[] = {&p, &b};
+    return coop((const void*)k_stage_refresh, s, nblocks, args);
+}
+cudaError_t launch_advance(cudaStream_t s, const Params& P, int nblocks) {
+    double* md = nullptr;
+    k_stage_advance<<<nblocks, TPB, 0, s>>>(P, md);
+    return cudaGetLastError();
+}
+cudaError_t launch_closest(cudaStream_t s, int nv, const double4* x, long long n, const int* kinds, const int* verts,
+                           double* out, int* has) {
+    if (n == 0) return cudaSuccess;
+    k_stage_closest<<<grid_for(n), 256, 0, s>>>(nv, x, n, kinds, verts, out, has);
+    return cudaGetLastError();
+}
+void launch_edge_color_round(cudaStream_t s, int ne, const int2* edges, const double* inv_mass, const int* vedge_off,
+                             const int* vedge, int* color, int* stamp, int round, int* colored) {
+    k_edge_color_round<<<grid_for(ne), 256, 0, s>>>(ne, edges, inv_mass, vedge_off, vedge, color, stamp, round,
+                                                   colored);
+}
+
+}  // namespace tw

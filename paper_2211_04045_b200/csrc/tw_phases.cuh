@@ -1,0 +1,1268 @@
+// Phase functions of the device-resident Alg. 1 (resolve.cpp:36-144). Every
+// phase is a grid-stride (or block-chunked, where order matters) loop run by
+// all CTAs of the persistent cooperative kernel; phases are separated by
+// grid_sync(). Reference citations are into /root/reference/proj.
+#pragma once
+
+#include "tw_engine.cuh"
+
+namespace tw {
+
+// =============================================================== barrier
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Sense-free generation barrier over all CTAs of a cooperative launch. Thread 0
+// of each CTA releases its CTA's writes (fence), arrives, and the last arriver
+// bumps the generation. A 20 s watchdog turns a hang into ERR_TIMEOUT.
+__device__ __forceinline__ bool grid_sync(Globals* g) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* genp = &g->bar_gen;
+        const unsigned gen = *genp;
+        __threadfence();
+        const unsigned arrived = atomicAdd(&g->bar_count, 1u);
+        if (arrived == gridDim.x - 1) {
+            atomicExch(&g->bar_count, 0u);
+            __threadfence();
+            atomicAdd(&g->bar_gen, 1u);
+        } else {
+            const unsigned long long t0 = global_ns();
+            while (*genp == gen) {
+                __nanosleep(32);
+                if (global_ns() - t0 > 20000000000ull) {
+                    atomicOr(&g->error, ERR_TIMEOUT);
+                    break;
+                }
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    return *((volatile int*)&g->error) == 0;
+}
+
+// ============================================================ block scans
+// exclusive scan of v over the CTA; *total receives the CTA sum
+__device__ __forceinline__ long long block_scan(long long v, long long* total) {
+    __shared__ long long ws[TPB / 32 + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) ws[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        long long s = lane < TPB / 32 ? ws[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < TPB / 32) ws[lane] = s;  // inclusive warp prefix
+    }
+    __syncthreads();
+    const long long wpre = warp ? ws[warp - 1] : 0;
+    *total = ws[TPB / 32 - 1];
+    __syncthreads();
+    return wpre + inc - v;
+}
+
+__device__ __forceinline__ long long block_sum(long long v) {
+    long long t;
+    block_scan(v, &t);
+    return t;
+}
+
+// sum of part[0..upto) (every thread gets it)
+__device__ __forceinline__ long long prefix_of(const long long* part, int upto) {
+    long long s = 0;
+    for (int i = threadIdx.x; i < upto; i += TPB) s += ((volatile const long long*)part)[i];
+    return block_sum(s);
+}
+
+__device__ __forceinline__ void chunk_of(long long n, long long* lo, long long* hi) {
+    const long long c = (n + gridDim.x - 1) / gridDim.x;
+    *lo = min(n, (long long)blockIdx.x * c);
+    *hi = min(n, *lo + c);
+}
+
+__device__ __forceinline__ long long gtid() { return (long long)blockIdx.x * TPB + threadIdx.x; }
+__device__ __forceinline__ long long gstride() { return (long long)gridDim.x * TPB; }
+
+struct XLoad {
+    const double4* x;
+    __device__ __forceinline__ d3 operator()(int i) const { return ld3(x, i); }
+};
+
+// ================================================================= BVH
+__device__ __forceinline__ void prim_box(const Params& P, int cls, int prim, double lo[3], double hi[3]) {
+    int ids[3];
+    int n;
+    if (cls == 0) {
+        const int4 t = P.tris[prim];
+        ids[0] = t.x, ids[1] = t.y, ids[2] = t.z, n = 3;
+    } else if (cls == 1) {
+        const int2 e = P.edges[prim];
+        ids[0] = e.x, ids[1] = e.y, n = 2;
+    } else {
+        ids[0] = P.iso[prim], n = 1;
+    }
+    const d3 p0 = ld3(P.x, ids[0]);
+    lo[0] = hi[0] = p0.x, lo[1] = hi[1] = p0.y, lo[2] = hi[2] = p0.z;
+    for (int i = 1; i < n; ++i) {
+        const d3 p = ld3(P.x, ids[i]);
+        lo[0] = fmin(lo[0], p.x), hi[0] = fmax(hi[0], p.x);
+        lo[1] = fmin(lo[1], p.y), hi[1] = fmax(hi[1], p.y);
+        lo[2] = fmin(lo[2], p.z), hi[2] = fmax(hi[2], p.z);
+    }
+}
+
+// A1: bottom-up refit of all three hierarchies at the current positions
+// (node flags are zero on entry; the second child to arrive builds the parent)
+__device__ void ph_refit(const Params& P) {
+    for (int cls = 0; cls < 3; ++cls) {
+        const Bvh& B = P.bvh[cls];
+        if (B.n == 0) continue;
+        for (long long j = gtid(); j < B.n; j += gstride()) {
+            double lo[3], hi[3];
+            prim_box(P, cls, B.prim[j], lo, hi);
+            int node = B.n - 1 + (int)j;
+            B.lo[node] = make_float4(__double2float_rd(lo[0]), __double2float_rd(lo[1]),
+                                     __double2float_rd(lo[2]), 0.f);
+            B.hi[node] = make_float4(__double2float_ru(hi[0]), __double2float_ru(hi[1]),
+                                     __double2float_ru(hi[2]), 0.f);
+            for (;;) {
+                const int par = B.parent[node];
+                if (par < 0) break;
+                __threadfence();
+                if (atomicAdd(&B.flag[par], 1u) == 0u) break;
+                __threadfence();
+                const int2 ch = B.child[par];
+                const float4 a0 = __ldcg(&B.lo[ch.x]), a1 = __ldcg(&B.hi[ch.x]);
+                const float4 b0 = __ldcg(&B.lo[ch.y]), b1 = __ldcg(&B.hi[ch.y]);
+                B.lo[par] = make_float4(fminf(a0.x, b0.x), fminf(a0.y, b0.y), fminf(a0.z, b0.z), 0.f);
+                B.hi[par] = make_float4(fmaxf(a1.x, b1.x), fmaxf(a1.y, b1.y), fmaxf(a1.z, b1.z), 0.f);
+                node = par;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ bool box_hit(float4 qlo, float4 qhi, float4 lo, float4 hi) {
+    return qlo.x <= hi.x && qlo.y <= hi.y && qlo.z <= hi.z && lo.x <= qhi.x && lo.y <= qhi.y &&
+           lo.z <= qhi.z;
+}
+
+// query classes in output (key) order: VV, VE, VT, EE
+__device__ __forceinline__ void query_of(const Params& P, long long q, int* ka, int* ia, int* kb,
+                                         int* cls) {
+    const long long niso = P.niso;
+    if (q < niso) {
+        *ka = KV, *ia = P.iso[q], *kb = KV, *cls = 2;
+    } else if (q < 2 * niso) {
+        *ka = KV, *ia = P.iso[q - niso], *kb = KE, *cls = 1;
+    } else if (q < 2 * niso + P.nv) {
+        *ka = KV, *ia = (int)(q - 2 * niso), *kb = KT, *cls = 0;
+    } else {
+        *ka = KE, *ia = (int)(q - 2 * niso - P.nv), *kb = KE, *cls = 1;
+    }
+}
+__device__ __forceinline__ long long num_queries(const Params& P) {
+    return 2LL * P.niso + P.nv + P.ne;
+}
+
+__device__ __forceinline__ void simplex_ids(const Params& P, int k, int idx, int* v) {
+    v[0] = v[1] = v[2] = -1;
+    if (k == KV) {
+        v[0] = idx;
+    } else if (k == KE) {
+        const int2 e = P.edges[idx];
+        v[0] = e.x, v[1] = e.y;
+    } else {
+        const int4 t = P.tris[idx];
+        v[0] = t.x, v[1] = t.y, v[2] = t.z;
+    }
+}
+
+// primitive -> simplex index of the b side for class cls
+__device__ __forceinline__ int prim_to_index(const Params& P, int cls, int prim) {
+    return cls == 2 ? P.iso[prim] : prim;
+}
+
+// The exact narrow-phase test of the reference search (proximity.cpp:162-167):
+// canonical candidate, non-adjacent, has a closest point, distance < d_max.
+__device__ __forceinline__ bool candidate_keep(const Params& P, int ka, int ia, const int* va,
+                                               int kb, int ib, Closest& c) {
+    if (ka == KE && ib <= ia) return false;             // EE: a is the lower edge index
+    if (ka == KV && kb == KV && ib <= ia) return false; // VV: a < b
+    int vb[3];
+    simplex_ids(P, kb, ib, vb);
+    const int h = pair_closest(ka, va, kb, vb, XLoad{P.x}, c);
+    return h == 1 && c.dist < P.cfg.d_max;
+}
+
+// A2: traverse every query (block-chunked, in key order) and record the
+// surviving partners; per-block totals go to part_q
+__device__ void ph_traverse(const Params& P) {
+    const long long nq = num_queries(P);
+    long long lo, hi;
+    chunk_of(nq, &lo, &hi);
+    long long cnt_sum = 0, evals = 0;
+    const double infl = P.cfg.d_max * (1.0 + 1e-6) + 1e-12;
+    for (long long q = lo + threadIdx.x; q < hi; q += TPB) {
+        int ka, ia, kb, cls;
+        query_of(P, q, &ka, &ia, &kb, &cls);
+        const Bvh& B = P.bvh[cls];
+        int cnt = 0;
+        if (B.n > 0) {
+            int va[3];
+            simplex_ids(P, ka, ia, va);
+            double lo3[3], hi3[3];
+            const d3 p0 = ld3(P.x, va[0]);
+            lo3[0] = hi3[0] = p0.x, lo3[1] = hi3[1] = p0.y, lo3[2] = hi3[2] = p0.z;
+            if (ka == KE) {
+                const d3 p1 = ld3(P.x, va[1]);
+                lo3[0] = fmin(lo3[0], p1.x), hi3[0] = fmax(hi3[0], p1.x);
+                lo3[1] = fmin(lo3[1], p1.y), hi3[1] = fmax(hi3[1], p1.y);
+                lo3[2] = fmin(lo3[2], p1.z), hi3[2] = fmax(hi3[2], p1.z);
+            }
+            const float4 qlo = make_float4(__double2float_rd(lo3[0] - infl), __double2float_rd(lo3[1] - infl),
+                                           __double2float_rd(lo3[2] - infl), 0.f);
+            const float4 qhi = make_float4(__double2float_ru(hi3[0] + infl), __double2float_ru(hi3[1] + infl),
+                                           __double2float_ru(hi3[2] + infl), 0.f);
+            int* slots = P.qslot + q * P.K;
+            int stack[64];
+            int sp = 0;
+            const int root = 0;
+            auto visit_leaf = [&](int node) {
+                const int ib = prim_to_index(P, cls, B.prim[node - (B.n - 1)]);
+                Closest c;
+                ++evals;
+                if (candidate_keep(P, ka, ia, va, kb, ib, c)) {
+                    if (cnt < P.K) slots[cnt] = ib;
+                    ++cnt;
+                }
+            };
+            if (B.n == 1) {
+                if (box_hit(qlo, qhi, B.lo[0], B.hi[0])) visit_leaf(0);
+            } else {
+                stack[sp++] = root;
+                while (sp > 0) {
+                    const int node = stack[--sp];
+                    const int2 ch = B.child[node];
+                    const int c2[2] = {ch.x, ch.y};
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        const int cn = c2[k];
+                        if (!box_hit(qlo, qhi, B.lo[cn], B.hi[cn])) continue;
+                        if (cn >= B.n - 1) {
+                            visit_leaf(cn);
+                        } else if (sp < 64) {
+                            stack[sp++] = cn;
+                        } else {
+                            atomicOr(&P.g->error, ERR_CAP_STACK);
+                        }
+                    }
+                }
+            }
+        }
+        P.qcount[q] = cnt;
+        if (cnt > P.K) {
+            atomicOr(&P.g->error, ERR_CAP_SLOTS);
+            atomicMax(&P.g->needed_k, cnt);
+        }
+        cnt_sum += cnt;
+    }
+    const long long tot = block_sum(cnt_sum);
+    const long long ev = block_sum(evals);
+    if (threadIdx.x == 0) {
+        P.part_q[blockIdx.x] = tot;
+        atomicAdd((unsigned long long*)&P.g->pairs_evaluated, (unsigned long long)ev);
+    }
+}
+
+__device__ __forceinline__ void vertex_min(const Params& P, int v, double d) {
+    atomicMin(&P.dmin[v], to_b(d));
+}
+
+// contact predicate of linearize_all (constraints.cpp:186-199): active,
+// not all static, inside the activation window, non-degenerate jacobian
+__device__ __forceinline__ bool contact_pred(const Params& P, int ka, int kb, const int* va,
+                                             const int* vb, const double4& dd, const double4& w,
+                                             uint8_t flags) {
+    if (!(flags & PF_ACTIVE) || (flags & PF_ALL_STATIC)) return false;
+    if (!(dd.w < P.cfg.delta)) return false;
+    double wa[3], wb[3];
+    unpack_weights(ka, kb, w, wa, wb);
+    Row c;
+    build_contact(ka, va, kb, vb, wa, wb, dd.w, mk(dd.x, dd.y, dd.z), P.cfg.delta, P.cfg.family,
+                  XLoad{P.x}, c);
+    return !(row_jnorm(c) < 1e-28);
+}
+
+// A3: prefix the per-query counts, sort each query's partners, evaluate and
+// write the pair records in key order; seed the vertex bound, the contact
+// predicate for the coming linearization, and reset the refit flags.
+__device__ void ph_emit_pairs(const Params& P, bool first_search) {
+    const long long nq = num_queries(P);
+    long long lo, hi;
+    chunk_of(nq, &lo, &hi);
+    const long long total = prefix_of(P.part_q, gridDim.x);
+    if (total > P.pcap) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) {
+            atomicOr(&P.g->error, ERR_CAP_PAIRS);
+            P.g->needed_pairs = total;
+        }
+        return;
+    }
+    long long base = prefix_of(P.part_q, blockIdx.x);
+    const long long block_lo = base;
+    long long ncontact = 0;
+    int touching = 0;
+    for (long long t = lo; t < hi; t += TPB) {
+        const long long q = t + threadIdx.x;
+        const int cnt = q < hi ? P.qcount[q] : 0;
+        long long tile_tot;
+        const long long off = base + block_scan(cnt, &tile_tot);
+        base += tile_tot;
+        if (q >= hi || cnt == 0) continue;
+        int ka, ia, kb, cls;
+        query_of(P, q, &ka, &ia, &kb, &cls);
+        int* s = P.qslot + q * P.K;
+        for (int i = 1; i < cnt; ++i) {  // insertion sort of the partner indices
+            const int v = s[i];
+            int j = i - 1;
+            while (j >= 0 && s[j] > v) s[j + 1] = s[j], --j;
+            s[j + 1] = v;
+        }
+        int va[3];
+        simplex_ids(P, ka, ia, va);
+        for (int i = 0; i < cnt; ++i) {
+            const int ib = s[i];
+            int vb[3];
+            simplex_ids(P, kb, ib, vb);
+            Closest c;
+            pair_closest(ka, va, kb, vb, XLoad{P.x}, c);
+            const long long p = off + i;
+            const int4 ids = ka == KE ? make_int4(va[0], va[1], vb[0], vb[1])
+                                      : make_int4(va[0], vb[0], vb[1], vb[2]);
+            bool all_static = true;
+            for (int k = 0; k <= ka; ++k) all_static &= P.inv_mass[va[k]] == 0.0;
+            for (int k = 0; k <= kb; ++k) all_static &= P.inv_mass[vb[k]] == 0.0;
+            uint8_t fl = PF_ACTIVE | (all_static ? PF_ALL_STATIC : 0) | (c.degenerate ? PF_DEGENERATE : 0);
+            const double4 dd = make_double4(c.dir.x, c.dir.y, c.dir.z, c.dist);
+            const double4 w = pack_weights(ka, kb, c);
+            if (contact_pred(P, ka, kb, va, vb, dd, w, fl)) {
+                fl |= PF_CONTACT;
+                ++ncontact;
+            }
+            P.pkey[p] = pair_key(ka, ia, kb, ib);
+            P.pids[p] = ids;
+            P.pdd[p] = dd;
+            P.pw[p] = w;
+            P.pflag[p] = fl;
+            for (int k = 0; k <= ka; ++k) vertex_min(P, va[k], c.dist);
+            for (int k = 0; k <= kb; ++k) vertex_min(P, vb[k], c.dist);
+            if (first_search && c.dist < 1e-10) touching = 1;
+        }
+    }
+    const long long nct = block_sum(ncontact);
+    const long long touch = block_sum(touching);
+    if (threadIdx.x == 0) {
+        P.part_c[blockIdx.x] = nct;
+        P.blk_lo[blockIdx.x] = block_lo;
+        P.blk_hi[blockIdx.x] = base;
+        if (touch) P.g->start_in_contact = 1;
+        if (blockIdx.x == 0) P.g->np = total;
+    }
+    // reset refit flags for the next search
+    for (int cls = 0; cls < 3; ++cls) {
+        const Bvh& B = P.bvh[cls];
+        for (long long j = gtid(); j < (long long)B.n - 1; j += gstride()) B.flag[j] = 0u;
+    }
+}
+
+// ============================================================== archive
+__device__ __forceinline__ long long arch_lower_bound(const uint64_t* keys, long long n, uint64_t k) {
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (keys[mid] < k) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// ============================================================ rows (B2)
+__device__ __forceinline__ void insert_list(const Params& P, int v, int entry) {
+    P.vnext[entry] = atomicExch(&P.vhead[v], entry);
+    atomicAdd(&P.vcnt[v], 1);
+}
+
+// edge-length row at x (constraints.cpp:144-173) + fill_diag + q
+__device__ __forceinline__ void edge_row(const Params& P, int e) {
+    const int2 ed = P.edges[e];
+    const double4 xi4 = P.x[ed.x], xj4 = P.x[ed.y];
+    const d3 xi = mk(xi4.x, xi4.y, xi4.z), xj = mk(xj4.x, xj4.y, xj4.z);
+    const double ly = P.ly[e];
+    const d3 d = sub(xi, xj);
+    const double len = nrm(d);
+    const double value = P.cfg.sigma - len / ly;
+    d3 g = mk(0, 0, 0), j0 = mk(0, 0, 0);
+    if (len > 1e-12) {
+        const d3 u = dvd(d, len);
+        g = dvd(u, ly);
+        j0 = dvd(neg(u), ly);
+    }
+    double dg = 0.0;
+    dg += xi4.w * sqn(j0);
+    dg += xj4.w * sqn(g);
+    const double diag = maxd(dg, 1e-10);
+    const d3 yi = ld3(P.yk1, ed.x), yj = ld3(P.yk1, ed.y);
+    double q = value;
+    q += dot(j0, sub(yi, xi));
+    q += dot(g, sub(yj, xj));
+    P.er_value[e] = value;
+    P.er_g[e] = make_double4(g.x, g.y, g.z, diag);
+    P.er_q[e] = q;
+}
+
+// jacobian block of edge row e at vertex slot m (0: -u/ly, 1: u/ly)
+__device__ __forceinline__ d3 edge_jac(const double4& g4, int m) {
+    const d3 g = mk(g4.x, g4.y, g4.z);
+    if (m == 1) return g;
+    if (g.x == 0.0 && g.y == 0.0 && g.z == 0.0) return g;  // len <= 1e-12: zero rows
+    return neg(g);
+}
+
+// B2: order-preserving compaction of the contact rows (pair order), their
+// q = c + J (y_k1 - x), warm-start multiplier from the archive, vertex
+// incidence lists; plus every edge row's value / jacobian / diag / q.
+__device__ void ph_rows(const Params& P, int sel, long long narch) {
+    const long long lo = P.blk_lo[blockIdx.x], hi = P.blk_hi[blockIdx.x];
+    const long long nc_total = prefix_of(P.part_c, gridDim.x);
+    long long base = prefix_of(P.part_c, blockIdx.x);
+    const uint64_t* akey = P.arch_key[sel];
+    const double* aval = P.arch_val[sel];
+    for (long long t = lo; t < hi; t += TPB) {
+        const long long p = t + threadIdx.x;
+        const int flag = (p < hi && (P.pflag[p] & PF_CONTACT)) ? 1 : 0;
+        long long tile_tot;
+        const long long pos = base + block_scan(flag, &tile_tot);
+        base += tile_tot;
+        if (!flag) continue;
+        const uint64_t key = P.pkey[p];
+        const int ka = key_ka(key), kb = key_kb(key);
+        int va[3], vb[3];
+        split_ids(ka, kb, P.pids[p], va, vb);
+        const double4 dd = P.pdd[p];
+        double wa[3], wb[3];
+        unpack_weights(ka, kb, P.pw[p], wa, wb);
+        Row c;
+        build_contact(ka, va, kb, vb, wa, wb, dd.w, mk(dd.x, dd.y, dd.z), P.cfg.delta, P.cfg.family,
+                      XLoad{P.x}, c);
+        // fill_diag (constraints.cpp:175-179) and q (lcp.cpp:16-20)
+        double dg = 0.0, q = c.value;
+        for (int m = 0; m < c.nverts; ++m) {
+            const double4 xv = P.x[c.v[m]];
+            dg += xv.w * sqn(c.jac[m]);
+            q += dot(c.jac[m], sub(ld3(P.yk1, c.v[m]), mk(xv.x, xv.y, xv.z)));
+        }
+        double* J = P.c_jac + pos * 12;
+        for (int m = 0; m < 4; ++m) {
+            const d3 j = m < c.nverts ? c.jac[m] : mk(0, 0, 0);
+            J[3 * m] = j.x, J[3 * m + 1] = j.y, J[3 * m + 2] = j.z;
+        }
+        P.c_ids[pos] = make_int4(c.v[0], c.nverts > 1 ? c.v[1] : -1, c.nverts > 2 ? c.v[2] : -1,
+                                 c.nverts > 3 ? c.v[3] : -1);
+        P.c_key[pos] = key;
+        P.c_value[pos] = c.value;
+        P.c_diag[pos] = maxd(dg, 1e-10);
+        P.c_q[pos] = q;
+        // warm start from the archive (resolve.cpp:86-93)
+        const long long at = arch_lower_bound(akey, narch, key);
+        double lam = 0.0;
+        if (at < narch && akey[at] == key) {
+            const double v = aval[at];
+            lam = isnan(v) ? 0.0 : v;
+            P.c_arch[pos] = at;
+        } else {
+            P.c_arch[pos] = -at - 1;
+        }
+        P.c_lambda[pos] = lam;
+        for (int m = 0; m < c.nverts; ++m)
+            if (P.inv_mass[c.v[m]] > 0.0) insert_list(P, c.v[m], (int)(pos * 4 + m));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.g->nc = nc_total;
+    if (P.cfg.edge_constraints)
+        for (long long k = gtid(); k < P.g->ner; k += gstride()) edge_row(P, P.er_edge[k]);
+}
+
+// sorted contact-row entries (4*row + m) incident to v; returns the count and
+// fills buf (capacity cap) when count <= cap
+__device__ __forceinline__ int vertex_entries(const Params& P, int v, int* buf, int cap) {
+    int n = 0;
+    for (int e = P.vhead[v]; e >= 0; e = P.vnext[e]) {
+        if (n < cap) {
+            int j = n - 1;
+            while (j >= 0 && buf[j] > e) buf[j + 1] = buf[j], --j;
+            buf[j + 1] = e;
+        }
+        ++n;
+    }
+    return n;
+}
+
+// k-th smallest entry (0-based) of v's list by repeated selection (large lists)
+__device__ __forceinline__ int vertex_entry_select(const Params& P, int v, int prev) {
+    int best = 0x7fffffff;
+    for (int e = P.vhead[v]; e >= 0; e = P.vnext[e])
+        if (e > prev && e < best) best = e;
+    return best;
+}
+
+// visit contact-row entries of v in ascending row order
+template <typename F>
+__device__ __forceinline__ void for_sorted_entries(const Params& P, int v, F&& f) {
+    constexpr int CAP = 48;
+    int buf[CAP];
+    const int n = vertex_entries(P, v, buf, CAP);
+    if (n <= CAP) {
+        for (int i = 0; i < n; ++i) f(buf[i]);
+    } else {
+        int prev = -1;
+        for (int i = 0; i < n; ++i) {
+            prev = vertex_entry_select(P, v, prev);
+            f(prev);
+        }
+    }
+}
+
+__device__ __forceinline__ void imp_add(d3& a, double s, d3 j) {
+    a.x = a.x + s * j.x;
+    a.y = a.y + s * j.y;
+    a.z = a.z + s * j.z;
+}
+
+// B3: warm-start impulse M^-1 J^T lambda accumulated per vertex in row order
+// (lcp.cpp:16-23: contact rows in pair order, then edge rows in edge order)
+// and the coloring priorities of the contact rows
+__device__ void ph_warm(const Params& P, long long nc) {
+    for (long long v = gtid(); v < P.nv; v += gstride()) {
+        const double im = P.inv_mass[v];
+        d3 a = mk(0, 0, 0);
+        if (im > 0.0) {
+            for_sorted_entries(P, (int)v, [&](int e) {
+                const int row = e >> 2, m = e & 3;
+                const double lam = P.c_lambda[row];
+                if (lam != 0.0) {
+                    const double* J = P.c_jac + (long long)row * 12 + 3 * m;
+                    imp_add(a, im * lam, mk(J[0], J[1], J[2]));
+                }
+            });
+            if (P.cfg.edge_constraints) {
+                for (int k = P.vedge_off[v]; k < P.vedge_off[v + 1]; ++k) {
+                    const int e = P.vedge[k];
+                    if (!P.is_er[e]) continue;
+                    const double lam = P.edge_lambda[e];
+                    if (lam != 0.0) imp_add(a, im * lam, edge_jac(P.er_g[e], P.edges[e].x == v ? 0 : 1));
+                }
+            }
+        }
+        P.imp[v] = make_double4(a.x, a.y, a.z, 0.0);
+    }
+    const uint64_t smix = P.cfg.color_seed * 0x9E3779B97F4A7C15ull;
+    for (long long i = gtid(); i < nc; i += gstride()) {
+        const int4 id = P.c_ids[i];
+        const int vv[4] = {id.x, id.y, id.z, id.w};
+        uint64_t deg = 0;
+        for (int m = 0; m < 4; ++m)
+            if (vv[m] >= 0 && P.inv_mass[vv[m]] > 0.0) deg += (uint64_t)(P.vcnt[vv[m]] - 1);
+        if (deg > 0xFFFFF) deg = 0xFFFFF;
+        P.c_prio[i] = (deg << 44) | (mix64(P.c_key[i] ^ smix) >> 20);
+        P.c_stamp[i] = 0;
+        P.c_color[i] = -1;
+    }
+}
+
+// ============================================================ coloring
+// C (device mode): one Jones-Plassmann round. Uncolored rows that beat every
+// neighbor uncolored at round start take the smallest color not used by
+// neighbors colored in earlier rounds (nor by the incident edge rows).
+__device__ void ph_color_round(const Params& P, long long nc, int k) {
+    for (long long i = gtid(); i < nc; i += gstride()) {
+        if (P.c_stamp[i] != 0) continue;
+        const int4 id = P.c_ids[i];
+        const int vv[4] = {id.x, id.y, id.z, id.w};
+        const uint64_t pi = P.c_prio[i];
+        bool is_max = true;
+        for (int m = 0; m < 4 && is_max; ++m) {
+            const int v = vv[m];
+            if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
+            for (int e = P.vhead[v]; e >= 0; e = P.vnext[e]) {
+                const int j = e >> 2;
+                if (j == i) continue;
+                const int sj = *((volatile int*)&P.c_stamp[j]);
+                if (sj != 0 && sj != k) continue;
+                if (!jp_beats(pi, i, P.c_prio[j], j)) {
+                    is_max = false;
+                    break;
+                }
+            }
+        }
+        if (!is_max) continue;
+        unsigned long long used[4] = {0, 0, 0, 0};
+        bool big = false;
+        auto mark = [&](int c) {
+            if (c < 256) used[c >> 6] |= 1ull << (c & 63);
+            else big = true;
+        };
+        for (int m = 0; m < 4; ++m) {
+            const int v = vv[m];
+            if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
+            for (int e = P.vhead[v]; e >= 0; e = P.vnext[e]) {
+                const int j = e >> 2;
+                if (j == i) continue;
+                const int sj = *((volatile int*)&P.c_stamp[j]);
+                if (sj >= 1 && sj < k) mark(P.c_color[j]);
+            }
+            if (P.cfg.edge_constraints)
+                for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
+                    const int ec = P.edge_color[P.vedge[q]];
+                    if (ec >= 0) mark(ec);
+                }
+        }
+        int col = -1;
+        for (int w = 0; w < 4 && col < 0; ++w)
+            if (~used[w]) col = w * 64 + __ffsll(~used[w]) - 1;
+        if (col < 0 || big) {
+            // > 256 colors around this row: linear search over the neighborhood
+            for (int c = (col < 0 ? 256 : col);; ++c) {
+                bool hit = c < 256 ? ((used[c >> 6] >> (c & 63)) & 1) : false;
+                for (int m = 0; m < 4 && !hit; ++m) {
+                    const int v = vv[m];
+                    if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
+                    for (int e = P.vhead[v]; e >= 0 && !hit; e = P.vnext[e]) {
+                        const int j = e >> 2;
+                        if (j == i) continue;
+                        const int sj = *((volatile int*)&P.c_stamp[j]);
+                        hit = sj >= 1 && sj < k && P.c_color[j] == c;
+                    }
+                    if (P.cfg.edge_constraints)
+                        for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1] && !hit; ++q)
+                            hit = P.edge_color[P.vedge[q]] == c;
+                }
+                if (!hit) {
+                    col = c;
+                    break;
+                }
+            }
+        }
+        P.c_color[i] = col;
+        P.c_stamp[i] = k;
+        atomicAdd(&P.g->colored, 1);
+        atomicMax(&P.g->max_color, col);
+        if (col < P.colcap) atomicAdd(&P.ccount[col], 1);
+        else atomicOr(&P.g->error, ERR_CAP_COLORS);
+    }
+}
+
+// ----------------------------------------------- reference coloring replica
+// mt19937_64 (single device thread)
+struct Mt64 {
+    unsigned long long mt[312];
+    int idx;
+    __device__ void seed(unsigned long long s) {
+        mt[0] = s;
+        for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i;
+        idx = 312;
+    }
+    __device__ unsigned long long next() {
+        if (idx >= 312) {
+            const unsigned long long upper = ~0ull << 31, lower = ~upper;
+            for (int k = 0; k < 312; ++k) {
+                const unsigned long long y = (mt[k] & upper) | (mt[(k + 1) % 312] & lower);
+                mt[k] = mt[(k + 156) % 312] ^ (y >> 1) ^ ((y & 1) ? 0xB5026F5AA96619E9ull : 0ull);
+            }
+            idx = 0;
+        }
+        unsigned long long z = mt[idx++];
+        z ^= (z >> 29) & 0x5555555555555555ull;
+        z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+        z ^= (z << 37) & 0xFFF7EEE000000000ull;
+        z ^= z >> 43;
+        return z;
+    }
+    // libstdc++ uniform_int_distribution<size_t>(0, range-1): Lemire _S_nd
+    __device__ unsigned long long below(unsigned long long range) {
+        unsigned long long g = next();
+        unsigned long long low = g * range, high = __umul64hi(g, range);
+        if (low < range) {
+            const unsigned long long thr = (0ull - range) % range;
+            while (low < thr) {
+                g = next();
+                low = g * range;
+                high = __umul64hi(g, range);
+            }
+        }
+        return high;
+    }
+};
+
+// C (reference mode): color_constraints (constraints.cpp:222-288) replayed on
+// one thread over contact rows [0, nc) and edge rows [nc, nc + ner).
+#define TW_INVARIANT(cond)                   \
+    if (!(cond)) {                           \
+        atomicOr(&P.g->error, ERR_INTERNAL); \
+        P.g->internal_line = __LINE__;       \
+        return;                              \
+    }
+
+__device__ void ph_color_ref(const Params& P, long long nc) {
+    const int* er_index = P.er_index;
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    const long long R = nc + P.g->ner;
+    if (R == 0) {
+        P.g->max_color = -1;
+        return;
+    }
+    int* pool = P.refpool;
+    long long top = 0;
+    auto alloc = [&](long long n) -> int* {
+        if (top + n > P.refpool_cap) {
+            atomicOr(&P.g->error, ERR_CAP_REFPOOL);
+            return nullptr;
+        }
+        int* p = pool + top;
+        top += n;
+        return p;
+    };
+    int* adj_off = alloc(R + 1);
+    if (!adj_off) return;
+    auto row_verts = [&](long long r, int* v) -> int {
+        if (r < nc) {
+            const int4 id = P.c_ids[r];
+            v[0] = id.x, v[1] = id.y, v[2] = id.z, v[3] = id.w;
+            int n = 0;
+            while (n < 4 && v[n] >= 0) ++n;
+            return n;
+        }
+        const int2 e = P.edges[P.er_edge[r - nc]];
+        v[0] = e.x, v[1] = e.y;
+        return 2;
+    };
+    // adjacency: sorted, unique neighbor lists through shared dynamic vertices
+    long long cur = top;
+    for (long long r = 0; r < R; ++r) {
+        adj_off[r] = (int)(cur - top);
+        int vv[4];
+        const int n = row_verts(r, vv);
+        long long start = cur;
+        for (int m = 0; m < n; ++m) {
+            const int v = vv[m];
+            if (!(P.inv_mass[v] > 0.0)) continue;
+            auto push = [&](long long j) {
+                if (cur >= P.refpool_cap) {
+                    atomicOr(&P.g->error, ERR_CAP_REFPOOL);
+                    return;
+                }
+                pool[cur++] = (int)j;
+            };
+            for (int e = P.vhead[v]; e >= 0; e = P.vnext[e]) {
+                const long long j = e >> 2;
+                TW_INVARIANT(j < nc);
+                if (j != r) push(j);
+            }
+            if (P.cfg.edge_constraints)
+                for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
+                    const int e = P.vedge[q];
+                    if (!P.is_er[e]) continue;
+                    TW_INVARIANT(er_index[e] >= 0 && er_index[e] < P.g->ner);
+                    const long long j = nc + er_index[e];
+                    if (j != r) push(j);
+                }
+        }
+        if (P.g->error) return;
+        // insertion sort + unique
+        for (long long i = start + 1; i < cur; ++i) {
+            const int v = pool[i];
+            long long j = i - 1;
+            while (j >= start && pool[j] > v) pool[j + 1] = pool[j], --j;
+            pool[j + 1] = v;
+        }
+        long long w = start;
+        for (long long i = start; i < cur; ++i)
+            if (i == start || pool[i] != pool[i - 1]) pool[w++] = pool[i];
+        cur = w;
+    }
+    adj_off[R] = (int)(cur - top);
+    int* adj = pool + top;
+    top = cur;
+    int* degree = alloc(R);
+    int* order = alloc(R);
+    int* removed = alloc(R);
+    int* used = alloc(R + 1);
+    if (!used) return;
+    int max_deg = 0;
+    for (long long i = 0; i < R; ++i) {
+        degree[i] = adj_off[i + 1] - adj_off[i];
+        removed[i] = 0;
+        if (degree[i] > max_deg) max_deg = degree[i];
+    }
+    // buckets as growable vectors in the pool: (ptr offset, size, cap)
+    int* bptr = alloc(max_deg + 1);
+    int* bsize = alloc(max_deg + 1);
+    int* bcap = alloc(max_deg + 1);
+    if (!bcap) return;
+    for (int d = 0; d <= max_deg; ++d) bptr[d] = -1, bsize[d] = 0, bcap[d] = 0;
+    auto bpush = [&](int d, int x) {
+        if (bsize[d] == bcap[d]) {
+            const int nc2 = bcap[d] ? bcap[d] * 2 : 4;
+            int* nb = alloc(nc2);
+            if (!nb) return;
+            for (int i = 0; i < bsize[d]; ++i) nb[i] = pool[bptr[d] + i];
+            bptr[d] = (int)(nb - pool);
+            bcap[d] = nc2;
+        }
+        pool[bptr[d] + bsize[d]++] = x;
+    };
+    for (long long i = 0; i < R; ++i) bpush(degree[i], (int)i);
+    if (P.g->error) return;
+    Mt64 rng;
+    rng.seed(P.cfg.color_seed);
+    for (long long picked = 0; picked < R; ++picked) {
+        int d = 0, cand = -1;
+        while (cand < 0) {
+            while (d <= max_deg && bsize[d] == 0) ++d;
+            TW_INVARIANT(d <= max_deg);
+            const unsigned long long at = rng.below((unsigned long long)bsize[d]);
+            TW_INVARIANT(at < (unsigned long long)bsize[d] && bptr[d] >= 0);
+            int* b = pool + bptr[d];
+            const int c = b[at];
+            TW_INVARIANT(c >= 0 && c < R);
+            b[at] = b[bsize[d] - 1];
+            --bsize[d];
+            if (!removed[c] && degree[c] == d) cand = c;
+        }
+        removed[cand] = 1;
+        order[picked] = cand;
+        for (int k = adj_off[cand]; k < adj_off[cand + 1]; ++k) {
+            const int nb = adj[k];
+            TW_INVARIANT(nb >= 0 && nb < R);
+            if (!removed[nb]) {
+                TW_INVARIANT(degree[nb] > 0);
+                bpush(--degree[nb], nb);
+            }
+        }
+        if (P.g->error) return;
+    }
+    // colors: -1 initially
+    auto color_of = [&](long long r) -> int {
+        return r < nc ? P.c_color[r] : P.er_color[P.er_edge[r - nc]];
+    };
+    for (long long r = 0; r < nc; ++r) P.c_color[r] = -1;
+    for (long long k = 0; k < P.g->ner; ++k) P.er_color[P.er_edge[k]] = -1;
+    for (long long i = 0; i <= R; ++i) used[i] = -1;
+    int maxc = -1;
+    for (long long it = R - 1; it >= 0; --it) {
+        const int i = order[it];
+        TW_INVARIANT(i >= 0 && i < R);
+        for (int k = adj_off[i]; k < adj_off[i + 1]; ++k) {
+            const int c = color_of(adj[k]);
+            TW_INVARIANT(c < R);
+            if (c >= 0) used[c] = i;
+        }
+        int col = 0;
+        while (used[col] == i) ++col;
+        if (i < nc) P.c_color[i] = col;
+        else P.er_color[P.er_edge[i - nc]] = col;
+        if (col > maxc) maxc = col;
+    }
+    P.g->max_color = maxc;
+}
+
+// D: bucket rows by color. Contact counts ccount come from the coloring
+// (device mode) or are counted here (reference mode, which also buckets the
+// edge rows of this step).
+__device__ void ph_bucket_count(const Params& P, long long nc) {
+    for (long long i = gtid(); i < nc; i += gstride()) atomicAdd(&P.ccount[P.c_color[i]], 1);
+    for (long long k = gtid(); k < P.g->ner; k += gstride())
+        atomicAdd(&P.er_color_cnt[P.er_color[P.er_edge[k]]], 1);
+}
+
+__device__ void ph_bucket_scatter(const Params& P, long long nc, int ncol, bool edges_too) {
+    // every block computes the color prefix (ncol is small); block 0 publishes
+    long long run = 0;
+    for (int base = 0; base < ncol; base += TPB) {
+        const int c = base + threadIdx.x;
+        const long long v = c < ncol ? P.ccount[c] : 0;
+        long long tt;
+        const long long ex = block_scan(v, &tt);
+        if (blockIdx.x == 0 && c < ncol) P.coff[c] = (int)(run + ex);
+        run += tt;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.coff[ncol] = (int)run;
+    if (edges_too) {
+        run = 0;
+        for (int base = 0; base < ncol; base += TPB) {
+            const int c = base + threadIdx.x;
+            const long long v = c < ncol ? P.er_color_cnt[c] : 0;
+            long long tt;
+            const long long ex = block_scan(v, &tt);
+            if (blockIdx.x == 0 && c < ncol) P.er_color_off[c] = (int)(run + ex);
+            run += tt;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) P.er_color_off[ncol] = (int)run;
+    }
+}
+
+__device__ void ph_bucket_place(const Params& P, long long nc, bool edges_too) {
+    // counting down leaves the count tables zeroed for the next step
+    for (long long i = gtid(); i < nc; i += gstride()) {
+        const int c = P.c_color[i];
+        const int slot = atomicSub(&P.ccount[c], 1) - 1;
+        P.c_by_color[P.coff[c] + slot] = (int)i;
+    }
+    if (edges_too)
+        for (long long k = gtid(); k < P.g->ner; k += gstride()) {
+            const int e = P.er_edge[k];
+            const int c = P.er_color[e];
+            const int slot = atomicSub(&P.er_color_cnt[c], 1) - 1;
+            P.er_by_color[P.er_color_off[c] + slot] = e;
+        }
+}
+
+// ================================================================= PGS
+// pgs_sweeps (lcp.cpp:27-42) for one color. Rows of a color share no dynamic
+// vertex, so the parallel update equals the sequential one bit for bit.
+__device__ __forceinline__ void pgs_contact_row(const Params& P, int i) {
+    const int4 id = P.c_ids[i];
+    const int vv[4] = {id.x, id.y, id.z, id.w};
+    const double* J = P.c_jac + (long long)i * 12;
+    double s = 0.0;
+    for (int m = 0; m < 4; ++m) {
+        const int v = vv[m];
+        if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
+        const double4 a = P.imp[v];
+        s += dot(mk(J[3 * m], J[3 * m + 1], J[3 * m + 2]), mk(a.x, a.y, a.z));
+    }
+    const double w = P.c_q[i] + s;
+    const double lam0 = P.c_lambda[i];
+    const double t = lam0 - w / P.c_diag[i];
+    const double lam = 0.0 < t ? t : 0.0;
+    const double d = lam - lam0;
+    if (d != 0.0) {
+        for (int m = 0; m < 4; ++m) {
+            const int v = vv[m];
+            if (v < 0) continue;
+            const double im = P.inv_mass[v];
+            if (!(im > 0.0)) continue;
+            double4 a = P.imp[v];
+            const double sc = im * d;
+            a.x = a.x + sc * J[3 * m];
+            a.y = a.y + sc * J[3 * m + 1];
+            a.z = a.z + sc * J[3 * m + 2];
+            P.imp[v] = a;
+        }
+    }
+    P.c_lambda[i] = lam;
+}
+
+__device__ __forceinline__ void pgs_edge_row(const Params& P, int e) {
+    const int2 ed = P.edges[e];
+    const double4 g4 = P.er_g[e];
+    const d3 j0 = edge_jac(g4, 0), j1 = edge_jac(g4, 1);
+    const double im0 = P.inv_mass[ed.x], im1 = P.inv_mass[ed.y];
+    double s = 0.0;
+    if (im0 > 0.0) {
+        const double4 a = P.imp[ed.x];
+        s += dot(j0, mk(a.x, a.y, a.z));
+    }
+    if (im1 > 0.0) {
+        const double4 a = P.imp[ed.y];
+        s += dot(j1, mk(a.x, a.y, a.z));
+    }
+    const double w = P.er_q[e] + s;
+    const double lam0 = P.edge_lambda[e];
+    const double t = lam0 - w / g4.w;
+    const double lam = 0.0 < t ? t : 0.0;
+    const double d = lam - lam0;
+    if (d != 0.0) {
+        if (im0 > 0.0) {
+            double4 a = P.imp[ed.x];
+            const double sc = im0 * d;
+            a.x = a.x + sc * j0.x, a.y = a.y + sc * j0.y, a.z = a.z + sc * j0.z;
+            P.imp[ed.x] = a;
+        }
+        if (im1 > 0.0) {
+            double4 a = P.imp[ed.y];
+            const double sc = im1 * d;
+            a.x = a.x + sc * j1.x, a.y = a.y + sc * j1.y, a.z = a.z + sc * j1.z;
+            P.imp[ed.y] = a;
+        }
+    }
+    P.edge_lambda[e] = lam;
+}
+
+__device__ void ph_pgs_color(const Params& P, int c, int ncol_contact, int ncol_edge) {
+    const long long c0 = c < ncol_contact ? P.coff[c] : 0, c1 = c < ncol_contact ? P.coff[c + 1] : 0;
+    const long long nci = c1 - c0;
+    long long e0 = 0, e1 = 0;
+    if (P.cfg.edge_constraints && c < ncol_edge) e0 = P.er_color_off[c], e1 = P.er_color_off[c + 1];
+    const long long n = nci + (e1 - e0);
+    for (long long k = gtid(); k < n; k += gstride()) {
+        if (k < nci) pgs_contact_row(P, P.c_by_color[c0 + k]);
+        else pgs_edge_row(P, P.er_by_color[e0 + (k - nci)]);
+    }
+}
+
+// ============================================================== Jacobi
+// projected_jacobi_sweeps (lcp.cpp:44-59): next = max(0, lam - (w*w_r)/diag)
+// for all rows, then impulses applied per vertex in row order.
+__device__ void ph_jacobi_next(const Params& P, long long nc) {
+    const double om = P.cfg.under_relax;
+    for (long long i = gtid(); i < nc; i += gstride()) {
+        const int4 id = P.c_ids[i];
+        const int vv[4] = {id.x, id.y, id.z, id.w};
+        const double* J = P.c_jac + i * 12;
+        double s = 0.0;
+        for (int m = 0; m < 4; ++m) {
+            const int v = vv[m];
+            if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
+            const double4 a = P.imp[v];
+            s += dot(mk(J[3 * m], J[3 * m + 1], J[3 * m + 2]), mk(a.x, a.y, a.z));
+        }
+        const double w = P.c_q[i] + s;
+        const double t = P.c_lambda[i] - om * w / P.c_diag[i];
+        P.c_next[i] = 0.0 < t ? t : 0.0;
+    }
+    if (P.cfg.edge_constraints)
+        for (long long k = gtid(); k < P.g->ner; k += gstride()) {
+            const int e = P.er_edge[k];
+            const int2 ed = P.edges[e];
+            const double4 g4 = P.er_g[e];
+            double s = 0.0;
+            if (P.inv_mass[ed.x] > 0.0) {
+                const double4 a = P.imp[ed.x];
+                s += dot(edge_jac(g4, 0), mk(a.x, a.y, a.z));
+            }
+            if (P.inv_mass[ed.y] > 0.0) {
+                const double4 a = P.imp[ed.y];
+                s += dot(edge_jac(g4, 1), mk(a.x, a.y, a.z));
+            }
+            const double w = P.er_q[e] + s;
+            const double t = P.edge_lambda[e] - om * w / g4.w;
+            P.er_value[e] = 0.0 < t ? t : 0.0;  // er_value reused as the Jacobi "next"
+        }
+}
+
+__device__ void ph_jacobi_apply(const Params& P, long long nc) {
+    for (long long v = gtid(); v < P.nv; v += gstride()) {
+        const double im = P.inv_mass[v];
+        if (!(im > 0.0)) continue;
+        double4 a4 = P.imp[v];
+        d3 a = mk(a4.x, a4.y, a4.z);
+        for_sorted_entries(P, (int)v, [&](int e) {
+            const int row = e >> 2, m = e & 3;
+            const double d = P.c_next[row] - P.c_lambda[row];
+            if (d != 0.0) {
+                const double* J = P.c_jac + (long long)row * 12 + 3 * m;
+                imp_add(a, im * d, mk(J[0], J[1], J[2]));
+            }
+        });
+        if (P.cfg.edge_constraints)
+            for (int k = P.vedge_off[v]; k < P.vedge_off[v + 1]; ++k) {
+                const int e = P.vedge[k];
+                if (!P.is_er[e]) continue;
+                const double d = P.er_value[e] - P.edge_lambda[e];
+                if (d != 0.0) imp_add(a, im * d, edge_jac(P.er_g[e], P.edges[e].x == v ? 0 : 1));
+            }
+        P.imp[v] = make_double4(a.x, a.y, a.z, 0.0);
+    }
+}
+
+__device__ void ph_jacobi_commit(const Params& P, long long nc) {
+    for (long long i = gtid(); i < nc; i += gstride()) P.c_lambda[i] = P.c_next[i];
+    if (P.cfg.edge_constraints)
+        for (long long k = gtid(); k < P.g->ner; k += gstride()) {
+            const int e = P.er_edge[k];
+            P.edge_lambda[e] = P.er_value[e];
+        }
+}
+
+// ============================================================ advance (F)
+// recover_target (lcp.cpp:131-136) + advance (advance.cpp:8-39) + lambda
+// store (resolve.cpp:106-111); resets per-vertex scratch for the next step.
+__device__ void ph_advance(const Params& P, double bound, int step, long long nc, int sel) {
+    const double half_gamma = 0.5 * P.cfg.gamma;
+    for (long long v = gtid(); v < P.nv; v += gstride()) {
+        const double4 x4 = P.x[v];
+        const unsigned long long db = P.dmin[v];
+        P.dmin[v] = INF_BITS;
+        P.vhead[v] = -1;
+        P.vcnt[v] = 0;
+        if (x4.w == 0.0) {  // static
+            P.r[v] = 0.0;
+        } else {
+            const double4 a = P.imp[v];
+            const d3 yk = ld3(P.yk1, (int)v);
+            const d3 y = mk(yk.x + a.x, yk.y + a.y, yk.z + a.z);
+            const d3 xv = mk(x4.x, x4.y, x4.z);
+            const d3 d = sub(y, xv);
+            const double dn = nrm(d);
+            if (dn == 0.0) {
+                P.r[v] = 0.0;
+            } else {
+                const double D = mind(bound, to_d(db));
+                const double limit = half_gamma * D;
+                double alpha = mind(limit / dn, 1.0);
+                d3 disp = scl(alpha, d);
+                if (alpha < 1.0) {
+                    const double dnorm = nrm(disp);
+                    if (dnorm > limit) {
+                        const double s = (limit / dnorm) * (1.0 - 1e-14);
+                        disp = mk(disp.x * s, disp.y * s, disp.z * s);
+                        alpha *= s;
+                    }
+                }
+                P.x[v] = make_double4(xv.x + disp.x, xv.y + disp.y, xv.z + disp.z, x4.w);
+                P.r[v] = P.r[v] * (1.0 - alpha);
+                atomicMax(&P.g->maxdisp_bits, to_b(nrm(disp)));
+            }
+        }
+        atomicMax(&P.g->resid_bits, to_b(P.r[v]));
+        if (P.cfg.record_path) {
+            const double4 xn = P.x[v];
+            double* o = P.path + ((long long)(step + 1) * P.nv + v) * 3;
+            o[0] = xn.x, o[1] = xn.y, o[2] = xn.z;
+        }
+    }
+    // contact multipliers -> archive (update in place; count new keys)
+    long long lo, hi;
+    chunk_of(nc, &lo, &hi);
+    long long nnew = 0;
+    for (long long i = lo + threadIdx.x; i < hi; i += TPB) {
+        const long long at = P.c_arch[i];
+        if (at >= 0) P.arch_val[sel][at] = P.c_lambda[i];
+        else ++nnew;
+    }
+    const long long t = block_sum(nnew);
+    if (threadIdx.x == 0) P.part_k[blockIdx.x] = t;
+}
+
+// G1: ranks of the new keys (pair order == key order) -> staging arrays
+__device__ void ph_arch_rank(const Params& P, long long nc) {
+    long long lo, hi;
+    chunk_of(nc, &lo, &hi);
+    long long base = prefix_of(P.part_k, blockIdx.x);
+    for (long long t = lo; t < hi; t += TPB) {
+        const long long i = t + threadIdx.x;
+        const int f = (i < hi && P.c_arch[i] < 0) ? 1 : 0;
+        long long tt;
+        const long long rk = base + block_scan(f, &tt);
+        base += tt;
+        if (!f) continue;
+        P.new_lb[rk] = -P.c_arch[i] - 1;
+        P.new_key[rk] = P.c_key[i];
+        P.new_val[rk] = P.c_lambda[i];
+    }
+}
+
+// G2: merge old archive + new keys into the other buffer
+__device__ void ph_arch_merge(const Params& P, long long nnew, int sel, long long narch) {
+    const uint64_t* ok = P.arch_key[sel];
+    const double* ov = P.arch_val[sel];
+    uint64_t* nk = P.arch_key[sel ^ 1];
+    double* nvl = P.arch_val[sel ^ 1];
+    for (long long j = gtid(); j < narch; j += gstride()) {
+        // number of new keys with lower bound <= j
+        long long lo = 0, hi = nnew;
+        while (lo < hi) {
+            const long long mid = (lo + hi) >> 1;
+            if (P.new_lb[mid] <= j) lo = mid + 1;
+            else hi = mid;
+        }
+        nk[j + lo] = ok[j];
+        nvl[j + lo] = ov[j];
+    }
+    for (long long r = gtid(); r < nnew; r += gstride()) {
+        nk[P.new_lb[r] + r] = P.new_key[r];
+        nvl[P.new_lb[r] + r] = P.new_val[r];
+    }
+}
+
+// ============================================================ refresh (H)
+// refresh_distances (proximity.cpp:190-202) with the pre-shrink bound, the
+// inactive-pair erase (resolve.cpp:122-123), the vertex bound of the next
+// step (proximity.cpp:204-211) and, when no search follows, the contact
+// predicate of the next linearization.
+__device__ void ph_refresh(const Params& P, double bound, bool next_search, bool erase, int sel,
+                           long long narch) {
+    const long long np = P.g->np;
+    long long lo, hi;
+    chunk_of(np, &lo, &hi);
+    long long ncontact = 0, nact = 0;
+    for (long long p = lo + threadIdx.x; p < hi; p += TPB) {
+        const uint64_t key = P.pkey[p];
+        const int ka = key_ka(key), kb = key_kb(key);
+        int va[3], vb[3];
+        split_ids(ka, kb, P.pids[p], va, vb);
+        Closest c;
+        const int h = pair_closest(ka, va, kb, vb, XLoad{P.x}, c);
+        uint8_t fl = P.pflag[p] & PF_ALL_STATIC;
+        double4 dd;
+        double4 w;
+        if (h != 1) {
+            dd = P.pdd[p];
+            w = P.pw[p];
+            fl |= P.pflag[p] & PF_DEGENERATE;
+        } else {
+            d3 dir = c.dir;
+            if (c.degenerate) {
+                const double4 old = P.pdd[p];
+                const d3 od = mk(old.x, old.y, old.z);
+                if (!is_zero(od)) dir = od;
+            }
+            dd = make_double4(dir.x, dir.y, dir.z, c.dist);
+            w = pack_weights(ka, kb, c);
+            P.pdd[p] = dd;
+            P.pw[p] = w;
+            if (c.degenerate) fl |= PF_DEGENERATE;
+            if (c.dist < bound) fl |= PF_ACTIVE;
+        }
+        if (fl & PF_ACTIVE) {
+            ++nact;
+            if (!next_search) {
+                for (int k = 0; k <= ka; ++k) vertex_min(P, va[k], dd.w);
+                for (int k = 0; k <= kb; ++k) vertex_min(P, vb[k], dd.w);
+            }
+        } else if (erase && narch > 0) {
+            const long long at = arch_lower_bound(P.arch_key[sel], narch, key);
+            if (at < narch && P.arch_key[sel][at] == key)
+                P.arch_val[sel][at] = __longlong_as_double(0x7ff8000000000000ll);
+        }
+        if (!next_search && contact_pred(P, ka, kb, va, vb, dd, w, fl)) {
+            fl |= PF_CONTACT;
+            ++ncontact;
+        }
+        P.pflag[p] = fl;
+    }
+    const long long nct = block_sum(ncontact);
+    const long long na = block_sum(nact);
+    if (threadIdx.x == 0) {
+        P.part_c[blockIdx.x] = nct;
+        P.blk_lo[blockIdx.x] = lo;
+        P.blk_hi[blockIdx.x] = hi;
+        atomicAdd(&P.g->nactive, (int)na);
+        atomicAdd((unsigned long long*)&P.g->pairs_evaluated, (unsigned long long)(hi - lo));
+    }
+}
+
+}  // namespace tw

@@ -1,0 +1,229 @@
+"""GPU parity: every device stage and the device-resident resolve against the
+C oracle on identical inputs, through the C-ABI. Integer/index results
+(pair keys, row and color counts, step counts) must match exactly; FP64
+results are bit-exact by construction (same IEEE operation order, no FMA
+contraction) and are compared with ==."""
+import numpy as np
+import pytest
+
+import pyoracle as O
+from paper_2211_04045_b200 import capi, scenes as S
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = capi.Context(0)
+    yield c
+    c.close()
+
+
+def _mesh(ctx, sc):
+    return capi.Mesh.from_scene(ctx, sc)
+
+
+def _same(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint8) if a.dtype == b.dtype else a, b.view(np.uint8) if a.dtype == b.dtype else b)
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+# ---------------------------------------------------------------- closest
+def _random_pairs(seed, n):
+    rng = np.random.default_rng(seed)
+    xs, kinds, verts = [], [], []
+    for i in range(n):
+        x = rng.uniform(-0.05, 0.05, size=(8, 3))
+        if i % 7 == 0:  # near-parallel / degenerate configurations
+            x[2] = x[0] + rng.uniform(-1e-13, 1e-13, 3)
+            x[3] = x[1] + (x[1] - x[0]) * 1e-3
+        base = 8 * i
+        xs.append(x)
+        k = i % 4
+        ka, kb = [(0, 0), (0, 1), (0, 2), (1, 1)][k]
+        va = [base] if ka == 0 else [base, base + 1]
+        vb = {0: [base + 1], 1: [base + 1, base + 2], 2: [base + 1, base + 2, base + 3]}[kb] if ka == 0 \
+            else [base + 2, base + 3]
+        kinds.append((ka, kb))
+        verts.append(va + [-1] * (3 - len(va)) + vb + [-1] * (3 - len(vb)))
+    return np.concatenate(xs), np.array(kinds, np.int32), np.array(verts, np.int32)
+
+
+def test_closest_bitexact(ctx):
+    x, kinds, verts = _random_pairs(20240811, 4000)
+    out, has = capi.closest_batch(ctx, x, kinds, verts)
+    for i in range(len(kinds)):
+        va = [v for v in verts[i, :3] if v >= 0]
+        vb = [v for v in verts[i, 3:] if v >= 0]
+        r = O.closest(int(kinds[i, 0]), va, int(kinds[i, 1]), vb, x)
+        if r is None:
+            assert has[i] == 0
+            continue
+        assert has[i] == 1
+        want = np.concatenate([[r["distance"]], r["weights_a"], r["weights_b"], r["direction"], [r["degenerate"]]])
+        assert bits_equal(out[i], want), (i, out[i], want)
+
+
+# ----------------------------------------------------------------- search
+def _pairs_equal(g, o):
+    assert np.array_equal(g.keys, o.keys)
+    assert bits_equal(g.dist, o.dist)
+    assert bits_equal(g.wa, o.wa)
+    assert bits_equal(g.wb, o.wb)
+    assert bits_equal(g.dir, o.dir)
+    assert np.array_equal(g.flags, o.flags)
+
+
+@pytest.mark.parametrize("which", ["x", "y"])
+def test_search_battery_bitexact(ctx, which):
+    for sc in S.scene_fixtures(0):
+        m = _mesh(ctx, sc)
+        assert np.array_equal(m.edges, sc.edges)
+        pos = getattr(sc, which)
+        for d_max in (4e-3, 8e-3):
+            g = capi.search(ctx, m, pos, d_max)
+            o = O.search(sc, pos, d_max)
+            _pairs_equal(g, o)
+
+
+def test_search_random_blobs_bitexact(ctx):  # test_proximity.cpp:189-217 on the device
+    rng = np.random.default_rng(42)
+    for _ in range(20):
+        x = rng.uniform(-0.012, 0.012, size=(9, 3))
+        mm = S.make_mesh(x, [(0, 1, 2), (3, 4, 5)], [(6, 7)])
+        sc = S.Scene("blob", x, x, mm.triangles, mm.edges, mm.strand_edges, mm.inv_mass)
+        m = _mesh(ctx, sc)
+        _pairs_equal(capi.search(ctx, m, x, 0.008), O.search(sc, x, 0.008))
+
+
+def test_search_isolated_and_empty(ctx):
+    mm = S.make_mesh([(0, 0, 0), (0.002, 0, 0), (0.01, 0, 0), (0.01, 0.01, 0)], edges=[(2, 3)])
+    sc = S.Scene("iso", mm.positions, mm.positions, mm.triangles, mm.edges, mm.strand_edges, mm.inv_mass)
+    m = _mesh(ctx, sc)
+    _pairs_equal(capi.search(ctx, m, sc.x, 0.02), O.search(sc, sc.x, 0.02))
+    far = S.make_mesh([(0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 0.01), (1, 0, 0.01), (0, 1, 0.01)],
+                      [(0, 1, 2), (3, 4, 5)])
+    sc = S.Scene("far", far.positions, far.positions, far.triangles, far.edges, far.strand_edges, far.inv_mass)
+    assert len(capi.search(ctx, _mesh(ctx, sc), sc.x, 0.004)) == 0
+
+
+def test_search_knot_bitexact(ctx):
+    sc = S.knot_scene(n_along=120, n_across=8, name="small_knot")
+    m = _mesh(ctx, sc)
+    for pos in (sc.x, 0.5 * (sc.x + sc.y)):
+        _pairs_equal(capi.search(ctx, m, pos, 4e-3), O.search(sc, pos, 4e-3))
+
+
+# ---------------------------------------------------------------- refresh
+def test_refresh_and_vertex_bound_bitexact(ctx):
+    for sc in S.scene_fixtures(0)[:9]:
+        m = _mesh(ctx, sc)
+        p0 = O.search(sc, sc.x, 8e-3)
+        mid = sc.x + 0.15 * (sc.y - sc.x)
+        for bound in (8e-3, 3e-3):
+            g = p0.take(len(p0))
+            o = p0.take(len(p0))
+            Dg = capi.refresh(ctx, m, mid, bound, g)
+            O.refresh(sc, mid, bound, o)
+            Do = O.vertex_bound(sc, bound, o, sc.nv)
+            _pairs_equal(g, o)
+            assert bits_equal(Dg, Do)
+
+
+# ---------------------------------------------------------------- advance
+def test_advance_bitexact(ctx):
+    rng = np.random.default_rng(17)
+    n = 5000
+    x = rng.uniform(-1, 1, (n, 3))
+    y = x + rng.uniform(-0.01, 0.01, (n, 3))
+    y[::11] = x[::11]  # zero displacement
+    inv = np.where(rng.uniform(size=n) < 0.1, 0.0, 1.0)
+    D = rng.uniform(0, 0.004, n)
+    r = rng.uniform(0.2, 1.0, n)
+    xg, rg, mg = capi.advance(ctx, inv, y, D, 0.9, x, r)
+    xo, ro, mo = O.advance(inv, y, D, 0.9, x, r)
+    assert bits_equal(xg, xo) and bits_equal(rg, ro) and mg == mo
+
+
+# ---------------------------------------------------------------- resolve
+def _compare_resolve(ctx, sc, **kw):
+    m = _mesh(ctx, sc)
+    xg, sg = capi.resolve(ctx, m, sc.x, sc.y, trace=True, **kw)
+    xo, so = O.resolve(sc, trace=True, **kw)
+    for k in ("steps", "searches", "converged", "start_in_contact", "step_law_violated"):
+        assert sg[k] == so[k], (sc.name, k, sg[k], so[k])
+    assert bits_equal(sg["step_max_disp"], so["step_max_disp"]), sc.name
+    for tg, to in zip(sg["trace"], so["trace"]):
+        for k in ("searched", "num_pairs", "num_contact_rows", "num_edge_rows", "num_colors", "num_active_pairs"):
+            assert tg[k] == to[k], (sc.name, k, tg, to)
+    assert sg["final_residual"] == so["final_residual"], sc.name
+    assert bits_equal(xg, xo), sc.name
+    return sg
+
+
+@pytest.mark.parametrize("coloring", ["reference", "device"])
+def test_resolve_battery_bitexact(ctx, coloring):
+    for sc in S.scene_fixtures(0):
+        _compare_resolve(ctx, sc, coloring_mode=coloring)
+
+
+@pytest.mark.parametrize("kw", [dict(solver="jacobi"), dict(constraint_family="gap"), dict(sweeps=3),
+                                dict(edge_constraints=False), dict(force_fresh_search=True),
+                                dict(eps=0.25), dict(step_limit=4)])
+def test_resolve_options_bitexact(ctx, kw):
+    for sc in [S.fixture_spike_patch(45.0), S.fixture_press(0.012), S.fixture_strand_cross(), S.fixture_particles()]:
+        _compare_resolve(ctx, sc, coloring_mode="reference", **kw)
+
+
+def test_resolve_knot_device_coloring_bitexact(ctx):
+    sc = S.knot_scene(n_along=200, n_across=10, name="small_knot")
+    _compare_resolve(ctx, sc, coloring_mode="device", step_limit=64)
+
+
+def test_resolve_path_is_certified(ctx):
+    for sc in [S.fixture_spike_patch(45.0), S.fixture_press(0.012), S.fixture_tube_twist()]:
+        m = _mesh(ctx, sc)
+        xg, st = capi.resolve(ctx, m, sc.x, sc.y, record_path=True)
+        assert not st["step_law_violated"]
+        assert O.ccd_certify_path(sc, st["path"])[1] == 0
+        assert np.array_equal(st["path"][-1], xg)
+
+
+def test_resolve_validation(ctx):
+    sc = S.fixture_particles()
+    m = _mesh(ctx, sc)
+    bad = sc.y.copy()
+    bad[0, 1] = np.nan
+    with pytest.raises(ValueError):
+        capi.resolve(ctx, m, sc.x, bad)
+    with pytest.raises(ValueError):
+        capi.resolve(ctx, m, sc.x, sc.y, gamma=1.5)
+    with pytest.raises(NotImplementedError):
+        capi.resolve(ctx, m, sc.x, sc.y, solver="al20")
+
+
+def test_resolve_deterministic(ctx):
+    sc = S.knot_scene(n_along=150, n_across=8)
+    m = _mesh(ctx, sc)
+    a, sa = capi.resolve(ctx, m, sc.x, sc.y, step_limit=40)
+    b, sb = capi.resolve(ctx, m, sc.x, sc.y, step_limit=40)
+    assert bits_equal(a, b) and sa["steps"] == sb["steps"]
+
+
+def test_pymodule_resolve_matches_oracle():
+    from paper_2211_04045_b200 import _twoway
+
+    for sc in [S.fixture_spike_patch(45.0), S.fixture_strand_cross()]:
+        xg, st = _twoway.resolve(sc.x, sc.y, sc.triangles, sc.strand_edges, sc.inv_mass, coloring="reference")
+        xo, so = O.resolve(sc)
+        assert st["steps"] == so["steps"] and bits_equal(xg, xo)
+    r = _twoway.vertex_triangle_closest([0.25, 0.25, 0.5], [0, 0, 0], [1, 0, 0], [0, 1, 0])
+    assert abs(r["distance"] - 0.5) < 1e-12
+    with pytest.raises(ValueError):
+        _twoway.resolve(sc.x, sc.y, sc.triangles, bogus=1)
