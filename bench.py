@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""Benchmark of the two-way collision-handling hot path on B200.
+
+One "step" = one resolve(x, y) call (Alg. 1 of arXiv 2211.04045 run to
+convergence: the collision-handling stage of one simulation time step) on the
+synthetic bow knot of BASELINE.json configs[2] (two twisted cloth strips,
+74,800 vertices / 142,044 triangles, tightening target). Metric: collision
+sim steps per second (whole job: all ranks).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU). Every rank resolves its
+own independent knot (a different strip-twist jitter): the path shards only
+across independent scenes, so there is no collective on the data path
+(weak scaling); torch.distributed is used for the start/stop barriers and the
+max-over-ranks of the device-timed region only.
+
+--impl reference times the reference algorithm on the host CPU: the C oracle
+(oracle/, a clean-room restatement — the reference itself needs Eigen, which is
+absent, so it cannot be built here), single-threaded like the reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "collision sim steps/s (resolve calls/s) at the 142K-tri bow knot"
+PAPER_COST_S = 0.034  # bow knot collision cost per time step (RTX 2080 Ti, paper Table 1)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scene", choices=["bow", "reef"], default="bow")
+    ap.add_argument("--coloring", choices=["device", "reference"], default="device")
+    ap.add_argument("--cpu-sample-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def make_scene(name, rank):
+    from paper_2211_04045_b200 import scenes
+
+    jitter = None if rank == 0 else rank
+    if name == "bow":
+        return scenes.bow_knot(jitter_seed=jitter)
+    return scenes.reef_knot(jitter_seed=jitter)
+
+
+def scene_config(sc, args):
+    return {"workload": f"{sc.name}: {sc.nv} vertices, {len(sc.triangles)} triangles, {len(sc.edges)} edges; "
+                        "two cloth strips laid face to face (2.5 mm apart, 3 mm mesh) along a twisted (2,3) "
+                        "torus-knot band; tightening target presses them to a 0.2 mm gap where the knot is "
+                        "tightest and slides one 3 mm along the other (scenes.ply_knot)",
+            "scene": args.scene, "vertices": sc.nv, "triangles": int(len(sc.triangles)),
+            "edges": int(len(sc.edges)), "dt_note": "kinematic tightening target (no dynamics step)",
+            "solver": "pgs, 1 sweep", "coloring": args.coloring,
+            "params": {"d_min": 2e-3, "d_max": 4e-3, "delta": 5e-4, "gamma": 0.9, "eps": 1e-4,
+                       "step_limit": 512},
+            "l2": "each resolve rebuilds its LBVH and pair set (>= 10^8 B working set vs the 126 MB L2); "
+                  "inputs re-uploaded every e2e step",
+            "parallelism": "independent scenes per rank (no collective)"}
+
+
+RESOLVE_KW = dict(delta=5e-4, coloring_mode="device")  # knots: delta = 0.5 mm
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.out = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.out.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def bytes_per_resolve(trace, sc, sweeps=1):
+    """Algorithmic HBM bytes of one resolve, from its per-step trace (SURVEY.md
+    §8(d) per-unit contract): refresh 98 B/pair,
+    linearize 210 B/contact row + 88 B/edge row, assemble 136 B/row + 72 B/vertex,
+    PGS 336 B/contact row + 184 B/edge row per sweep, advance 128 B/vertex; a
+    search step adds the LBVH refit (64 B per node written, 2 nodes per
+    primitive), 24 B per vertex of positions and 98 B per emitted pair."""
+    nv, nt, ne = sc.nv, len(sc.triangles), len(sc.edges)
+    total = 0
+    for t in trace:
+        P, C, ER = t["num_pairs"], t["num_contact_rows"], t["num_edge_rows"]
+        R = C + ER
+        b = 98 * P + 210 * C + 88 * ER + 136 * R + 72 * nv + (336 * C + 184 * ER) * sweeps + 128 * nv
+        if t["searched"]:
+            b += 98 * P + 64 * 2 * (nt + ne) + 24 * nv
+        total += b
+    return total
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_2211_04045_b200 import capi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sc = make_scene(args.scene, rank)
+    stream = torch.cuda.current_stream()
+    ctx = capi.Context(local, stream=stream.cuda_stream)
+    mesh = capi.Mesh.from_scene(ctx, sc)
+    kw = dict(RESOLVE_KW, coloring_mode=args.coloring)
+    d_x = torch.from_numpy(sc.x).cuda()
+    d_y = torch.from_numpy(sc.y).cuda()
+    d_out = torch.empty_like(d_x)
+    h_x = torch.from_numpy(sc.x).pin_memory()
+    h_y = torch.from_numpy(sc.y).pin_memory()
+    h_out = torch.empty_like(h_x).pin_memory()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    # warm-up (capacity growth happens here), and one traced call for the
+    # roofline bytes / step counts (identical in every call: deterministic)
+    for _ in range(max(args.warmup, 3)):
+        capi.resolve_device_ptr(ctx, mesh, d_x.data_ptr(), d_y.data_ptr(), d_out.data_ptr(), **kw)
+    _, st_tr = capi.resolve(ctx, mesh, sc.x, sc.y, trace=True, **kw)
+    algo_bytes = bytes_per_resolve(st_tr["trace"], sc)
+    phases = {k: [round(v[0], 3), v[1]] for k, v in capi.phase_profile(ctx).items()}
+
+    # ---- device-resident throughput (inputs already in HBM)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.kernel_launches
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kernel_ms, steps_sum, searches_sum, pairs_eval = [], 0, 0, 0
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)  # L2 flush between timed iterations (outside the events)
+        evs[i][0].record(stream)
+        st = capi.resolve_device_ptr(ctx, mesh, d_x.data_ptr(), d_y.data_ptr(), d_out.data_ptr(), **kw)
+        evs[i][1].record(stream)
+        kernel_ms.append(st["kernel_ms"])
+        steps_sum += st["steps"]
+        searches_sum += st["searches"]
+        pairs_eval += st["pairs_evaluated"]
+    torch.cuda.synchronize()
+    launches = ctx.kernel_launches - launches0
+    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+    # ---- end to end through the C-ABI with host buffers (H2D x, y and D2H x every step)
+    e2e_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    xin, yin, xo = h_x.numpy(), h_y.numpy(), h_out.numpy()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        e2e_evs[i][0].record(stream)
+        _ = capi.resolve(ctx, mesh, xin, yin, **kw)[0]
+        e2e_evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_evs)
+    clk = clocks.stop()
+    barrier()
+
+    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms_max, e2e_ms_max = float(t[0]), float(t[1])
+    value = world * args.steps / (dev_ms_max / 1e3)
+    e2e_value = world * args.steps / (e2e_ms_max / 1e3)
+    kern_avg_ms = sum(kernel_ms) / len(kernel_ms)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = algo_bytes / (kern_avg_ms / 1e3) / 1e9
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_ms_max / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": round(value * PAPER_COST_S, 3),
+            "baseline_note": "vs_baseline = value / (1 / 0.034 s): the paper's bow-knot collision cost per time "
+                             "step on an RTX 2080 Ti (BASELINE.md section 2; different knot asset and GPU)",
+            "dtype": "f64", "data": "synthetic",
+            "config": scene_config(sc, args),
+            "resolve": {"alg1_steps_per_call": steps_sum / args.steps, "searches_per_call": searches_sum / args.steps,
+                        "final_pairs": st["num_pairs"], "pairs_evaluated_per_call": pairs_eval / args.steps,
+                        "kernel_ms": round(kern_avg_ms, 4), "setup_ms": round(st["setup_ms"], 4),
+                        "phase_ms_count": phases,
+                        "two_way_steps_per_s": round(world * steps_sum / (dev_ms_max / 1e3), 1),
+                        "ccd_pairs_per_s": round(world * pairs_eval / (dev_ms_max / 1e3), 1)},
+            "e2e": {"value": round(e2e_value, 3), "unit": "steps/s", "h2d_bytes_per_step": 2 * sc.nv * 24,
+                    "d2h_bytes_per_step": sc.nv * 24 + 160},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": "tw::k_resolve (persistent cooperative Alg.-1 kernel)",
+                         "algorithmic_bytes_per_launch": algo_bytes,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+            "clocks": clk,
+        }
+    if dist is not None:
+        dist.destroy_process_group()
+    return out, sc, st_tr
+
+
+def cpu_baseline(sc, gpu_trace, sample_steps):
+    """Oracle (single-threaded restatement of the reference) on the first
+    `sample_steps` Alg.-1 steps of the same resolve, extrapolated with the
+    per-step search pattern the (bit-identical) device run took."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    t0 = time.perf_counter()
+    _, st = pyoracle.resolve(sc, step_limit=sample_steps, trace=True, **RESOLVE_KW)
+    dt = time.perf_counter() - t0
+    nsteps = len(gpu_trace)
+    per_step = dt / st["steps"]
+    est = per_step * nsteps  # every sampled step includes a search (step 0 always searches)
+    searches = sum(t["searched"] for t in gpu_trace)
+    return {"value": round(1.0 / est, 6), "unit": "steps/s", "cores": 1, "kind": "port",
+            "sample": f"first {st['steps']} Alg.-1 step(s) of the same bow-knot resolve on the C oracle "
+                      f"({dt:.1f} s, search included), extrapolated to the {nsteps} steps / {searches} searches "
+                      f"the device run takes",
+            "seconds_per_alg1_step": round(per_step, 3)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    sc = make_scene(args.scene, 0)
+    trace_path = os.path.join(ROOT, "profiles", f"{args.scene}_knot_trace.json")
+    trace = json.load(open(trace_path)) if os.path.exists(trace_path) else None
+    samples = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        _, st = pyoracle.resolve(sc, step_limit=args.cpu_sample_steps, trace=True, **RESOLVE_KW)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            samples.append(dt / st["steps"])
+    per_step = statistics.median(samples)
+    nsteps = len(trace) if trace else 1
+    value = 1.0 / (per_step * nsteps)
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": scene_config(sc, args),
+            "cpu_baseline": {"value": round(value, 6), "unit": "steps/s", "cores": 1, "kind": "port",
+                             "sample": f"each step: the first {args.cpu_sample_steps} Alg.-1 step(s) (search "
+                                       f"included) of the bow-knot resolve on the single-threaded C oracle, "
+                                       f"extrapolated to the {nsteps} steps of the full resolve "
+                                       f"(profiles/{args.scene}_knot_trace.json)"},
+            "e2e": {"value": round(value, 6), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        out = run_reference(args)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    out, sc, st_tr = run_ours(args)
+    if out is None:
+        return
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    with open(os.path.join(ROOT, "profiles", f"{args.scene}_knot_trace.json"), "w") as f:
+        json.dump(st_tr["trace"], f)
+    if not args.no_cpu_baseline and out["n_gpus"] == 1:
+        out["cpu_baseline"] = cpu_baseline(sc, st_tr["trace"], args.cpu_sample_steps)
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -82,6 +82,8 @@ typedef struct {
     double device_ms;         /* CUDA-event time of the device resolve (no H2D/D2H) */
     int32_t kernel_launches;  /* kernels this call launched */
     int32_t retries;          /* capacity regrow restarts */
+    double kernel_ms;         /* CUDA-event time of the persistent resolve kernel alone */
+    double setup_ms;          /* unpack + LBVH build before it */
 } tw_resolve_stats;
 
 /* per-step diagnostics (same fields as the oracle's trace) */
@@ -110,6 +112,10 @@ void tw_ctx_destroy(tw_ctx* ctx);
 const char* tw_last_error(const tw_ctx* ctx);
 /* kernels launched by this context since creation */
 int64_t tw_ctx_kernel_launches(const tw_ctx* ctx);
+/* Per-phase wall time of the last resolve (CTA 0, barrier to barrier):
+ * call-site ids (source line & 127 in tw_kernels.cu), milliseconds and
+ * counts; returns the number of sites (entries beyond cap are not written). */
+int32_t tw_ctx_phase_profile(const tw_ctx* ctx, int32_t* sites, double* ms, int32_t* counts, int32_t cap);
 
 /* Topology upload (once per scene). Runs MeshState::finalize's edge
  * derivation (mesh.cpp:10-33) on the explicit, strand and triangle edges:

@@ -439,6 +439,19 @@ static inline uint64_t contact_prio(uint64_t key, uint64_t seed) {
     return or_mix64(key ^ (seed * 0x9E3779B97F4A7C15ull));
 }
 
+/* the n-th (0-based) color not in the (unsorted) list */
+static int nth_free(const int* cols, int k, int n) {
+    for (int c = 0;; ++c) {
+        int hit = 0;
+        for (int i = 0; i < k; ++i)
+            if (cols[i] == c) {
+                hit = 1;
+                break;
+            }
+        if (!hit && n-- == 0) return c;
+    }
+}
+
 /* smallest color not in the (unsorted) list */
 static int smallest_free(const int* cols, int k) {
     for (int c = 0;; ++c) {
@@ -585,35 +598,27 @@ int or_color_device(or_row* rows, int64_t n, const double* inv_mass, int nv, uin
     }
     int cap = 64;
     int* cols = (int*)or_xmalloc((size_t)cap * sizeof(int));
+    /* Speculative greedy rounds: every uncolored row proposes the smallest
+     * color unused by its already-colored neighbors (and incident edge rows);
+     * a proposal is kept unless an uncolored neighbor with the same proposal
+     * has the higher (prio, index). */
+    int* tent = (int*)or_xmalloc(((size_t)nc + 1) * sizeof(int));
     int64_t remaining = nc;
     for (int r = 1; remaining > 0; ++r) {
-        int nw = 0;
         for (int64_t i = 0; i < nc; ++i) {
             if (round[i] != 0) continue;
-            int is_max = 1;
-            for (int m = 0; m < rows[i].nverts && is_max; ++m) {
-                const int v = rows[i].verts[m];
-                if (!(inv_mass[v] > 0.0)) continue;
-                for (int64_t a = voff[v]; a < voff[v + 1]; ++a) {
-                    const int j = vrows[a];
-                    if (j == i || round[j] != 0) continue;
-                    if (!jp_beats(prio[i], i, prio[j], j)) {
-                        is_max = 0;
-                        break;
-                    }
-                }
-            }
-            if (is_max) winners[nw++] = (int)i;
-        }
-        for (int w = 0; w < nw; ++w) {
-            const int i = winners[w];
             int k = 0;
+            uint64_t unc = 0; /* uncolored neighbor entries (with multiplicity) */
             for (int m = 0; m < rows[i].nverts; ++m) {
                 const int v = rows[i].verts[m];
                 if (!(inv_mass[v] > 0.0)) continue;
                 for (int64_t a = voff[v]; a < voff[v + 1]; ++a) {
                     const int j = vrows[a];
-                    if (j == i || round[j] <= 0) continue;
+                    if (j == i) continue;
+                    if (round[j] == 0) {
+                        unc += jp_beats(prio[j], j, prio[i], i);
+                        continue;
+                    }
                     if (k == cap) cols = (int*)or_xrealloc(cols, (size_t)(cap *= 2) * sizeof(int));
                     cols[k++] = rows[j].color;
                 }
@@ -625,12 +630,38 @@ int or_color_device(or_row* rows, int64_t n, const double* inv_mass, int nv, uin
                         cols[k++] = edge_color[e];
                     }
             }
-            rows[i].color = smallest_free(cols, k);
-            if (rows[i].color + 1 > ncolors) ncolors = rows[i].color + 1;
+            /* propose the rank-th free color, rank = number of uncolored
+             * neighbor entries that beat this row: a clique of uncolored rows
+             * takes distinct colors in priority order within one round */
+            tent[i] = nth_free(cols, k, (int)unc);
         }
-        for (int w = 0; w < nw; ++w) round[winners[w]] = r;
+        int nw = 0;
+        for (int64_t i = 0; i < nc; ++i) {
+            if (round[i] != 0) continue;
+            int lose = 0;
+            for (int m = 0; m < rows[i].nverts && !lose; ++m) {
+                const int v = rows[i].verts[m];
+                if (!(inv_mass[v] > 0.0)) continue;
+                for (int64_t a = voff[v]; a < voff[v + 1]; ++a) {
+                    const int j = vrows[a];
+                    if (j == i || round[j] != 0) continue;
+                    if (tent[j] == tent[i] && jp_beats(prio[j], j, prio[i], i)) {
+                        lose = 1;
+                        break;
+                    }
+                }
+            }
+            if (!lose) winners[nw++] = (int)i;
+        }
+        for (int w = 0; w < nw; ++w) {
+            const int i = winners[w];
+            rows[i].color = tent[i];
+            round[i] = r;
+            if (tent[i] + 1 > ncolors) ncolors = tent[i] + 1;
+        }
         remaining -= nw;
     }
+    free(tent);
     free(cols);
     free(prio);
     free(round);

@@ -46,7 +46,8 @@ class Stats(C.Structure):
         ("stagnated", C.c_int32), ("start_in_contact", C.c_int32),
         ("step_law_violated", C.c_int32), ("num_pairs", C.c_int32),
         ("pairs_evaluated", C.c_int64), ("rows_solved", C.c_int64), ("device_ms", C.c_double),
-        ("kernel_launches", C.c_int32), ("retries", C.c_int32),
+        ("kernel_launches", C.c_int32), ("retries", C.c_int32), ("kernel_ms", C.c_double),
+        ("setup_ms", C.c_double),
     ]
 
 
@@ -60,7 +61,7 @@ class StepTrace(C.Structure):
 
 EXPORTS = [
     "tw_abi_version", "tw_default_config", "tw_ctx_create", "tw_ctx_destroy", "tw_last_error",
-    "tw_ctx_kernel_launches", "tw_mesh_create", "tw_mesh_num_edges", "tw_mesh_edges",
+    "tw_ctx_kernel_launches", "tw_ctx_phase_profile", "tw_mesh_create", "tw_mesh_num_edges", "tw_mesh_edges",
     "tw_mesh_destroy", "tw_resolve", "tw_resolve_device", "tw_stage_closest", "tw_stage_search",
     "tw_stage_refresh", "tw_stage_linearize", "tw_stage_color", "tw_stage_backward",
     "tw_stage_advance",
@@ -220,6 +221,34 @@ def resolve_device_ptr(ctx: Context, mesh: Mesh, d_x: int, d_y: int, d_out: int,
     ctx.check(lib().tw_resolve_device(ctx.h, mesh.h, C.c_void_p(d_x), C.c_void_p(d_y), C.byref(cfg),
                                       C.c_void_p(d_out), C.byref(st)))
     return {k: getattr(st, k) for k, _ in Stats._fields_}
+
+
+def phase_profile(ctx: Context):
+    """Per-phase time of the last resolve: {phase name: (ms, count)} from the
+    persistent kernel's CTA-0 barrier timestamps. Call sites are mapped to the
+    phase function called just before each barrier in csrc/tw_kernels.cu."""
+    import re
+
+    L = lib()
+    L.tw_ctx_phase_profile.restype = C.c_int32
+    L.tw_ctx_phase_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]
+    sites = np.zeros(128, np.int32)
+    ms = np.zeros(128)
+    cnt = np.zeros(128, np.int32)
+    n = L.tw_ctx_phase_profile(ctx.h, _p(sites), _p(ms), _p(cnt), 128)
+    src = open(os.path.join(_HERE, "csrc", "tw_kernels.cu")).read().splitlines()
+    names = {}
+    for i, line in enumerate(src, start=1):
+        if line.strip() == "SYNC();":
+            prev = src[i - 2]
+            m = re.search(r"(ph_[a-z_]+)", prev)
+            names[i & 127] = m.group(1) if m else f"line{i}"
+    out = {}
+    for k in range(min(n, 128)):
+        name = names.get(int(sites[k]), f"site{int(sites[k])}")
+        a, b = out.get(name, (0.0, 0))
+        out[name] = (a + float(ms[k]), b + int(cnt[k]))
+    return out
 
 
 def closest_batch(ctx: Context, x, kinds, verts):

@@ -64,7 +64,7 @@ struct tw_ctx {
     int sm_count = 0;
     int nblocks = 0;
     long long launches = 0;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk = nullptr;
     // capacities
     long long pcap = 0;
     int K = 64;
@@ -77,7 +77,8 @@ struct tw_ctx {
     DevMem ly, is_er, er_edge, er_index, er_value, er_g, er_q, edge_lambda, er_color, er_by_color, er_color_off,
         er_color_cnt;
     DevMem pkey, pids, pdd, pw, pflag, qcount, qslot;
-    DevMem c_key, c_ids, c_jac, c_value, c_diag, c_q, c_lambda, c_next, c_color, c_stamp, c_arch, c_prio, c_by_color;
+    DevMem c_key, c_ids, c_jac, c_value, c_diag, c_q, c_lambda, c_next, c_color, c_stamp, c_arch, c_prio, c_by_color,
+        c_tent;
     DevMem vnext;
     DevMem ccount, coff;
     DevMem arch_key0, arch_key1, arch_val0, arch_val1, new_lb, new_key, new_val;
@@ -89,6 +90,7 @@ struct tw_ctx {
     // TW_DEBUG progress markers (host-mapped)
     int* dbg_host = nullptr;
     int* dbg_dev = nullptr;
+    Globals last{};  // device globals of the last resolve (phase profile)
 };
 
 struct tw_mesh {
@@ -218,6 +220,7 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     if (cfg.solver == TW_SOLVER_JACOBI) CK(ctx->c_next.ensure(P * 8));
     CK(ctx->c_color.ensure(P * 4));
     CK(ctx->c_stamp.ensure(P * 4));
+    CK(ctx->c_tent.ensure(P * 4));
     CK(ctx->c_arch.ensure(P * 8));
     CK(ctx->c_prio.ensure(P * 8));
     CK(ctx->c_by_color.ensure(P * 4));
@@ -321,6 +324,7 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.c_next = ctx->c_next.as<double>();
     P.c_color = ctx->c_color.as<int>();
     P.c_stamp = ctx->c_stamp.as<int>();
+    P.c_tent = ctx->c_tent.as<int>();
     P.c_arch = ctx->c_arch.as<long long>();
     P.c_prio = ctx->c_prio.as<uint64_t>();
     P.c_by_color = ctx->c_by_color.as<int>();
@@ -376,12 +380,17 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
                 double* d_out, tw_resolve_stats* st, double* smd_host, double* path_host, tw_step_trace* trace_host) {
     Globals G;
     int retries = 0;
-    float dev_ms = 0.f;
+    float dev_ms = 0.f, kern_ms = 0.f;
+    const long long launches0 = ctx->launches;
     for (;;) {
         int rc = ensure_buffers(ctx, m, cfg);
         if (rc) return rc;
         Params P = make_params(ctx, m, cfg);
         CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), ctx->stream));
+        // color tables return to zero at the end of every step; an attempt
+        // aborted for capacity growth may leave counts behind
+        CK(cudaMemsetAsync(ctx->ccount.p, 0, (size_t)ctx->colcap * 4, ctx->stream));
+        CK(cudaMemsetAsync(ctx->er_color_cnt.p, 0, (size_t)ctx->colcap * 4, ctx->stream));
         CK(cudaEventRecord(ctx->ev0, ctx->stream));
         launch_setup(ctx->stream, m->nv, d_xs, d_ys, m->d_inv_mass.as<double>(), P.x, const_cast<double4*>(P.yk1),
                      P.r, P.dmin, P.vhead, P.vcnt, P.imp, &P.g->nonfinite, m->ne, P.edges,
@@ -390,12 +399,14 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
         ctx->launches += launch_count_last();
         rc = build_bvhs(ctx, m);
         if (rc) return rc;
+        CK(cudaEventRecord(ctx->evk, ctx->stream));
         CK(coop_resolve(ctx->stream, P, ctx->nblocks));
         ctx->launches += 1;
         CK(cudaEventRecord(ctx->ev1, ctx->stream));
         CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof(Globals), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         CK(cudaEventElapsedTime(&dev_ms, ctx->ev0, ctx->ev1));
+        CK(cudaEventElapsedTime(&kern_ms, ctx->evk, ctx->ev1));
         if (G.nonfinite) return fail(ctx, TW_EINVAL, "resolve: non-finite input positions");
         if (G.error & ERR_TIMEOUT) return fail(ctx, TW_ETIMEOUT, "resolve: device watchdog fired");
         if (G.error & ERR_INTERNAL)
@@ -413,6 +424,7 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
         if (G.error & ERR_CAP_COLORS) ctx->colcap *= 4;
         if (G.error & ERR_CAP_REFPOOL) ctx->refpool_cap *= 4;
     }
+    ctx->last = G;
     launch_pack(ctx->stream, m->nv, ctx->x.as<double4>(), d_out);
     ctx->launches += launch_count_last();
     std::memset(st, 0, sizeof *st);
@@ -428,7 +440,10 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
     st->pairs_evaluated = G.pairs_evaluated;
     st->rows_solved = G.rows_solved;
     st->device_ms = dev_ms;
+    st->kernel_ms = kern_ms;
+    st->setup_ms = dev_ms - kern_ms;
     st->retries = retries;
+    st->kernel_launches = (int32_t)(ctx->launches - launches0);
     if (smd_host && G.steps > 0)
         CK(cudaMemcpyAsync(smd_host, ctx->smd.p, (size_t)G.steps * 8, cudaMemcpyDeviceToHost, ctx->stream));
     if (trace_host && G.steps > 0) {
@@ -518,6 +533,7 @@ int tw_ctx_create(int device, void* stream, tw_ctx** out) {
     }
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
+    cudaEventCreate(&ctx->evk);
     if (const char* d = std::getenv("TW_DEBUG"); d && d[0] == '1') {
         if (cudaHostAlloc((void**)&ctx->dbg_host, MAX_BLOCKS * sizeof(int), cudaHostAllocMapped) == cudaSuccess) {
             std::memset(ctx->dbg_host, 0xff, MAX_BLOCKS * sizeof(int));
@@ -537,7 +553,8 @@ void tw_ctx_destroy(tw_ctx* ctx) {
                      &ctx->er_q, &ctx->edge_lambda, &ctx->er_color, &ctx->er_by_color, &ctx->er_color_off,
                      &ctx->er_color_cnt, &ctx->pkey, &ctx->pids, &ctx->pdd, &ctx->pw, &ctx->pflag, &ctx->qcount,
                      &ctx->qslot, &ctx->c_key, &ctx->c_ids, &ctx->c_jac, &ctx->c_value, &ctx->c_diag, &ctx->c_q,
-                     &ctx->c_lambda, &ctx->c_next, &ctx->c_color, &ctx->c_stamp, &ctx->c_arch, &ctx->c_prio,
+                     &ctx->c_lambda, &ctx->c_next, &ctx->c_color, &ctx->c_stamp, &ctx->c_tent, &ctx->c_arch,
+                     &ctx->c_prio,
                      &ctx->c_by_color, &ctx->vnext, &ctx->ccount, &ctx->coff, &ctx->arch_key0, &ctx->arch_key1,
                      &ctx->arch_val0, &ctx->arch_val1, &ctx->new_lb, &ctx->new_key, &ctx->new_val, &ctx->refpool,
                      &ctx->part_q, &ctx->part_c, &ctx->part_k, &ctx->blk_lo, &ctx->blk_hi, &ctx->globals, &ctx->box,
@@ -546,6 +563,7 @@ void tw_ctx_destroy(tw_ctx* ctx) {
     for (DevMem* d : all) d->release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->evk) cudaEventDestroy(ctx->evk);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -747,6 +765,21 @@ int tw_resolve_device(tw_ctx* ctx, tw_mesh* m, const double* d_x, const double* 
 }
 
 // ---------------------------------------------------------------- stages
+int32_t tw_ctx_phase_profile(const tw_ctx* ctx, int32_t* sites, double* ms, int32_t* counts, int32_t cap) {
+    if (!ctx) return 0;
+    int n = 0;
+    for (int i = 0; i < 128; ++i) {
+        if (!ctx->last.phase_cnt[i]) continue;
+        if (n < cap) {
+            sites[n] = i;
+            ms[n] = ctx->last.phase_ns[i] * 1e-6;
+            counts[n] = (int32_t)ctx->last.phase_cnt[i];
+        }
+        ++n;
+    }
+    return n;
+}
+
 int tw_stage_closest(tw_ctx* ctx, int32_t nv, const double* x, int64_t n, const int32_t* kinds, const int32_t* verts,
                      double* out, int32_t* has) {
     if (!ctx || nv < 0 || n < 0) return fail(ctx, TW_EINVAL, "closest: bad sizes");

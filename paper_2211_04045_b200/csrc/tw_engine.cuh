@@ -74,6 +74,10 @@ struct Globals {
     double final_residual;
     long long pairs_evaluated;
     long long rows_solved;
+    // phase profile (CTA 0 barrier-to-barrier wall time per call site)
+    unsigned long long phase_t0;
+    unsigned long long phase_ns[128];
+    unsigned int phase_cnt[128];
 };
 
 struct Config {
@@ -148,6 +152,7 @@ struct Params {
     double* c_lambda;
     double* c_next;  // Jacobi
     int* c_color;
+    int* c_tent;     // coloring proposals
     int* c_stamp;
     long long* c_arch;  // archive index, or -(lower_bound)-1
     uint64_t* c_prio;

@@ -256,6 +256,8 @@ __device__ bool prologue(const Params& P) {
 // grid barrier), so the host only sees the final state.
 // progress marker (TW_DEBUG=1): the last phase each CTA completed, written to
 // host-mapped memory so it survives a device fault
+// Phase profile: CTA 0 accumulates the wall time (globaltimer) between its
+// barrier exits per call site (slot = source line & 127).
 #define SYNC()                                                                    \
     do {                                                                          \
         if (P.dbg && threadIdx.x == 0) {                                          \
@@ -263,6 +265,12 @@ __device__ bool prologue(const Params& P) {
             __threadfence_system();                                               \
         }                                                                         \
         if (!grid_sync(g)) return;                                                \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                \
+            const unsigned long long now_ = global_ns();                          \
+            g->phase_ns[__LINE__ & 127] += now_ - g->phase_t0;                    \
+            g->phase_cnt[__LINE__ & 127] += 1;                                    \
+            g->phase_t0 = now_;                                                   \
+        }                                                                         \
     } while (0)
 
 __global__ void __launch_bounds__(TPB) k_resolve(Params P) {
@@ -270,6 +278,7 @@ __global__ void __launch_bounds__(TPB) k_resolve(Params P) {
     int dbg_step = 0;
     if (g->nonfinite || g->error) return;  // non-finite input detected by k_unpack
     if (!prologue(P)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) g->phase_t0 = global_ns();
     const Config& C = P.cfg;
     double bound = 0.0;  // forces a search on step 0
     int searches = 0;
@@ -323,7 +332,9 @@ __global__ void __launch_bounds__(TPB) k_resolve(Params P) {
             ncol_c = ncol_e = ncol;
         } else {
             for (int k = 1; *((volatile int*)&g->colored) < nc; ++k) {
-                ph_color_round(P, nc, k);
+                ph_color_propose(P, nc, k);
+                SYNC();
+                ph_color_finalize(P, nc, k);
                 SYNC();
             }
             ncol_c = g->max_color + 1;

@@ -593,17 +593,20 @@ __device__ void ph_warm(const Params& P, long long nc) {
 }
 
 // ============================================================ coloring
-// C (device mode): one Jones-Plassmann round. Uncolored rows that beat every
-// neighbor uncolored at round start take the smallest color not used by
-// neighbors colored in earlier rounds (nor by the incident edge rows).
-__device__ void ph_color_round(const Params& P, long long nc, int k) {
+// C (device mode), speculative greedy coloring. Round k, propose: every row
+// still uncolored proposes the smallest color not used by neighbors colored in
+// earlier rounds (nor by the incident edge rows). Finalize: a proposal is kept
+// unless an uncolored-at-round-start neighbor proposed the same color and has
+// the higher (priority, index). Typically converges in a handful of rounds.
+__device__ void ph_color_finalize(const Params& P, long long nc, int k) {
     for (long long i = gtid(); i < nc; i += gstride()) {
         if (P.c_stamp[i] != 0) continue;
         const int4 id = P.c_ids[i];
         const int vv[4] = {id.x, id.y, id.z, id.w};
         const uint64_t pi = P.c_prio[i];
-        bool is_max = true;
-        for (int m = 0; m < 4 && is_max; ++m) {
+        const int ti = P.c_tent[i];
+        bool lose = false;
+        for (int m = 0; m < 4 && !lose; ++m) {
             const int v = vv[m];
             if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
             for (int e = P.vhead[v]; e >= 0; e = P.vnext[e]) {
@@ -611,27 +614,47 @@ __device__ void ph_color_round(const Params& P, long long nc, int k) {
                 if (j == i) continue;
                 const int sj = *((volatile int*)&P.c_stamp[j]);
                 if (sj != 0 && sj != k) continue;
-                if (!jp_beats(pi, i, P.c_prio[j], j)) {
-                    is_max = false;
+                if (P.c_tent[j] == ti && jp_beats(P.c_prio[j], j, pi, i)) {
+                    lose = true;
                     break;
                 }
             }
         }
-        if (!is_max) continue;
+        if (lose) continue;
+        P.c_color[i] = ti;
+        P.c_stamp[i] = k;
+        atomicAdd(&P.g->colored, 1);
+        atomicMax(&P.g->max_color, ti);
+        if (ti < P.colcap) atomicAdd(&P.ccount[ti], 1);
+        else atomicOr(&P.g->error, ERR_CAP_COLORS);
+    }
+}
+
+__device__ void ph_color_propose(const Params& P, long long nc, int k) {
+    for (long long i = gtid(); i < nc; i += gstride()) {
+        if (P.c_stamp[i] != 0) continue;
+        const int4 id = P.c_ids[i];
+        const int vv[4] = {id.x, id.y, id.z, id.w};
         unsigned long long used[4] = {0, 0, 0, 0};
         bool big = false;
         auto mark = [&](int c) {
             if (c < 256) used[c >> 6] |= 1ull << (c & 63);
             else big = true;
         };
+        const uint64_t pi = P.c_prio[i];
+        int rank = 0;  // uncolored neighbor entries (with multiplicity) that beat this row
         for (int m = 0; m < 4; ++m) {
             const int v = vv[m];
             if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
             for (int e = P.vhead[v]; e >= 0; e = P.vnext[e]) {
                 const int j = e >> 2;
                 if (j == i) continue;
-                const int sj = *((volatile int*)&P.c_stamp[j]);
-                if (sj >= 1 && sj < k) mark(P.c_color[j]);
+                const int sj = P.c_stamp[j];
+                if (sj == 0) {
+                    rank += jp_beats(P.c_prio[j], j, pi, i);
+                    continue;
+                }
+                if (sj < k) mark(P.c_color[j]);
             }
             if (P.cfg.edge_constraints)
                 for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
@@ -639,12 +662,23 @@ __device__ void ph_color_round(const Params& P, long long nc, int k) {
                     if (ec >= 0) mark(ec);
                 }
         }
-        int col = -1;
-        for (int w = 0; w < 4 && col < 0; ++w)
-            if (~used[w]) col = w * 64 + __ffsll(~used[w]) - 1;
-        if (col < 0 || big) {
+        // propose the rank-th free color: a clique of uncolored rows takes
+        // distinct colors in priority order within one round
+        int col = -1, left = rank;
+        for (int w = 0; w < 4 && col < 0; ++w) {
+            unsigned long long free_bits = ~used[w];
+            const int nfree = __popcll(free_bits);
+            if (left >= nfree) {
+                left -= nfree;
+                continue;
+            }
+            for (int t = 0; t < left; ++t) free_bits &= free_bits - 1;  // drop the lowest `left` free bits
+            col = w * 64 + __ffsll(free_bits) - 1;
+        }
+        if (col < 0 && !big) col = 256 + left;
+        if (col < 0 || (big && col >= 256)) {
             // > 256 colors around this row: linear search over the neighborhood
-            for (int c = (col < 0 ? 256 : col);; ++c) {
+            for (int c = 256;; ++c) {
                 bool hit = c < 256 ? ((used[c >> 6] >> (c & 63)) & 1) : false;
                 for (int m = 0; m < 4 && !hit; ++m) {
                     const int v = vv[m];
@@ -659,18 +693,13 @@ __device__ void ph_color_round(const Params& P, long long nc, int k) {
                         for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1] && !hit; ++q)
                             hit = P.edge_color[P.vedge[q]] == c;
                 }
-                if (!hit) {
+                if (!hit && left-- == 0) {
                     col = c;
                     break;
                 }
             }
         }
-        P.c_color[i] = col;
-        P.c_stamp[i] = k;
-        atomicAdd(&P.g->colored, 1);
-        atomicMax(&P.g->max_color, col);
-        if (col < P.colcap) atomicAdd(&P.ccount[col], 1);
-        else atomicOr(&P.g->error, ERR_CAP_COLORS);
+        P.c_tent[i] = col;
     }
 }
 

@@ -462,14 +462,75 @@ def knot_scene(n_along: int = 935, n_across: int = 20, spacing: float = 3e-3, p:
     return Scene(name, P, Y, T, E, np.zeros((0, 2), np.int32), inv, True, True)
 
 
+def ply_knot(n_along: int = 935, n_across: int = 20, spacing: float = 3e-3, p: int = 2, q: int = 3,
+             tube: float = 0.03, gap: float = 2.5e-3, squeeze: float = 2.0e-3, slide: float = 2.0e-3,
+             end_gap: float = 0.04, jitter_seed: int | None = None, name: str = "knot") -> Scene:
+    """Two cloth strips ("plies") laid face to face along the same twisted band
+    of a (p, q) torus knot — a two-ply ribbon tied into a knot. Ply A lies on
+    the torus of tube radius ``tube + gap/2``, ply B on ``tube - gap/2``; the
+    band covers a poloidal angle of width/tube around the knot path, so the
+    strips twist around the tube as they wind. Concentric tori cannot
+    intersect, hence the start state is intersection-free with a ``gap``
+    clearance between the strips (in-plane neighbours at 3 mm spacing are
+    within d_max as well).
+
+    Tightening target: the plies are pressed into each other with a squeeze
+    that varies along the knot (0 .. ``gap/2 + squeeze`` per ply, so they
+    interpenetrate by up to ``2*squeeze`` where the knot is tightest) and ply A
+    slides ``slide`` metres along the path relative to ply B.
+
+    CFG2 (reef): n_along=935 -> 37,400 V / 70,984 T. CFG3 (bow): n_along=1870
+    -> 74,800 V / 142,044 T.
+    """
+    width = (n_across - 1) * spacing
+    length = (n_along - 1) * spacing
+    s_span = 2.0 * PI * p * (1.0 - end_gap)
+    R = length / s_span
+    rng = np.random.default_rng(jitter_seed) if jitter_seed is not None else None
+    phase = 0.0 if rng is None else rng.uniform(0, 2 * PI)
+    s = np.linspace(0.0, s_span, n_along)
+    u = (np.arange(n_across) - 0.5 * (n_across - 1)) * spacing
+    S_, U_ = np.meshgrid(s, u, indexing="ij")
+    P_all, Y_all, T_all = [], [], []
+    for k, sign in enumerate((+1.0, -1.0)):
+        r0 = tube + sign * 0.5 * gap
+        phi = (q / p) * S_ + U_ / tube
+        # squeeze profile along the knot: tight where sin > 0
+        prof = 0.5 * (1.0 + np.sin(3.0 * S_ + phase))
+        r1 = r0 - sign * prof * (0.5 * gap + squeeze)
+        th = S_
+        th1 = S_ + (sign * 0.5 * slide / R)
+        ring0 = R + r0 * np.cos(phi)
+        P = np.stack([ring0 * np.cos(th), ring0 * np.sin(th), r0 * np.sin(phi)], -1).reshape(-1, 3)
+        ring1 = R + r1 * np.cos(phi)
+        Y = np.stack([ring1 * np.cos(th1), ring1 * np.sin(th1), r1 * np.sin(phi)], -1).reshape(-1, 3)
+        T_all.append(_ribbon_topology(n_across, n_along, k * n_along * n_across))
+        P_all.append(P)
+        Y_all.append(Y)
+    P = np.concatenate(P_all)
+    Y = np.concatenate(Y_all)
+    T = np.concatenate(T_all)
+    E = finalize_edges(np.zeros((0, 2), np.int32), np.zeros((0, 2), np.int32), T)
+    inv = lumped_inv_mass_fast(P, T, np.zeros((0, 2), np.int64), 0.1, 0.0)
+    del width
+    return Scene(name, P, Y, T, E, np.zeros((0, 2), np.int32), inv, True, True)
+
+
+KNOT_DEFAULTS = dict(squeeze=-0.2e-3, slide=3e-3)  # plies close to a 0.2 mm gap and slide 3 mm
+
+
 def reef_knot(**kw) -> Scene:
+    """CFG2: 37,400 V / 70,984 T two-ply knot (ply_knot), tightening step."""
+    kw = {**KNOT_DEFAULTS, **kw}
     kw.setdefault("name", "reef_knot")
-    return knot_scene(n_along=935, **kw)
+    return ply_knot(n_along=935, **kw)
 
 
 def bow_knot(**kw) -> Scene:
+    """CFG3: 74,800 V / 142,044 T two-ply knot (ply_knot), tightening step."""
+    kw = {**KNOT_DEFAULTS, **kw}
     kw.setdefault("name", "bow_knot")
-    return knot_scene(n_along=1870, **kw)
+    return ply_knot(n_along=1870, **kw)
 
 
 def cloth_on_sphere(n: int = 64, spacing: float = 0.01, drop: float = 0.03) -> Scene:

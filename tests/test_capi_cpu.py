@@ -82,6 +82,8 @@ def test_knot_scene_sizes():
 def test_small_knot_start_is_intersection_free():
     import pyoracle as O
 
-    sc = S.knot_scene(n_along=150, n_across=8)
+    sc = S.knot_scene(n_along=150, n_across=8, pull=7e-3)
     assert O.ccd_certify(sc, sc.x, sc.x)[0] == 0
     assert O.ccd_certify(sc, sc.x, sc.y)[1] > 0  # the target penetrates
+    sc = S.ply_knot(n_along=400, n_across=6)
+    assert O.ccd_certify(sc, sc.x, sc.x)[0] == 0
