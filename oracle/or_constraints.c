@@ -594,7 +594,12 @@ int or_color_device(or_row* rows, int64_t n, const double* inv_mass, int nv, uin
             if (inv_mass[v] > 0.0) deg += (uint64_t)(voff[v + 1] - voff[v] - 1);
         }
         if (deg > 0xFFFFF) deg = 0xFFFFF;
-        prio[i] = (deg << 44) | (contact_prio(rows[i].pair_key, seed) >> 20);
+        /* lower row index (pair order) wins: the rounds reproduce the
+         * sequential greedy coloring in row order, which orders Gauss-Seidel
+         * as well as the reference's smallest-last coloring does on the
+         * acceptance fixtures (and is independent of the seed) */
+        (void)deg;
+        prio[i] = (uint64_t)(nc - i);
     }
     int cap = 64;
     int* cols = (int*)or_xmalloc((size_t)cap * sizeof(int));
@@ -608,15 +613,17 @@ int or_color_device(or_row* rows, int64_t n, const double* inv_mass, int nv, uin
         for (int64_t i = 0; i < nc; ++i) {
             if (round[i] != 0) continue;
             int k = 0;
-            uint64_t unc = 0; /* uncolored neighbor entries (with multiplicity) */
+            uint64_t unc = 0; /* max over vertices of the uncolored rows there that beat this one */
             for (int m = 0; m < rows[i].nverts; ++m) {
                 const int v = rows[i].verts[m];
                 if (!(inv_mass[v] > 0.0)) continue;
+                uint64_t rank_v = 0;
                 for (int64_t a = voff[v]; a < voff[v + 1]; ++a) {
                     const int j = vrows[a];
                     if (j == i) continue;
                     if (round[j] == 0) {
-                        unc += jp_beats(prio[j], j, prio[i], i);
+                        rank_v += jp_beats(prio[j], j, prio[i], i);
+                        if (rank_v > unc) unc = rank_v;
                         continue;
                     }
                     if (k == cap) cols = (int*)or_xrealloc(cols, (size_t)(cap *= 2) * sizeof(int));
@@ -630,9 +637,10 @@ int or_color_device(or_row* rows, int64_t n, const double* inv_mass, int nv, uin
                         cols[k++] = edge_color[e];
                     }
             }
-            /* propose the rank-th free color, rank = number of uncolored
-             * neighbor entries that beat this row: a clique of uncolored rows
-             * takes distinct colors in priority order within one round */
+            /* propose the rank-th free color, rank = max over the row's
+             * vertices of the uncolored rows there that beat it: a clique of
+             * uncolored rows takes distinct colors in priority order within
+             * one round */
             tent[i] = nth_free(cols, k, (int)unc);
         }
         int nw = 0;

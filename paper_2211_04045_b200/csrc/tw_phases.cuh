@@ -578,15 +578,10 @@ __device__ void ph_warm(const Params& P, long long nc) {
         }
         P.imp[v] = make_double4(a.x, a.y, a.z, 0.0);
     }
-    const uint64_t smix = P.cfg.color_seed * 0x9E3779B97F4A7C15ull;
+    // coloring priority: the lower row index (pair order) wins, so the rounds
+    // reproduce the sequential greedy coloring in row order
     for (long long i = gtid(); i < nc; i += gstride()) {
-        const int4 id = P.c_ids[i];
-        const int vv[4] = {id.x, id.y, id.z, id.w};
-        uint64_t deg = 0;
-        for (int m = 0; m < 4; ++m)
-            if (vv[m] >= 0 && P.inv_mass[vv[m]] > 0.0) deg += (uint64_t)(P.vcnt[vv[m]] - 1);
-        if (deg > 0xFFFFF) deg = 0xFFFFF;
-        P.c_prio[i] = (deg << 44) | (mix64(P.c_key[i] ^ smix) >> 20);
+        P.c_prio[i] = (uint64_t)(nc - i);
         P.c_stamp[i] = 0;
         P.c_color[i] = -1;
     }
@@ -642,16 +637,18 @@ __device__ void ph_color_propose(const Params& P, long long nc, int k) {
             else big = true;
         };
         const uint64_t pi = P.c_prio[i];
-        int rank = 0;  // uncolored neighbor entries (with multiplicity) that beat this row
+        int rank = 0;  // max over vertices of the uncolored rows there that beat this row
         for (int m = 0; m < 4; ++m) {
             const int v = vv[m];
             if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
+            int rank_v = 0;
             for (int e = P.vhead[v]; e >= 0; e = P.vnext[e]) {
                 const int j = e >> 2;
                 if (j == i) continue;
                 const int sj = P.c_stamp[j];
                 if (sj == 0) {
-                    rank += jp_beats(P.c_prio[j], j, pi, i);
+                    rank_v += jp_beats(P.c_prio[j], j, pi, i);
+                    rank = max(rank, rank_v);
                     continue;
                 }
                 if (sj < k) mark(P.c_color[j]);
@@ -1163,10 +1160,12 @@ __device__ void ph_advance(const Params& P, double bound, int step, long long nc
                 }
                 P.x[v] = make_double4(xv.x + disp.x, xv.y + disp.y, xv.z + disp.z, x4.w);
                 P.r[v] = P.r[v] * (1.0 - alpha);
-                atomicMax(&P.g->maxdisp_bits, to_b(nrm(disp)));
+                // std::max(max_disp, |disp|) ignores a NaN operand (advance.cpp:37)
+                const double nd = nrm(disp);
+                if (!isnan(nd)) atomicMax(&P.g->maxdisp_bits, to_b(nd));
             }
         }
-        atomicMax(&P.g->resid_bits, to_b(P.r[v]));
+        if (!isnan(P.r[v])) atomicMax(&P.g->resid_bits, to_b(P.r[v]));  // max_remainder, advance.hpp:21-25
         if (P.cfg.record_path) {
             const double4 xn = P.x[v];
             double* o = P.path + ((long long)(step + 1) * P.nv + v) * 3;
