@@ -173,7 +173,11 @@ def test_resolve_battery_bitexact(ctx, coloring):
         _compare_resolve(ctx, sc, coloring_mode=coloring)
 
 
-@pytest.mark.parametrize("kw", [dict(solver="jacobi"), dict(constraint_family="gap"), dict(sweeps=3),
+# Jacobi (omega = 0.5) diverges to NaN on the press fixture after ~440 steps;
+# past that point the reference's hash grid bins NaN coordinates through the
+# undefined (int64_t)floor(NaN), which is not a parity target, so Jacobi is
+# compared over the finite part of the trajectory.
+@pytest.mark.parametrize("kw", [dict(solver="jacobi", step_limit=300), dict(constraint_family="gap"), dict(sweeps=3),
                                 dict(edge_constraints=False), dict(force_fresh_search=True),
                                 dict(eps=0.25), dict(step_limit=4)])
 def test_resolve_options_bitexact(ctx, kw):
