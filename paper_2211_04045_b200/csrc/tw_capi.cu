@@ -63,6 +63,7 @@ struct tw_ctx {
     std::string err;
     int sm_count = 0;
     int nblocks = 0;
+    int minb = 4;  // resolve-kernel instance (CTAs per SM)
     long long launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk = nullptr;
     // capacities
@@ -73,13 +74,12 @@ struct tw_ctx {
     long long refpool_cap = 0;
     // buffers
     DevMem xs, ys, xo;  // N x 3 staging
-    DevMem x, yk1, r, imp, dmin, vhead, vcnt;
+    DevMem x, yk1, r, imp, dmin, voff, vcnt, vinc, c_slot, erank, part_v;
     DevMem ly, is_er, er_edge, er_index, er_value, er_g, er_q, edge_lambda, er_color, er_by_color, er_color_off,
         er_color_cnt;
-    DevMem pkey, pids, pdd, pw, pflag, qcount, qslot;
+    DevMem pkey, pids, pdd, pw, pflag, qcount, qslot, qoff;
     DevMem c_key, c_ids, c_jac, c_value, c_diag, c_q, c_lambda, c_next, c_color, c_stamp, c_arch, c_prio, c_by_color,
         c_tent;
-    DevMem vnext;
     DevMem ccount, coff;
     DevMem arch_key0, arch_key1, arch_val0, arch_val1, new_lb, new_key, new_val;
     DevMem refpool;
@@ -191,7 +191,11 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     CK(ctx->r.ensure(nv * 8));
     CK(ctx->imp.ensure(nv * 32));
     CK(ctx->dmin.ensure(nv * 8));
-    CK(ctx->vhead.ensure(nv * 4));
+    CK(ctx->voff.ensure((nv + 1) * 4));
+    CK(ctx->vinc.ensure(P * 16));
+    CK(ctx->c_slot.ensure(P * 16));
+    CK(ctx->erank.ensure(P * 16));
+    CK(ctx->part_v.ensure((size_t)ctx->nblocks * 8));
     CK(ctx->vcnt.ensure(nv * 4));
     CK(ctx->ly.ensure(ne * 8));
     CK(ctx->is_er.ensure(ne));
@@ -210,6 +214,7 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     CK(ctx->pflag.ensure(P));
     CK(ctx->qcount.ensure((size_t)std::max(1LL, nq) * 4));
     CK(ctx->qslot.ensure((size_t)std::max(1LL, nq) * ctx->K * 4));
+    CK(ctx->qoff.ensure((size_t)(nq + 1) * 8));
     CK(ctx->c_key.ensure(P * 8));
     CK(ctx->c_ids.ensure(P * 16));
     CK(ctx->c_jac.ensure(P * 96));
@@ -224,7 +229,6 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     CK(ctx->c_arch.ensure(P * 8));
     CK(ctx->c_prio.ensure(P * 8));
     CK(ctx->c_by_color.ensure(P * 4));
-    CK(ctx->vnext.ensure(P * 16));
     CK(ctx->ccount.ensure((size_t)ctx->colcap * 4));
     CK(ctx->coff.ensure(((size_t)ctx->colcap + 1) * 4));
     CK(ctx->er_color_cnt.ensure((size_t)ctx->colcap * 4));
@@ -314,6 +318,7 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.pflag = ctx->pflag.as<uint8_t>();
     P.qcount = ctx->qcount.as<int>();
     P.qslot = ctx->qslot.as<int>();
+    P.qoff = ctx->qoff.as<long long>();
     P.c_key = ctx->c_key.as<uint64_t>();
     P.c_ids = ctx->c_ids.as<int4>();
     P.c_jac = ctx->c_jac.as<double>();
@@ -328,8 +333,11 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.c_arch = ctx->c_arch.as<long long>();
     P.c_prio = ctx->c_prio.as<uint64_t>();
     P.c_by_color = ctx->c_by_color.as<int>();
-    P.vhead = ctx->vhead.as<int>();
-    P.vnext = ctx->vnext.as<int>();
+    P.voff = ctx->voff.as<int>();
+    P.vinc = ctx->vinc.as<int>();
+    P.c_slot = ctx->c_slot.as<int>();
+    P.erank = ctx->erank.as<int>();
+    P.part_v = ctx->part_v.as<long long>();
     P.vcnt = ctx->vcnt.as<int>();
     P.colcap = ctx->colcap;
     P.ccount = ctx->ccount.as<int>();
@@ -393,14 +401,14 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
         CK(cudaMemsetAsync(ctx->er_color_cnt.p, 0, (size_t)ctx->colcap * 4, ctx->stream));
         CK(cudaEventRecord(ctx->ev0, ctx->stream));
         launch_setup(ctx->stream, m->nv, d_xs, d_ys, m->d_inv_mass.as<double>(), P.x, const_cast<double4*>(P.yk1),
-                     P.r, P.dmin, P.vhead, P.vcnt, P.imp, &P.g->nonfinite, m->ne, P.edges,
+                     P.r, P.dmin, P.voff, P.vcnt, P.imp, &P.g->nonfinite, m->ne, P.edges,
                      const_cast<double*>(P.ly), P.is_er, P.edge_lambda, P.er_color, P.edge_color,
                      cfg.edge_constraints ? 1 : 0, cfg.coloring_mode == TW_COLOR_DEVICE ? 1 : 0);
         ctx->launches += launch_count_last();
         rc = build_bvhs(ctx, m);
         if (rc) return rc;
         CK(cudaEventRecord(ctx->evk, ctx->stream));
-        CK(coop_resolve(ctx->stream, P, ctx->nblocks));
+        CK(coop_resolve(ctx->stream, P, ctx->nblocks, ctx->minb));
         ctx->launches += 1;
         CK(cudaEventRecord(ctx->ev1, ctx->stream));
         CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof(Globals), cudaMemcpyDeviceToHost, ctx->stream));
@@ -517,10 +525,10 @@ int tw_ctx_create(int device, void* stream, tw_ctx** out) {
         delete ctx;
         return TW_ECUDA;
     }
-    int per_sm = resolve_blocks_per_sm();
-    int want = 2;
-    if (const char* s = std::getenv("TW_BLOCKS_PER_SM")) want = std::max(1, std::atoi(s));
-    per_sm = std::max(1, std::min(per_sm, want));
+    int want = 4;  // measured best on B200 (bow knot): 64 regs, 32 warps/SM
+    if (const char* s = std::getenv("TW_BLOCKS_PER_SM")) want = std::min(4, std::max(2, std::atoi(s)));
+    ctx->minb = want;
+    const int per_sm = std::max(1, std::min(resolve_blocks_per_sm(want), want));
     ctx->nblocks = std::min(ctx->sm_count * per_sm, tw::MAX_BLOCKS);
     if (stream) {
         ctx->stream = (cudaStream_t)stream;
@@ -548,14 +556,15 @@ void tw_ctx_destroy(tw_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    DevMem* all[] = {&ctx->xs, &ctx->ys, &ctx->xo, &ctx->x, &ctx->yk1, &ctx->r, &ctx->imp, &ctx->dmin, &ctx->vhead,
+    DevMem* all[] = {&ctx->xs, &ctx->ys, &ctx->xo, &ctx->x, &ctx->yk1, &ctx->r, &ctx->imp, &ctx->dmin, &ctx->voff,
+                     &ctx->vinc, &ctx->c_slot, &ctx->erank, &ctx->part_v,
                      &ctx->vcnt, &ctx->ly, &ctx->is_er, &ctx->er_edge, &ctx->er_index, &ctx->er_value, &ctx->er_g,
                      &ctx->er_q, &ctx->edge_lambda, &ctx->er_color, &ctx->er_by_color, &ctx->er_color_off,
                      &ctx->er_color_cnt, &ctx->pkey, &ctx->pids, &ctx->pdd, &ctx->pw, &ctx->pflag, &ctx->qcount,
-                     &ctx->qslot, &ctx->c_key, &ctx->c_ids, &ctx->c_jac, &ctx->c_value, &ctx->c_diag, &ctx->c_q,
+                     &ctx->qslot, &ctx->qoff, &ctx->c_key, &ctx->c_ids, &ctx->c_jac, &ctx->c_value, &ctx->c_diag, &ctx->c_q,
                      &ctx->c_lambda, &ctx->c_next, &ctx->c_color, &ctx->c_stamp, &ctx->c_tent, &ctx->c_arch,
                      &ctx->c_prio,
-                     &ctx->c_by_color, &ctx->vnext, &ctx->ccount, &ctx->coff, &ctx->arch_key0, &ctx->arch_key1,
+                     &ctx->c_by_color, &ctx->ccount, &ctx->coff, &ctx->arch_key0, &ctx->arch_key1,
                      &ctx->arch_val0, &ctx->arch_val1, &ctx->new_lb, &ctx->new_key, &ctx->new_val, &ctx->refpool,
                      &ctx->part_q, &ctx->part_c, &ctx->part_k, &ctx->blk_lo, &ctx->blk_hi, &ctx->globals, &ctx->box,
                      &ctx->bvh_tmp, &ctx->smd, &ctx->trace, &ctx->path, &ctx->s_kinds, &ctx->s_verts, &ctx->s_out,
@@ -965,7 +974,7 @@ int tw_stage_advance(tw_ctx* ctx, int32_t nv, const double* inv_mass, const doub
     CK(ctx->r.ensure(n * 8));
     CK(ctx->imp.ensure(n * 32));
     CK(ctx->dmin.ensure(n * 8));
-    CK(ctx->vhead.ensure(n * 4));
+    CK(ctx->voff.ensure((n + 1) * 4));
     CK(ctx->vcnt.ensure(n * 4));
     CK(ctx->globals.ensure(sizeof(Globals)));
     CK(ctx->part_k.ensure((size_t)ctx->nblocks * 8));
@@ -992,7 +1001,7 @@ int tw_stage_advance(tw_ctx* ctx, int32_t nv, const double* inv_mass, const doub
     P.r = ctx->r.as<double>();
     P.imp = ctx->imp.as<double4>();
     P.dmin = ctx->dmin.as<unsigned long long>();
-    P.vhead = ctx->vhead.as<int>();
+    P.voff = ctx->voff.as<int>();
     P.vcnt = ctx->vcnt.as<int>();
     P.part_k = ctx->part_k.as<long long>();
     P.g = ctx->globals.as<Globals>();

@@ -51,6 +51,8 @@ struct Globals {
     int error;
     int nonfinite;
     int internal_line;
+    unsigned long long work_q;  // dynamic query counter of the traversal (reset by the refit)
+    unsigned long long work_s;  // dynamic query counter of the partner sort (reset by the refit)
     int ner;             // edge rows of this call (set by the prologue)
     int needed_k;
     long long np;        // pairs in the set
@@ -142,6 +144,7 @@ struct Params {
     uint8_t* pflag;
     int* qcount;
     int* qslot;     // nq * K
+    long long* qoff;  // nq + 1 output offsets
     // ---- contact rows
     uint64_t* c_key;
     int4* c_ids;
@@ -157,10 +160,12 @@ struct Params {
     long long* c_arch;  // archive index, or -(lower_bound)-1
     uint64_t* c_prio;
     int* c_by_color;
-    // vertex -> contact-row incidence (linked lists, entry = 4*row + m)
-    int* vhead;
-    int* vnext;
-    int* vcnt;
+    // vertex -> contact-row incidence, CSR rebuilt every step (entry = 4*row + m)
+    int* vcnt;      // entries per vertex (nv)
+    int* voff;      // segment offsets (nv + 1)
+    int* vinc;      // entries, each segment sorted by entry id (4 * rows)
+    int* c_slot;    // slot of each entry in its segment before sorting (4 * rows)
+    int* erank;     // position of each entry in its sorted segment (4 * rows)
     // color tables
     int colcap;
     int* ccount;
@@ -180,6 +185,7 @@ struct Params {
     long long* part_q;
     long long* part_c;
     long long* part_k;
+    long long* part_v;
     long long* blk_lo;  // per block pair range
     long long* blk_hi;
     // globals + outputs

@@ -12,7 +12,7 @@ namespace tw {
 
 // k_unpack + k_edges_init
 void launch_setup(cudaStream_t s, int nv, const double* xs, const double* ys, const double* inv_mass,
-                  double4* x, double4* yk1, double* r, unsigned long long* dmin, int* vhead, int* vcnt,
+                  double4* x, double4* yk1, double* r, unsigned long long* dmin, int* voff, int* vcnt,
                   double4* imp, int* nonfinite, int ne, const int2* edges, double* ly, uint8_t* is_er,
                   double* edge_lambda, int* er_color, const int* edge_color, int edge_rows,
                   int device_coloring);
@@ -29,14 +29,14 @@ int launch_count_last();  // kernels launched by the last launcher call
 void launch_bounds(cudaStream_t s, int nv, const double4* x, unsigned long long* box);
 
 // cooperative kernels
-cudaError_t coop_resolve(cudaStream_t s, const Params& P, int nblocks);
+cudaError_t coop_resolve(cudaStream_t s, const Params& P, int nblocks, int minb);
 cudaError_t coop_search(cudaStream_t s, const Params& P, int nblocks);
 cudaError_t coop_refresh(cudaStream_t s, const Params& P, int nblocks, double bound);
 cudaError_t launch_advance(cudaStream_t s, const Params& P, int nblocks);
 cudaError_t launch_closest(cudaStream_t s, int nv, const double4* x, long long n, const int* kinds,
                            const int* verts, double* out, int* has);
-// blocks per SM the resolve kernel can keep resident
-int resolve_blocks_per_sm();
+// blocks per SM the resolve kernel instance built for `minb` CTAs/SM keeps resident
+int resolve_blocks_per_sm(int minb);
 
 // device-mode edge precoloring: one Jones-Plassmann round; returns via
 // *colored the number of edges colored so far (device counter)

@@ -14,7 +14,7 @@ namespace tw {
 // static override y_k1 = x_start (resolve.cpp:48-50), initialise r = 1 and
 // the per-vertex scratch; flag non-finite input (resolve.cpp:41-43).
 __global__ void k_unpack(int nv, const double* xs, const double* ys, const double* inv_mass, double4* x,
-                         double4* yk1, double* r, unsigned long long* dmin, int* vhead, int* vcnt,
+                         double4* yk1, double* r, unsigned long long* dmin, int* voff, int* vcnt,
                          double4* imp, int* nonfinite) {
     for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
          v += (long long)gridDim.x * blockDim.x) {
@@ -29,7 +29,7 @@ __global__ void k_unpack(int nv, const double* xs, const double* ys, const doubl
         yk1[v] = make_double4(b0, b1, b2, im);
         r[v] = 1.0;
         dmin[v] = INF_BITS;
-        vhead[v] = -1;
+        voff[v] = 0;
         vcnt[v] = 0;
         imp[v] = make_double4(0, 0, 0, 0);
     }
@@ -273,7 +273,10 @@ __device__ bool prologue(const Params& P) {
         }                                                                         \
     } while (0)
 
-__global__ void __launch_bounds__(TPB) k_resolve(Params P) {
+// MINB = resident CTAs per SM the register allocation targets (2: 128 regs,
+// 3: 80, 4: 64); the context picks the instance (TW_BLOCKS_PER_SM).
+template <int MINB>
+__global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
     Globals* g = P.g;
     int dbg_step = 0;
     if (g->nonfinite || g->error) return;  // non-finite input detected by k_unpack
@@ -296,7 +299,11 @@ __global__ void __launch_bounds__(TPB) k_resolve(Params P) {
             SYNC();
             ph_traverse(P);
             SYNC();
-            ph_emit_pairs(P, searches == 0);
+            ph_query_totals(P);
+            SYNC();
+            ph_emit_pairs(P);
+            SYNC();
+            ph_emit_records(P, searches == 0);
             SYNC();
             bound = C.d_max;
             ++searches;
@@ -312,6 +319,12 @@ __global__ void __launch_bounds__(TPB) k_resolve(Params P) {
         SYNC();
         const long long nc = g->nc;
         if (lead) g->nactive = 0;
+        ph_inc_totals(P);
+        SYNC();
+        ph_inc_offsets(P);
+        SYNC();
+        ph_inc_scatter(P, nc);
+        SYNC();
         ph_warm(P, nc);
         SYNC();
         int ncol_c, ncol_e, ncol;
@@ -419,16 +432,21 @@ __global__ void __launch_bounds__(TPB) k_resolve(Params P) {
 }
 
 // ======================================================== stage kernels
-__global__ void __launch_bounds__(TPB) k_stage_search(Params P) {
+// stage kernels run on the context's cooperative grid (up to 4 CTAs/SM)
+__global__ void __launch_bounds__(TPB, 4) k_stage_search(Params P) {
     ph_refit(P);
     if (!grid_sync(P.g)) return;
     ph_traverse(P);
     if (!grid_sync(P.g)) return;
-    ph_emit_pairs(P, false);
+    ph_query_totals(P);
+    if (!grid_sync(P.g)) return;
+    ph_emit_pairs(P);
+    if (!grid_sync(P.g)) return;
+    ph_emit_records(P, false);
 }
 
 // refresh + per-vertex bound into P.r (min(bound, dmin))
-__global__ void __launch_bounds__(TPB) k_stage_refresh(Params P, double bound) {
+__global__ void __launch_bounds__(TPB, 4) k_stage_refresh(Params P, double bound) {
     ph_refresh(P, bound, false, false, 0, 0);
     if (!grid_sync(P.g)) return;
     for (long long v = gtid(); v < P.nv; v += gstride()) P.r[v] = mind(bound, to_d(P.dmin[v]));
@@ -508,13 +526,13 @@ static int grid_for(long long n, int tpb = 256) {
 }
 
 void launch_setup(cudaStream_t s, int nv, const double* xs, const double* ys, const double* inv_mass,
-                  double4* x, double4* yk1, double* r, unsigned long long* dmin, int* vhead, int* vcnt,
+                  double4* x, double4* yk1, double* r, unsigned long long* dmin, int* voff, int* vcnt,
                   double4* imp, int* nonfinite, int ne, const int2* edges, double* ly, uint8_t* is_er,
                   double* edge_lambda, int* er_color, const int* edge_color, int edge_rows,
                   int device_coloring) {
     g_last_launches = 0;
     if (nv > 0) {
-        k_unpack<<<grid_for(nv), 256, 0, s>>>(nv, xs, ys, inv_mass, x, yk1, r, dmin, vhead, vcnt, imp, nonfinite);
+        k_unpack<<<grid_for(nv), 256, 0, s>>>(nv, xs, ys, inv_mass, x, yk1, r, dmin, voff, vcnt, imp, nonfinite);
         ++g_last_launches;
     }
     if (ne > 0) {
@@ -564,9 +582,15 @@ void launch_bounds(cudaStream_t s, int nv, const double4* x, unsigned long long*
     k_bounds<<<grid_for(nv), 256, 0, s>>>(nv, x, box);
 }
 
-int resolve_blocks_per_sm() {
+static const void* resolve_fn(int minb) {
+    if (minb >= 4) return (const void*)k_resolve<4>;
+    if (minb == 3) return (const void*)k_resolve<3>;
+    return (const void*)k_resolve<2>;
+}
+
+int resolve_blocks_per_sm(int minb) {
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_resolve, TPB, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, resolve_fn(minb), TPB, 0);
     return b;
 }
 
@@ -574,10 +598,10 @@ static cudaError_t coop(const void* fn, cudaStream_t s, int nblocks, void** args
     return cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(TPB), args, 0, s);
 }
 
-cudaError_t coop_resolve(cudaStream_t s, const Params& P, int nblocks) {
+cudaError_t coop_resolve(cudaStream_t s, const Params& P, int nblocks, int minb) {
     Params p = P;
     void* args[] = {&p};
-    return coop((const void*)k_resolve, s, nblocks, args);
+    return coop(resolve_fn(minb), s, nblocks, args);
 }
 cudaError_t coop_search(cudaStream_t s, const Params& P, int nblocks) {
     Params p = P;

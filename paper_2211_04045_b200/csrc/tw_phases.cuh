@@ -127,6 +127,7 @@ __device__ __forceinline__ void prim_box(const Params& P, int cls, int prim, dou
 // A1: bottom-up refit of all three hierarchies at the current positions
 // (node flags are zero on entry; the second child to arrive builds the parent)
 __device__ void ph_refit(const Params& P) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.g->work_q = 0ull, P.g->work_s = 0ull;  // traverse / sort
     for (int cls = 0; cls < 3; ++cls) {
         const Bvh& B = P.bvh[cls];
         if (B.n == 0) continue;
@@ -210,13 +211,22 @@ __device__ __forceinline__ bool candidate_keep(const Params& P, int ka, int ia, 
 
 // A2: traverse every query (block-chunked, in key order) and record the
 // surviving partners; per-block totals go to part_q
+// Queries are handed out dynamically, 32 at a time per warp, from a global
+// counter (work per query varies by two orders of magnitude); the per-block
+// totals of the counts for the order-preserving prefix are summed afterwards
+// (ph_query_totals).
 __device__ void ph_traverse(const Params& P) {
     const long long nq = num_queries(P);
-    long long lo, hi;
-    chunk_of(nq, &lo, &hi);
-    long long cnt_sum = 0, evals = 0;
+    long long evals = 0;
     const double infl = P.cfg.d_max * (1.0 + 1e-6) + 1e-12;
-    for (long long q = lo + threadIdx.x; q < hi; q += TPB) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        long long base = 0;
+        if (lane == 0) base = (long long)atomicAdd(&P.g->work_q, 32ull);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= nq) break;
+        const long long q = base + lane;
+        if (q >= nq) continue;
         int ka, ia, kb, cls;
         query_of(P, q, &ka, &ia, &kb, &cls);
         const Bvh& B = P.bvh[cls];
@@ -278,14 +288,21 @@ __device__ void ph_traverse(const Params& P) {
             atomicOr(&P.g->error, ERR_CAP_SLOTS);
             atomicMax(&P.g->needed_k, cnt);
         }
-        cnt_sum += cnt;
     }
-    const long long tot = block_sum(cnt_sum);
     const long long ev = block_sum(evals);
-    if (threadIdx.x == 0) {
-        P.part_q[blockIdx.x] = tot;
-        atomicAdd((unsigned long long*)&P.g->pairs_evaluated, (unsigned long long)ev);
-    }
+    if (threadIdx.x == 0) atomicAdd((unsigned long long*)&P.g->pairs_evaluated, (unsigned long long)ev);
+}
+
+// A2b: per-block totals of the query counts over the block's chunk (the
+// chunking ph_emit_pairs uses)
+__device__ void ph_query_totals(const Params& P) {
+    const long long nq = num_queries(P);
+    long long lo, hi;
+    chunk_of(nq, &lo, &hi);
+    long long s = 0;
+    for (long long q = lo + threadIdx.x; q < hi; q += TPB) s += P.qcount[q];
+    const long long tot = block_sum(s);
+    if (threadIdx.x == 0) P.part_q[blockIdx.x] = tot;
 }
 
 __device__ __forceinline__ void vertex_min(const Params& P, int v, double d) {
@@ -307,10 +324,31 @@ __device__ __forceinline__ bool contact_pred(const Params& P, int ka, int kb, co
     return !(row_jnorm(c) < 1e-28);
 }
 
+// ascending bitonic sort of 64 ints held as (a, b) = elements (lane, lane + 32)
+__device__ __forceinline__ void bitonic64(int& a, int& b, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {  // k == 64: partner is the other register of this lane
+                const int lo = min(a, b), hi = max(a, b);
+                a = lo, b = hi;
+                continue;
+            }
+            const int pa = __shfl_xor_sync(0xffffffffu, a, j);
+            const int pb = __shfl_xor_sync(0xffffffffu, b, j);
+            const bool low = (lane & j) == 0;
+            const bool up_a = (lane & k) == 0, up_b = ((lane + 32) & k) == 0;
+            a = (up_a == low) ? min(a, pa) : max(a, pa);
+            b = (up_b == low) ? min(b, pb) : max(b, pb);
+        }
+    }
+}
+
 // A3: prefix the per-query counts, sort each query's partners, evaluate and
 // write the pair records in key order; seed the vertex bound, the contact
 // predicate for the coming linearization, and reset the refit flags.
-__device__ void ph_emit_pairs(const Params& P, bool first_search) {
+__device__ void ph_emit_pairs(const Params& P) {
     const long long nq = num_queries(P);
     long long lo, hi;
     chunk_of(nq, &lo, &hi);
@@ -322,70 +360,108 @@ __device__ void ph_emit_pairs(const Params& P, bool first_search) {
         }
         return;
     }
+    // pass 1 (this phase): per-query output offsets ...
     long long base = prefix_of(P.part_q, blockIdx.x);
-    const long long block_lo = base;
-    long long ncontact = 0;
-    int touching = 0;
     for (long long t = lo; t < hi; t += TPB) {
         const long long q = t + threadIdx.x;
         const int cnt = q < hi ? P.qcount[q] : 0;
         long long tile_tot;
         const long long off = base + block_scan(cnt, &tile_tot);
         base += tile_tot;
-        if (q >= hi || cnt == 0) continue;
+        if (q >= hi) continue;
+        P.qoff[q] = off;
+    }
+    // ... and the key order of each query's partners: one warp per query
+    // (bitonic sort of up to 64 in registers), queries handed out dynamically
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        long long qb = 0;
+        if (lane == 0) qb = (long long)atomicAdd(&P.g->work_s, 8ull);
+        qb = __shfl_sync(0xffffffffu, qb, 0);
+        if (qb >= nq) break;
+        for (long long q = qb; q < qb + 8 && q < nq; ++q) {
+            const int cnt = P.qcount[q];
+            if (cnt < 2) continue;
+            int* s = P.qslot + q * P.K;
+            if (cnt <= 64) {
+                int a = lane < cnt ? s[lane] : 0x7fffffff;
+                int b = lane + 32 < cnt ? s[lane + 32] : 0x7fffffff;
+                bitonic64(a, b, lane);
+                if (lane < cnt) s[lane] = a;
+                if (lane + 32 < cnt) s[lane + 32] = b;
+            } else if (lane == 0) {
+                for (int i = 1; i < cnt; ++i) {
+                    const int v = s[i];
+                    int j = i - 1;
+                    while (j >= 0 && s[j] > v) s[j + 1] = s[j], --j;
+                    s[j + 1] = v;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) P.qoff[nq] = total;
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.g->np = total;
+    // reset refit flags for the next search
+    for (int cls = 0; cls < 3; ++cls) {
+        const Bvh& B = P.bvh[cls];
+        for (long long j = gtid(); j < (long long)B.n - 1; j += gstride()) B.flag[j] = 0u;
+    }
+}
+
+// A3b: the pair records, balanced over the output: CTA b writes pairs
+// [b P / nb, (b+1) P / nb) — the query of pair p is found by binary search on
+// the query offsets.
+__device__ void ph_emit_records(const Params& P, bool first_search) {
+    const long long nq = num_queries(P);
+    const long long np = P.g->np;
+    long long lo, hi;
+    chunk_of(np, &lo, &hi);
+    long long ncontact = 0;
+    int touching = 0;
+    for (long long p = lo + threadIdx.x; p < hi; p += TPB) {
+        long long a = 0, b = nq;  // last query with qoff <= p
+        while (b - a > 1) {
+            const long long mid = (a + b) >> 1;
+            if (P.qoff[mid] <= p) a = mid;
+            else b = mid;
+        }
+        const long long q = a;
         int ka, ia, kb, cls;
         query_of(P, q, &ka, &ia, &kb, &cls);
-        int* s = P.qslot + q * P.K;
-        for (int i = 1; i < cnt; ++i) {  // insertion sort of the partner indices
-            const int v = s[i];
-            int j = i - 1;
-            while (j >= 0 && s[j] > v) s[j + 1] = s[j], --j;
-            s[j + 1] = v;
-        }
-        int va[3];
+        const int ib = P.qslot[q * P.K + (p - P.qoff[q])];
+        int va[3], vb[3];
         simplex_ids(P, ka, ia, va);
-        for (int i = 0; i < cnt; ++i) {
-            const int ib = s[i];
-            int vb[3];
-            simplex_ids(P, kb, ib, vb);
-            Closest c;
-            pair_closest(ka, va, kb, vb, XLoad{P.x}, c);
-            const long long p = off + i;
-            const int4 ids = ka == KE ? make_int4(va[0], va[1], vb[0], vb[1])
-                                      : make_int4(va[0], vb[0], vb[1], vb[2]);
-            bool all_static = true;
-            for (int k = 0; k <= ka; ++k) all_static &= P.inv_mass[va[k]] == 0.0;
-            for (int k = 0; k <= kb; ++k) all_static &= P.inv_mass[vb[k]] == 0.0;
-            uint8_t fl = PF_ACTIVE | (all_static ? PF_ALL_STATIC : 0) | (c.degenerate ? PF_DEGENERATE : 0);
-            const double4 dd = make_double4(c.dir.x, c.dir.y, c.dir.z, c.dist);
-            const double4 w = pack_weights(ka, kb, c);
-            if (contact_pred(P, ka, kb, va, vb, dd, w, fl)) {
-                fl |= PF_CONTACT;
-                ++ncontact;
-            }
-            P.pkey[p] = pair_key(ka, ia, kb, ib);
-            P.pids[p] = ids;
-            P.pdd[p] = dd;
-            P.pw[p] = w;
-            P.pflag[p] = fl;
-            for (int k = 0; k <= ka; ++k) vertex_min(P, va[k], c.dist);
-            for (int k = 0; k <= kb; ++k) vertex_min(P, vb[k], c.dist);
-            if (first_search && c.dist < 1e-10) touching = 1;
+        simplex_ids(P, kb, ib, vb);
+        Closest c;
+        pair_closest(ka, va, kb, vb, XLoad{P.x}, c);
+        const int4 ids = ka == KE ? make_int4(va[0], va[1], vb[0], vb[1]) : make_int4(va[0], vb[0], vb[1], vb[2]);
+        bool all_static = true;
+        for (int k = 0; k <= ka; ++k) all_static &= P.inv_mass[va[k]] == 0.0;
+        for (int k = 0; k <= kb; ++k) all_static &= P.inv_mass[vb[k]] == 0.0;
+        uint8_t fl = PF_ACTIVE | (all_static ? PF_ALL_STATIC : 0) | (c.degenerate ? PF_DEGENERATE : 0);
+        const double4 dd = make_double4(c.dir.x, c.dir.y, c.dir.z, c.dist);
+        const double4 w = pack_weights(ka, kb, c);
+        if (contact_pred(P, ka, kb, va, vb, dd, w, fl)) {
+            fl |= PF_CONTACT;
+            ++ncontact;
         }
+        P.pkey[p] = pair_key(ka, ia, kb, ib);
+        P.pids[p] = ids;
+        P.pdd[p] = dd;
+        P.pw[p] = w;
+        P.pflag[p] = fl;
+        for (int k = 0; k <= ka; ++k) vertex_min(P, va[k], c.dist);
+        for (int k = 0; k <= kb; ++k) vertex_min(P, vb[k], c.dist);
+        if (first_search && c.dist < 1e-10) touching = 1;
     }
     const long long nct = block_sum(ncontact);
     const long long touch = block_sum(touching);
     if (threadIdx.x == 0) {
         P.part_c[blockIdx.x] = nct;
-        P.blk_lo[blockIdx.x] = block_lo;
-        P.blk_hi[blockIdx.x] = base;
+        P.blk_lo[blockIdx.x] = lo;
+        P.blk_hi[blockIdx.x] = hi;
         if (touch) P.g->start_in_contact = 1;
-        if (blockIdx.x == 0) P.g->np = total;
-    }
-    // reset refit flags for the next search
-    for (int cls = 0; cls < 3; ++cls) {
-        const Bvh& B = P.bvh[cls];
-        for (long long j = gtid(); j < (long long)B.n - 1; j += gstride()) B.flag[j] = 0u;
     }
 }
 
@@ -401,9 +477,12 @@ __device__ __forceinline__ long long arch_lower_bound(const uint64_t* keys, long
 }
 
 // ============================================================ rows (B2)
-__device__ __forceinline__ void insert_list(const Params& P, int v, int entry) {
-    P.vnext[entry] = atomicExch(&P.vhead[v], entry);
-    atomicAdd(&P.vcnt[v], 1);
+// Vertex -> contact-row incidence, built per step as CSR: B2 takes a slot per
+// (row, dynamic vertex) entry, then counts are scanned (ph_inc_totals,
+// ph_inc_offsets) and entries scattered (ph_inc_scatter); ph_warm sorts each
+// vertex segment by entry id (= row order).
+__device__ __forceinline__ void record_incidence(const Params& P, int v, int entry) {
+    P.c_slot[entry] = atomicAdd(&P.vcnt[v], 1);
 }
 
 // edge-length row at x (constraints.cpp:144-173) + fill_diag + q
@@ -497,52 +576,90 @@ __device__ void ph_rows(const Params& P, int sel, long long narch) {
             P.c_arch[pos] = -at - 1;
         }
         P.c_lambda[pos] = lam;
-        for (int m = 0; m < c.nverts; ++m)
-            if (P.inv_mass[c.v[m]] > 0.0) insert_list(P, c.v[m], (int)(pos * 4 + m));
+        for (int m = 0; m < 4; ++m) {
+            const int e = (int)(pos * 4 + m);
+            if (m < c.nverts && P.inv_mass[c.v[m]] > 0.0) record_incidence(P, c.v[m], e);
+            else P.c_slot[e] = -1;
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) P.g->nc = nc_total;
     if (P.cfg.edge_constraints)
         for (long long k = gtid(); k < P.g->ner; k += gstride()) edge_row(P, P.er_edge[k]);
 }
 
-// sorted contact-row entries (4*row + m) incident to v; returns the count and
-// fills buf (capacity cap) when count <= cap
-__device__ __forceinline__ int vertex_entries(const Params& P, int v, int* buf, int cap) {
-    int n = 0;
-    for (int e = P.vhead[v]; e >= 0; e = P.vnext[e]) {
-        if (n < cap) {
-            int j = n - 1;
-            while (j >= 0 && buf[j] > e) buf[j + 1] = buf[j], --j;
-            buf[j + 1] = e;
-        }
-        ++n;
+// B2b: per-block totals of the incidence counts over the block's vertex chunk
+__device__ void ph_inc_totals(const Params& P) {
+    long long lo, hi;
+    chunk_of(P.nv, &lo, &hi);
+    long long s = 0;
+    for (long long v = lo + threadIdx.x; v < hi; v += TPB) s += P.vcnt[v];
+    const long long t = block_sum(s);
+    if (threadIdx.x == 0) P.part_v[blockIdx.x] = t;
+}
+
+// B2c: CSR offsets of the incidence
+__device__ void ph_inc_offsets(const Params& P) {
+    long long lo, hi;
+    chunk_of(P.nv, &lo, &hi);
+    long long base = prefix_of(P.part_v, blockIdx.x);
+    for (long long t = lo; t < hi; t += TPB) {
+        const long long v = t + threadIdx.x;
+        const int c = v < hi ? P.vcnt[v] : 0;
+        long long tt;
+        const long long o = base + block_scan(c, &tt);
+        base += tt;
+        if (v < hi) P.voff[v] = (int)o;
     }
-    return n;
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) P.voff[P.nv] = (int)base;
 }
 
-// k-th smallest entry (0-based) of v's list by repeated selection (large lists)
-__device__ __forceinline__ int vertex_entry_select(const Params& P, int v, int prev) {
-    int best = 0x7fffffff;
-    for (int e = P.vhead[v]; e >= 0; e = P.vnext[e])
-        if (e > prev && e < best) best = e;
-    return best;
+// B2d: scatter the entries (4*row + m) into their vertex segments
+__device__ void ph_inc_scatter(const Params& P, long long nc) {
+    for (long long e = gtid(); e < 4 * nc; e += gstride()) {
+        const int s = P.c_slot[e];
+        if (s < 0) continue;
+        const int v = (&P.c_ids[e >> 2].x)[e & 3];
+        P.vinc[P.voff[v] + s] = (int)e;
+    }
 }
 
-// visit contact-row entries of v in ascending row order
+// in-place ascending sort of a vertex segment (insertion sort for short
+// segments, heap sort for long ones; segments live in L1/L2)
+__device__ __forceinline__ void sort_segment(int* a, int n) {
+    if (n <= 48) {
+        for (int i = 1; i < n; ++i) {
+            const int v = a[i];
+            int j = i - 1;
+            while (j >= 0 && a[j] > v) a[j + 1] = a[j], --j;
+            a[j + 1] = v;
+        }
+        return;
+    }
+    auto sift = [&](int root, int end) {
+        while (2 * root + 1 < end) {
+            int child = 2 * root + 1;
+            if (child + 1 < end && a[child] < a[child + 1]) ++child;
+            if (a[root] >= a[child]) return;
+            const int t = a[root];
+            a[root] = a[child];
+            a[child] = t;
+            root = child;
+        }
+    };
+    for (int i = n / 2 - 1; i >= 0; --i) sift(i, n);
+    for (int end = n - 1; end > 0; --end) {
+        const int t = a[0];
+        a[0] = a[end];
+        a[end] = t;
+        sift(0, end);
+    }
+}
+
+// visit the (sorted) contact-row entries of v
 template <typename F>
 __device__ __forceinline__ void for_sorted_entries(const Params& P, int v, F&& f) {
-    constexpr int CAP = 48;
-    int buf[CAP];
-    const int n = vertex_entries(P, v, buf, CAP);
-    if (n <= CAP) {
-        for (int i = 0; i < n; ++i) f(buf[i]);
-    } else {
-        int prev = -1;
-        for (int i = 0; i < n; ++i) {
-            prev = vertex_entry_select(P, v, prev);
-            f(prev);
-        }
-    }
+    const int b = P.voff[v], e = P.voff[v + 1];
+    for (int k = b; k < e; ++k) f(P.vinc[k]);
 }
 
 __device__ __forceinline__ void imp_add(d3& a, double s, d3 j) {
@@ -559,6 +676,10 @@ __device__ void ph_warm(const Params& P, long long nc) {
         const double im = P.inv_mass[v];
         d3 a = mk(0, 0, 0);
         if (im > 0.0) {
+            const int b = P.voff[v], n = P.voff[v + 1] - b;
+            sort_segment(P.vinc + b, n);
+            // entry rank inside the vertex clique (round-1 coloring proposal)
+            for (int k = 0; k < n; ++k) P.erank[P.vinc[b + k]] = k;
             for_sorted_entries(P, (int)v, [&](int e) {
                 const int row = e >> 2, m = e & 3;
                 const double lam = P.c_lambda[row];
@@ -598,18 +719,18 @@ __device__ void ph_color_finalize(const Params& P, long long nc, int k) {
         if (P.c_stamp[i] != 0) continue;
         const int4 id = P.c_ids[i];
         const int vv[4] = {id.x, id.y, id.z, id.w};
-        const uint64_t pi = P.c_prio[i];
         const int ti = P.c_tent[i];
         bool lose = false;
+        // rows beating this one (lower index) precede its entry in the sorted segments
         for (int m = 0; m < 4 && !lose; ++m) {
             const int v = vv[m];
             if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
-            for (int e = P.vhead[v]; e >= 0; e = P.vnext[e]) {
-                const int j = e >> 2;
-                if (j == i) continue;
+            const int b = P.voff[v], pos = P.erank[4 * i + m];
+            for (int t = b; t < b + pos; ++t) {
+                const int j = P.vinc[t] >> 2;
                 const int sj = *((volatile int*)&P.c_stamp[j]);
                 if (sj != 0 && sj != k) continue;
-                if (P.c_tent[j] == ti && jp_beats(P.c_prio[j], j, pi, i)) {
+                if (P.c_tent[j] == ti) {
                     lose = true;
                     break;
                 }
@@ -636,22 +757,26 @@ __device__ void ph_color_propose(const Params& P, long long nc, int k) {
             if (c < 256) used[c >> 6] |= 1ull << (c & 63);
             else big = true;
         };
-        const uint64_t pi = P.c_prio[i];
         int rank = 0;  // max over vertices of the uncolored rows there that beat this row
         for (int m = 0; m < 4; ++m) {
             const int v = vv[m];
             if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
-            int rank_v = 0;
-            for (int e = P.vhead[v]; e >= 0; e = P.vnext[e]) {
-                const int j = e >> 2;
-                if (j == i) continue;
-                const int sj = P.c_stamp[j];
-                if (sj == 0) {
-                    rank_v += jp_beats(P.c_prio[j], j, pi, i);
-                    rank = max(rank, rank_v);
-                    continue;
+            const int b = P.voff[v], e = P.voff[v + 1], pos = P.erank[4 * i + m];
+            if (k == 1) {
+                rank = max(rank, pos);  // round 1: everything uncolored, nothing colored
+            } else {
+                int rank_v = 0;
+                for (int t = b; t < e; ++t) {
+                    const int j = P.vinc[t] >> 2;
+                    if (j == i) continue;
+                    const int sj = P.c_stamp[j];
+                    if (sj == 0) {
+                        rank_v += t < b + pos;  // rows before this entry have a lower index
+                        continue;
+                    }
+                    if (sj < k) mark(P.c_color[j]);
                 }
-                if (sj < k) mark(P.c_color[j]);
+                rank = max(rank, rank_v);
             }
             if (P.cfg.edge_constraints)
                 for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
@@ -680,10 +805,10 @@ __device__ void ph_color_propose(const Params& P, long long nc, int k) {
                 for (int m = 0; m < 4 && !hit; ++m) {
                     const int v = vv[m];
                     if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
-                    for (int e = P.vhead[v]; e >= 0 && !hit; e = P.vnext[e]) {
-                        const int j = e >> 2;
+                    for (int t = P.voff[v]; t < P.voff[v + 1] && !hit; ++t) {
+                        const int j = P.vinc[t] >> 2;
                         if (j == i) continue;
-                        const int sj = *((volatile int*)&P.c_stamp[j]);
+                        const int sj = P.c_stamp[j];
                         hit = sj >= 1 && sj < k && P.c_color[j] == c;
                     }
                     if (P.cfg.edge_constraints)
@@ -801,8 +926,8 @@ __device__ void ph_color_ref(const Params& P, long long nc) {
                 }
                 pool[cur++] = (int)j;
             };
-            for (int e = P.vhead[v]; e >= 0; e = P.vnext[e]) {
-                const long long j = e >> 2;
+            for (int t = P.voff[v]; t < P.voff[v + 1]; ++t) {
+                const long long j = P.vinc[t] >> 2;
                 TW_INVARIANT(j < nc);
                 if (j != r) push(j);
             }
@@ -1132,7 +1257,6 @@ __device__ void ph_advance(const Params& P, double bound, int step, long long nc
         const double4 x4 = P.x[v];
         const unsigned long long db = P.dmin[v];
         P.dmin[v] = INF_BITS;
-        P.vhead[v] = -1;
         P.vcnt[v] = 0;
         if (x4.w == 0.0) {  // static
             P.r[v] = 0.0;
