@@ -179,7 +179,7 @@ void grow_ll(long long& v, long long need) {
 
 int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) {
     const size_t nv = (size_t)std::max(1, m->nv), ne = (size_t)std::max(1, m->ne);
-    const long long nq = 2LL * m->niso + m->nv + m->ne;
+    const long long nq = 2 * pad32(m->niso) + pad32(m->nv) + pad32(m->ne);  // = num_queries
     if (ctx->pcap == 0) ctx->pcap = 8LL * (m->nv + m->ne) + 4096;
     if (ctx->arch_cap < ctx->pcap) ctx->arch_cap = ctx->pcap;
     const size_t P = (size_t)ctx->pcap;

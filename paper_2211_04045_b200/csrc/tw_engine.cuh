@@ -206,6 +206,7 @@ __device__ __forceinline__ unsigned long long to_b(double d) {
     return (unsigned long long)__double_as_longlong(d);
 }
 constexpr unsigned long long INF_BITS = 0x7ff0000000000000ull;
+__host__ __device__ __forceinline__ long long pad32(long long n) { return (n + 31) & ~31LL; }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z += 0x9E3779B97F4A7C15ull;

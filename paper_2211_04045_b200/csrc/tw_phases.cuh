@@ -161,22 +161,24 @@ __device__ __forceinline__ bool box_hit(float4 qlo, float4 qhi, float4 lo, float
            lo.z <= qhi.z;
 }
 
-// query classes in output (key) order: VV, VE, VT, EE
+// Query index space in output (key) order — VV, VE, VT, EE — with every
+// class starting at a multiple of 32 so that a warp's 32 queries share one
+// hierarchy; padding queries are invalid (ia = -1) and produce no pairs.
 __device__ __forceinline__ void query_of(const Params& P, long long q, int* ka, int* ia, int* kb,
                                          int* cls) {
-    const long long niso = P.niso;
-    if (q < niso) {
-        *ka = KV, *ia = P.iso[q], *kb = KV, *cls = 2;
-    } else if (q < 2 * niso) {
-        *ka = KV, *ia = P.iso[q - niso], *kb = KE, *cls = 1;
-    } else if (q < 2 * niso + P.nv) {
-        *ka = KV, *ia = (int)(q - 2 * niso), *kb = KT, *cls = 0;
+    const long long niso = P.niso, s1 = pad32(niso), s2 = 2 * s1, s3 = s2 + pad32(P.nv);
+    if (q < s1) {
+        *ka = KV, *ia = q < niso ? P.iso[q] : -1, *kb = KV, *cls = 2;
+    } else if (q < s2) {
+        *ka = KV, *ia = q - s1 < niso ? P.iso[q - s1] : -1, *kb = KE, *cls = 1;
+    } else if (q < s3) {
+        *ka = KV, *ia = q - s2 < P.nv ? (int)(q - s2) : -1, *kb = KT, *cls = 0;
     } else {
-        *ka = KE, *ia = (int)(q - 2 * niso - P.nv), *kb = KE, *cls = 1;
+        *ka = KE, *ia = q - s3 < P.ne ? (int)(q - s3) : -1, *kb = KE, *cls = 1;
     }
 }
 __device__ __forceinline__ long long num_queries(const Params& P) {
-    return 2LL * P.niso + P.nv + P.ne;
+    return 2 * pad32(P.niso) + pad32(P.nv) + pad32(P.ne);
 }
 
 __device__ __forceinline__ void simplex_ids(const Params& P, int k, int idx, int* v) {
@@ -209,30 +211,34 @@ __device__ __forceinline__ bool candidate_keep(const Params& P, int ka, int ia, 
     return h == 1 && c.dist < P.cfg.d_max;
 }
 
-// A2: traverse every query (block-chunked, in key order) and record the
-// surviving partners; per-block totals go to part_q
-// Queries are handed out dynamically, 32 at a time per warp, from a global
-// counter (work per query varies by two orders of magnitude); the per-block
-// totals of the counts for the order-preserving prefix are summed afterwards
-// (ph_query_totals).
+// A2: traverse every query and record the surviving partners. A warp takes 32
+// consecutive queries (spatially coherent: consecutive vertices / edges of
+// the mesh) from a global counter and walks the hierarchy as a packet: one
+// shared DFS stack, a node is descended when any lane's query box overlaps
+// it (ballot), so the walk itself never diverges; at a leaf only the lanes
+// whose box overlaps run the exact FP64 test. The per-block totals for the
+// order-preserving prefix are summed afterwards (ph_query_totals).
+constexpr int TRAV_STACK = 64;
 __device__ void ph_traverse(const Params& P) {
+    __shared__ int sstack[TPB / 32][TRAV_STACK];
     const long long nq = num_queries(P);
     long long evals = 0;
     const double infl = P.cfg.d_max * (1.0 + 1e-6) + 1e-12;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int* stack = sstack[warp];
     for (;;) {
         long long base = 0;
         if (lane == 0) base = (long long)atomicAdd(&P.g->work_q, 32ull);
         base = __shfl_sync(0xffffffffu, base, 0);
         if (base >= nq) break;
-        const long long q = base + lane;
-        if (q >= nq) continue;
+        const long long q = base + lane;  // nq is a multiple of 32
         int ka, ia, kb, cls;
-        query_of(P, q, &ka, &ia, &kb, &cls);
+        query_of(P, q, &ka, &ia, &kb, &cls);  // ka, kb, cls are warp-uniform
         const Bvh& B = P.bvh[cls];
         int cnt = 0;
-        if (B.n > 0) {
-            int va[3];
+        int va[3] = {-1, -1, -1};
+        float4 qlo = make_float4(1.f, 1.f, 1.f, 0.f), qhi = make_float4(0.f, 0.f, 0.f, 0.f);  // empty box
+        if (ia >= 0) {
             simplex_ids(P, ka, ia, va);
             double lo3[3], hi3[3];
             const d3 p0 = ld3(P.x, va[0]);
@@ -243,44 +249,47 @@ __device__ void ph_traverse(const Params& P) {
                 lo3[1] = fmin(lo3[1], p1.y), hi3[1] = fmax(hi3[1], p1.y);
                 lo3[2] = fmin(lo3[2], p1.z), hi3[2] = fmax(hi3[2], p1.z);
             }
-            const float4 qlo = make_float4(__double2float_rd(lo3[0] - infl), __double2float_rd(lo3[1] - infl),
-                                           __double2float_rd(lo3[2] - infl), 0.f);
-            const float4 qhi = make_float4(__double2float_ru(hi3[0] + infl), __double2float_ru(hi3[1] + infl),
-                                           __double2float_ru(hi3[2] + infl), 0.f);
-            int* slots = P.qslot + q * P.K;
-            int stack[64];
+            qlo = make_float4(__double2float_rd(lo3[0] - infl), __double2float_rd(lo3[1] - infl),
+                              __double2float_rd(lo3[2] - infl), 0.f);
+            qhi = make_float4(__double2float_ru(hi3[0] + infl), __double2float_ru(hi3[1] + infl),
+                              __double2float_ru(hi3[2] + infl), 0.f);
+        }
+        int* slots = P.qslot + q * P.K;
+        auto visit_leaf = [&](int node) {
+            const int ib = prim_to_index(P, cls, B.prim[node - (B.n - 1)]);
+            Closest c;
+            ++evals;
+            if (candidate_keep(P, ka, ia, va, kb, ib, c)) {
+                if (cnt < P.K) slots[cnt] = ib;
+                ++cnt;
+            }
+        };
+        if (B.n == 1) {
+            if (ia >= 0 && box_hit(qlo, qhi, B.lo[0], B.hi[0])) visit_leaf(0);
+        } else if (B.n > 1 && __any_sync(0xffffffffu, ia >= 0)) {
             int sp = 0;
-            const int root = 0;
-            auto visit_leaf = [&](int node) {
-                const int ib = prim_to_index(P, cls, B.prim[node - (B.n - 1)]);
-                Closest c;
-                ++evals;
-                if (candidate_keep(P, ka, ia, va, kb, ib, c)) {
-                    if (cnt < P.K) slots[cnt] = ib;
-                    ++cnt;
-                }
-            };
-            if (B.n == 1) {
-                if (box_hit(qlo, qhi, B.lo[0], B.hi[0])) visit_leaf(0);
-            } else {
-                stack[sp++] = root;
-                while (sp > 0) {
-                    const int node = stack[--sp];
-                    const int2 ch = B.child[node];
-                    const int c2[2] = {ch.x, ch.y};
+            if (lane == 0) stack[0] = 0;
+            sp = 1;
+            __syncwarp();
+            while (sp > 0) {
+                const int node = stack[--sp];
+                __syncwarp();
+                const int2 ch = B.child[node];
 #pragma unroll
-                    for (int k = 0; k < 2; ++k) {
-                        const int cn = c2[k];
-                        if (!box_hit(qlo, qhi, B.lo[cn], B.hi[cn])) continue;
-                        if (cn >= B.n - 1) {
-                            visit_leaf(cn);
-                        } else if (sp < 64) {
-                            stack[sp++] = cn;
-                        } else {
-                            atomicOr(&P.g->error, ERR_CAP_STACK);
-                        }
+                for (int k = 0; k < 2; ++k) {
+                    const int cn = k ? ch.y : ch.x;
+                    const bool hit = box_hit(qlo, qhi, B.lo[cn], B.hi[cn]);
+                    if (!__any_sync(0xffffffffu, hit)) continue;
+                    if (cn >= B.n - 1) {
+                        if (hit) visit_leaf(cn);
+                    } else if (sp < TRAV_STACK) {
+                        if (lane == 0) stack[sp] = cn;
+                        ++sp;
+                    } else if (lane == 0) {
+                        atomicOr(&P.g->error, ERR_CAP_STACK);
                     }
                 }
+                __syncwarp();
             }
         }
         P.qcount[q] = cnt;
@@ -306,7 +315,9 @@ __device__ void ph_query_totals(const Params& P) {
 }
 
 __device__ __forceinline__ void vertex_min(const Params& P, int v, double d) {
-    atomicMin(&P.dmin[v], to_b(d));
+    const unsigned long long b = to_b(d);
+    // the bound only decreases: skip the atomic when it cannot lower it
+    if (b < *((volatile unsigned long long*)&P.dmin[v])) atomicMin(&P.dmin[v], b);
 }
 
 // contact predicate of linearize_all (constraints.cpp:186-199): active,
