@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--scene", choices=["bow", "reef"], default="bow")
     ap.add_argument("--coloring", choices=["device", "reference"], default="device")
-    ap.add_argument("--cpu-sample-steps", type=int, default=1)
+    ap.add_argument("--cpu-sample-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -148,6 +148,22 @@ def bytes_per_resolve(trace, sc, sweeps=1):
     return total
 
 
+def max_over_ranks(vals, dist, device):
+    """Elementwise max over ranks of per-rank timings (ms); identity at N = 1."""
+    import torch
+
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
+def whole_job_rate(world, steps, ms_max):
+    """Resolves per second over all ranks: every rank resolves its own scene
+    `steps` times, the job takes the slowest rank's time (weak scaling)."""
+    return world * steps / (ms_max / 1e3)
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -223,12 +239,9 @@ def run_ours(args):
     clk = clocks.stop()
     barrier()
 
-    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_ms_max, e2e_ms_max = float(t[0]), float(t[1])
-    value = world * args.steps / (dev_ms_max / 1e3)
-    e2e_value = world * args.steps / (e2e_ms_max / 1e3)
+    dev_ms_max, e2e_ms_max = max_over_ranks([dev_ms, e2e_ms], dist, "cuda")
+    value = whole_job_rate(world, args.steps, dev_ms_max)
+    e2e_value = whole_job_rate(world, args.steps, e2e_ms_max)
     kern_avg_ms = sum(kernel_ms) / len(kernel_ms)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
@@ -266,56 +279,85 @@ def run_ours(args):
     return out, sc, st_tr
 
 
-def cpu_baseline(sc, gpu_trace, sample_steps):
-    """Oracle (single-threaded restatement of the reference) on the first
-    `sample_steps` Alg.-1 steps of the same resolve, extrapolated with the
-    per-step search pattern the (bit-identical) device run took."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle
+class OracleSampler:
+    """Bounded CPU sample of the bow-knot resolve on the C oracle (the
+    single-threaded restatement of the reference, oracle/): the proximity
+    search at x (proximity.cpp:87-181) timed once, and single non-search
+    Alg.-1 steps (refresh, per-vertex bound, linearize, color, assemble + PGS +
+    recover, advance: resolve.cpp:64-131) timed per sample. A full resolve is
+    estimated as searches x t_search + steps x t_step with the step/search
+    counts of the (bit-identical) device run."""
 
-    t0 = time.perf_counter()
-    _, st = pyoracle.resolve(sc, step_limit=sample_steps, trace=True, **RESOLVE_KW)
-    dt = time.perf_counter() - t0
-    nsteps = len(gpu_trace)
-    per_step = dt / st["steps"]
-    est = per_step * nsteps  # every sampled step includes a search (step 0 always searches)
-    searches = sum(t["searched"] for t in gpu_trace)
+    def __init__(self, sc):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import numpy as np
+        import pyoracle
+
+        self.np, self.po, self.sc = np, pyoracle, sc
+        cfg = pyoracle.default_config(**RESOLVE_KW)
+        self.cfg = cfg
+        inv = sc.inv_mass
+        self.y = np.where((inv == 0)[:, None], sc.x, sc.y)  # static override (resolve.cpp:47-50)
+        E = np.asarray(sc.edges).reshape(-1, 2)
+        self.ly = np.linalg.norm(self.y[E[:, 0]] - self.y[E[:, 1]], axis=1)
+        t0 = time.perf_counter()
+        self.pairs = pyoracle.search(sc, sc.x, cfg.d_max, cap=160 * sc.nv)
+        self.t_search = time.perf_counter() - t0
+
+    def step(self):
+        po, sc, cfg = self.po, self.sc, self.cfg
+        t0 = time.perf_counter()
+        po.refresh(sc, sc.x, cfg.d_max, self.pairs)
+        D = po.vertex_bound(sc, cfg.d_max, self.pairs, sc.nv)
+        rows = po.linearize(sc, sc.x, self.pairs, self.ly, delta=cfg.delta, sigma=cfg.sigma)
+        nc, col = po.color(sc, rows, cfg.color_seed, mode=cfg.coloring_mode)
+        b = po.backward(sc.inv_mass, rows, col, nc, sc.x, self.y)
+        po.advance(sc.inv_mass, b["y"], D, cfg.gamma, sc.x, self.np.ones(sc.nv))
+        return time.perf_counter() - t0
+
+    def describe(self, nsamples, nsteps, nsearch):
+        return (f"C oracle on the host, 1 thread: the bow-knot proximity search timed once "
+                f"({self.t_search:.1f} s, {len(self.pairs)} pairs) + the median of {nsamples} single "
+                f"non-search Alg.-1 steps; estimate = {nsearch} searches + {nsteps} steps of the device run")
+
+
+def cpu_baseline(sc, gpu_trace, nsamples):
+    """cpu_baseline of the ours-arm line (rank 0, N = 1; ~45 s of host work)."""
+    s = OracleSampler(sc)
+    t_step = statistics.median([s.step() for _ in range(max(1, nsamples))])
+    nsteps, nsearch = len(gpu_trace), sum(t["searched"] for t in gpu_trace)
+    est = nsearch * s.t_search + nsteps * t_step
     return {"value": round(1.0 / est, 6), "unit": "steps/s", "cores": 1, "kind": "port",
-            "sample": f"first {st['steps']} Alg.-1 step(s) of the same bow-knot resolve on the C oracle "
-                      f"({dt:.1f} s, search included), extrapolated to the {nsteps} steps / {searches} searches "
-                      f"the device run takes",
-            "seconds_per_alg1_step": round(per_step, 3)}
+            "sample": s.describe(max(1, nsamples), nsteps, nsearch),
+            "seconds_search": round(s.t_search, 3), "seconds_per_step": round(t_step, 3)}
 
 
 def run_reference(args):
+    """--impl reference: the reference's algorithm on the host CPU (the C
+    oracle: the reference itself needs Eigen, absent here). Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle
-
     sc = make_scene(args.scene, 0)
     trace_path = os.path.join(ROOT, "profiles", f"{args.scene}_knot_trace.json")
-    trace = json.load(open(trace_path)) if os.path.exists(trace_path) else None
+    trace = json.load(open(trace_path))  # committed: the device run's per-step trace (deterministic)
+    nsteps, nsearch = len(trace), sum(t["searched"] for t in trace)
+    s = OracleSampler(sc)
     samples = []
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        _, st = pyoracle.resolve(sc, step_limit=args.cpu_sample_steps, trace=True, **RESOLVE_KW)
-        dt = time.perf_counter() - t0
+        dt = s.step()
         if i >= args.warmup:
-            samples.append(dt / st["steps"])
-    per_step = statistics.median(samples)
-    nsteps = len(trace) if trace else 1
-    value = 1.0 / (per_step * nsteps)
+            samples.append(dt)
+    t_step = statistics.median(samples)
+    value = 1.0 / (nsearch * s.t_search + nsteps * t_step)
     return {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "steps/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": scene_config(sc, args),
             "cpu_baseline": {"value": round(value, 6), "unit": "steps/s", "cores": 1, "kind": "port",
-                             "sample": f"each step: the first {args.cpu_sample_steps} Alg.-1 step(s) (search "
-                                       f"included) of the bow-knot resolve on the single-threaded C oracle, "
-                                       f"extrapolated to the {nsteps} steps of the full resolve "
-                                       f"(profiles/{args.scene}_knot_trace.json)"},
+                             "sample": s.describe(args.steps, nsteps, nsearch) +
+                             f" (profiles/{args.scene}_knot_trace.json)",
+                             "seconds_search": round(s.t_search, 3), "seconds_per_step": round(t_step, 3)},
             "e2e": {"value": round(value, 6), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

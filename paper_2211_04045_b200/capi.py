@@ -232,19 +232,20 @@ def phase_profile(ctx: Context):
     L = lib()
     L.tw_ctx_phase_profile.restype = C.c_int32
     L.tw_ctx_phase_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]
-    sites = np.zeros(128, np.int32)
-    ms = np.zeros(128)
-    cnt = np.zeros(128, np.int32)
-    n = L.tw_ctx_phase_profile(ctx.h, _p(sites), _p(ms), _p(cnt), 128)
+    NS = 256  # kPhaseSites (csrc/tw_engine.cuh)
+    sites = np.zeros(NS, np.int32)
+    ms = np.zeros(NS)
+    cnt = np.zeros(NS, np.int32)
+    n = L.tw_ctx_phase_profile(ctx.h, _p(sites), _p(ms), _p(cnt), NS)
     src = open(os.path.join(_HERE, "csrc", "tw_kernels.cu")).read().splitlines()
     names = {}
     for i, line in enumerate(src, start=1):
         if line.strip() == "SYNC();":
             prev = src[i - 2]
             m = re.search(r"(ph_[a-z_]+)", prev)
-            names[i & 127] = m.group(1) if m else f"line{i}"
+            names[i % NS] = m.group(1) if m else f"line{i}"
     out = {}
-    for k in range(min(n, 128)):
+    for k in range(min(n, NS)):
         name = names.get(int(sites[k]), f"site{int(sites[k])}")
         a, b = out.get(name, (0.0, 0))
         out[name] = (a + float(ms[k]), b + int(cnt[k]))

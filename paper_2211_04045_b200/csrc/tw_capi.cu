@@ -64,6 +64,7 @@ struct tw_ctx {
     int sm_count = 0;
     int nblocks = 0;
     int minb = 4;  // resolve-kernel instance (CTAs per SM)
+    long long pgs_tail_rows = 512;  // TW_PGS_TAIL
     long long launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk = nullptr;
     // capacities
@@ -78,8 +79,8 @@ struct tw_ctx {
     DevMem ly, is_er, er_edge, er_index, er_value, er_g, er_q, edge_lambda, er_color, er_by_color, er_color_off,
         er_color_cnt;
     DevMem pkey, pids, pdd, pw, pflag, qcount, qslot, qoff;
-    DevMem c_key, c_ids, c_jac, c_value, c_diag, c_q, c_lambda, c_next, c_color, c_stamp, c_arch, c_prio, c_by_color,
-        c_tent;
+    DevMem c_key, c_ids, c_jac, c_value, c_diag, c_q, c_lambda, c_next, c_color, c_stamp, c_arch, c_lost, c_by_color,
+        c_tent, vmask, vbig;
     DevMem ccount, coff;
     DevMem arch_key0, arch_key1, arch_val0, arch_val1, new_lb, new_key, new_val;
     DevMem refpool;
@@ -227,7 +228,9 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     CK(ctx->c_stamp.ensure(P * 4));
     CK(ctx->c_tent.ensure(P * 4));
     CK(ctx->c_arch.ensure(P * 8));
-    CK(ctx->c_prio.ensure(P * 8));
+    CK(ctx->c_lost.ensure(P * 4));
+    CK(ctx->vmask.ensure(nv * 32));
+    CK(ctx->vbig.ensure(nv * 4));
     CK(ctx->c_by_color.ensure(P * 4));
     CK(ctx->ccount.ensure((size_t)ctx->colcap * 4));
     CK(ctx->coff.ensure(((size_t)ctx->colcap + 1) * 4));
@@ -331,7 +334,9 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.c_stamp = ctx->c_stamp.as<int>();
     P.c_tent = ctx->c_tent.as<int>();
     P.c_arch = ctx->c_arch.as<long long>();
-    P.c_prio = ctx->c_prio.as<uint64_t>();
+    P.c_lost = ctx->c_lost.as<int>();
+    P.vmask = ctx->vmask.as<unsigned long long>();
+    P.vbig = ctx->vbig.as<int>();
     P.c_by_color = ctx->c_by_color.as<int>();
     P.voff = ctx->voff.as<int>();
     P.vinc = ctx->vinc.as<int>();
@@ -353,6 +358,7 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.refpool_cap = ctx->refpool_cap;
     P.refpool = ctx->refpool.as<int>();
     P.nblocks = ctx->nblocks;
+    P.pgs_tail_rows = ctx->pgs_tail_rows;
     P.part_q = ctx->part_q.as<long long>();
     P.part_c = ctx->part_c.as<long long>();
     P.part_k = ctx->part_k.as<long long>();
@@ -394,6 +400,7 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
         int rc = ensure_buffers(ctx, m, cfg);
         if (rc) return rc;
         Params P = make_params(ctx, m, cfg);
+        if (!trace_host) P.trace = nullptr;  // lets the kernel skip work only a trace would show
         CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), ctx->stream));
         // color tables return to zero at the end of every step; an attempt
         // aborted for capacity growth may leave counts behind
@@ -528,6 +535,7 @@ int tw_ctx_create(int device, void* stream, tw_ctx** out) {
     int want = 4;  // measured best on B200 (bow knot): 64 regs, 32 warps/SM
     if (const char* s = std::getenv("TW_BLOCKS_PER_SM")) want = std::min(4, std::max(2, std::atoi(s)));
     ctx->minb = want;
+    if (const char* s = std::getenv("TW_PGS_TAIL")) ctx->pgs_tail_rows = std::max(0LL, std::atoll(s));
     const int per_sm = std::max(1, std::min(resolve_blocks_per_sm(want), want));
     ctx->nblocks = std::min(ctx->sm_count * per_sm, tw::MAX_BLOCKS);
     if (stream) {
@@ -563,7 +571,7 @@ void tw_ctx_destroy(tw_ctx* ctx) {
                      &ctx->er_color_cnt, &ctx->pkey, &ctx->pids, &ctx->pdd, &ctx->pw, &ctx->pflag, &ctx->qcount,
                      &ctx->qslot, &ctx->qoff, &ctx->c_key, &ctx->c_ids, &ctx->c_jac, &ctx->c_value, &ctx->c_diag, &ctx->c_q,
                      &ctx->c_lambda, &ctx->c_next, &ctx->c_color, &ctx->c_stamp, &ctx->c_tent, &ctx->c_arch,
-                     &ctx->c_prio,
+                     &ctx->c_lost, &ctx->vmask, &ctx->vbig,
                      &ctx->c_by_color, &ctx->ccount, &ctx->coff, &ctx->arch_key0, &ctx->arch_key1,
                      &ctx->arch_val0, &ctx->arch_val1, &ctx->new_lb, &ctx->new_key, &ctx->new_val, &ctx->refpool,
                      &ctx->part_q, &ctx->part_c, &ctx->part_k, &ctx->blk_lo, &ctx->blk_hi, &ctx->globals, &ctx->box,
@@ -777,7 +785,7 @@ int tw_resolve_device(tw_ctx* ctx, tw_mesh* m, const double* d_x, const double* 
 int32_t tw_ctx_phase_profile(const tw_ctx* ctx, int32_t* sites, double* ms, int32_t* counts, int32_t cap) {
     if (!ctx) return 0;
     int n = 0;
-    for (int i = 0; i < 128; ++i) {
+    for (int i = 0; i < kPhaseSites; ++i) {
         if (!ctx->last.phase_cnt[i]) continue;
         if (n < cap) {
             sites[n] = i;

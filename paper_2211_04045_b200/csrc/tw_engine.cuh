@@ -21,6 +21,7 @@ namespace tw {
 
 constexpr int TPB = 256;  // threads per block of every engine kernel
 constexpr int MAX_BLOCKS = 1024;
+constexpr int kPhaseSites = 256;  // phase-profile slots, indexed by SYNC() source line mod 256
 
 enum : int {
     ERR_CAP_SLOTS = 1,    // a broad-phase query produced more than K candidates
@@ -78,8 +79,8 @@ struct Globals {
     long long rows_solved;
     // phase profile (CTA 0 barrier-to-barrier wall time per call site)
     unsigned long long phase_t0;
-    unsigned long long phase_ns[128];
-    unsigned int phase_cnt[128];
+    unsigned long long phase_ns[kPhaseSites];
+    unsigned int phase_cnt[kPhaseSites];
 };
 
 struct Config {
@@ -158,8 +159,12 @@ struct Params {
     int* c_tent;     // coloring proposals
     int* c_stamp;
     long long* c_arch;  // archive index, or -(lower_bound)-1
-    uint64_t* c_prio;
+    int* c_lost;        // coloring: round in which the row's proposal lost
     int* c_by_color;
+    // coloring: per-vertex mask of the colors < 256 taken around the vertex
+    // (edge rows + contact rows colored so far), and a flag for colors >= 256
+    unsigned long long* vmask;  // 4 per vertex
+    int* vbig;
     // vertex -> contact-row incidence, CSR rebuilt every step (entry = 4*row + m)
     int* vcnt;      // entries per vertex (nv)
     int* voff;      // segment offsets (nv + 1)
@@ -180,6 +185,9 @@ struct Params {
     // reference coloring scratch
     long long refpool_cap;
     int* refpool;
+    // PGS colors with at most this many rows at the end of the color order run
+    // on one CTA (ph_pgs_tail); 0 disables
+    long long pgs_tail_rows;
     // per block scratch
     int nblocks;
     long long* part_q;

@@ -267,8 +267,8 @@ __device__ bool prologue(const Params& P) {
         if (!grid_sync(g)) return;                                                \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                                \
             const unsigned long long now_ = global_ns();                          \
-            g->phase_ns[__LINE__ & 127] += now_ - g->phase_t0;                    \
-            g->phase_cnt[__LINE__ & 127] += 1;                                    \
+            g->phase_ns[__LINE__ % kPhaseSites] += now_ - g->phase_t0;                    \
+            g->phase_cnt[__LINE__ % kPhaseSites] += 1;                                    \
             g->phase_t0 = now_;                                                   \
         }                                                                         \
     } while (0)
@@ -345,9 +345,15 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
             ncol_c = ncol_e = ncol;
         } else {
             for (int k = 1; *((volatile int*)&g->colored) < nc; ++k) {
+                if (k > 1) {
+                    ph_color_rank(P);
+                    SYNC();
+                }
                 ph_color_propose(P, nc, k);
                 SYNC();
-                ph_color_finalize(P, nc, k);
+                ph_color_conflict(P, k);
+                SYNC();
+                ph_color_commit(P, nc, k);
                 SYNC();
             }
             ncol_c = g->max_color + 1;
@@ -359,11 +365,17 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
             SYNC();
         }
         if (C.solver == 0) {
-            for (int sw = 0; sw < C.sweeps; ++sw)
-                for (int c = 0; c < ncol; ++c) {
+            const int ctail = first_tail_color(P, ncol, ncol_c, ncol_e, P.pgs_tail_rows);
+            for (int sw = 0; sw < C.sweeps; ++sw) {
+                for (int c = 0; c < ctail; ++c) {
                     ph_pgs_color(P, c, ncol_c, ncol_e);
                     SYNC();
                 }
+                if (ctail < ncol) {
+                    ph_pgs_tail(P, ctail, ncol, ncol_c, ncol_e);
+                    SYNC();
+                }
+            }
         } else {
             for (int sw = 0; sw < C.sweeps; ++sw) {
                 ph_jacobi_next(P, nc);
@@ -399,8 +411,17 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
             sel ^= 1;
             narch += nnew;
         }
-        ph_refresh(P, bound, next_search, true, sel, narch);
-        SYNC();
+        // refresh at x^(l+1) (resolve.cpp:120-123). Without a trace to fill,
+        // the refresh after the final step has no observable effect, and
+        // before a re-search only its multiplier erasures matter.
+        const bool final_step = residual < C.eps || l + 1 == C.step_limit;
+        if (P.trace || (!final_step && !next_search)) {
+            ph_refresh(P, bound, next_search, true, sel, narch);
+            SYNC();
+        } else if (!final_step && narch > 0) {
+            ph_refresh_archive(P, bound, sel, narch);
+            SYNC();
+        }
         if (lead && P.trace) {
             Trace& t = P.trace[l];
             t.searched = search;

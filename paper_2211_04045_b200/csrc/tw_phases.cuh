@@ -15,25 +15,28 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-// Sense-free generation barrier over all CTAs of a cooperative launch. Thread 0
-// of each CTA releases its CTA's writes (fence), arrives, and the last arriver
-// bumps the generation. A 20 s watchdog turns a hang into ERR_TIMEOUT.
+// Grid barrier over all CTAs of a cooperative launch, one atomic per CTA:
+// CTA 0 adds 2^31 - (nblocks - 1), every other CTA adds 1, so the arrival
+// that completes the count flips bit 31 and the waiters watch for the flip
+// (no separate release store: ~1.6 us per barrier at 592 CTAs on B200 against
+// 3.3 us for arrive + generation bump, tools/bar_bench.cu). A waiter also
+// leaves when the error word is set — CTAs that bail out on an error may
+// never arrive — and a 20 s watchdog turns any other hang into ERR_TIMEOUT.
 __device__ __forceinline__ bool grid_sync(Globals* g) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* genp = &g->bar_gen;
-        const unsigned gen = *genp;
+        const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
         __threadfence();
-        const unsigned arrived = atomicAdd(&g->bar_count, 1u);
-        if (arrived == gridDim.x - 1) {
-            atomicExch(&g->bar_count, 0u);
-            __threadfence();
-            atomicAdd(&g->bar_gen, 1u);
-        } else {
-            const unsigned long long t0 = global_ns();
-            while (*genp == gen) {
-                __nanosleep(32);
-                if (global_ns() - t0 > 20000000000ull) {
+        const unsigned old = atomicAdd(&g->bar_count, inc);
+        volatile unsigned* cnt = &g->bar_count;
+        volatile int* err = &g->error;
+        unsigned long long t0 = 0;
+        for (unsigned it = 0; ((old ^ *cnt) & 0x80000000u) == 0u; ++it) {
+            if ((it & 63u) == 63u) {
+                if (*err) break;
+                const unsigned long long t = global_ns();
+                if (t0 == 0) t0 = t;
+                else if (t - t0 > 20000000000ull) {
                     atomicOr(&g->error, ERR_TIMEOUT);
                     break;
                 }
@@ -709,51 +712,130 @@ __device__ void ph_warm(const Params& P, long long nc) {
             }
         }
         P.imp[v] = make_double4(a.x, a.y, a.z, 0.0);
+        if (P.cfg.coloring_mode == 1) {
+            // device coloring: the vertex starts with the colors of its edge rows
+            unsigned long long mk4[4] = {0, 0, 0, 0};
+            int big = 0;
+            if (im > 0.0 && P.cfg.edge_constraints)
+                for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
+                    const int ec = P.edge_color[P.vedge[q]];
+                    if (ec >= 256) big = 1;
+                    else if (ec >= 0) mk4[ec >> 6] |= 1ull << (ec & 63);
+                }
+            for (int w = 0; w < 4; ++w) P.vmask[4 * v + w] = mk4[w];
+            P.vbig[v] = big;
+        }
     }
-    // coloring priority: the lower row index (pair order) wins, so the rounds
-    // reproduce the sequential greedy coloring in row order
     for (long long i = gtid(); i < nc; i += gstride()) {
-        P.c_prio[i] = (uint64_t)(nc - i);
         P.c_stamp[i] = 0;
+        P.c_lost[i] = 0;
         P.c_color[i] = -1;
     }
 }
 
 // ============================================================ coloring
-// C (device mode), speculative greedy coloring. Round k, propose: every row
-// still uncolored proposes the smallest color not used by neighbors colored in
-// earlier rounds (nor by the incident edge rows). Finalize: a proposal is kept
-// unless an uncolored-at-round-start neighbor proposed the same color and has
-// the higher (priority, index). Typically converges in a handful of rounds.
-__device__ void ph_color_finalize(const Params& P, long long nc, int k) {
-    for (long long i = gtid(); i < nc; i += gstride()) {
-        if (P.c_stamp[i] != 0) continue;
-        const int4 id = P.c_ids[i];
-        const int vv[4] = {id.x, id.y, id.z, id.w};
-        const int ti = P.c_tent[i];
-        bool lose = false;
-        // rows beating this one (lower index) precede its entry in the sorted segments
-        for (int m = 0; m < 4 && !lose; ++m) {
-            const int v = vv[m];
-            if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
-            const int b = P.voff[v], pos = P.erank[4 * i + m];
-            for (int t = b; t < b + pos; ++t) {
-                const int j = P.vinc[t] >> 2;
-                const int sj = *((volatile int*)&P.c_stamp[j]);
-                if (sj != 0 && sj != k) continue;
-                if (P.c_tent[j] == ti) {
-                    lose = true;
-                    break;
-                }
+// C (device mode), speculative greedy coloring in rounds; the lower row index
+// (pair order) has priority, so a round reproduces the sequential greedy
+// coloring in row order wherever it does not conflict. Round k:
+//   rank     (vertex pass) every uncolored entry learns how many uncolored
+//            entries precede it in its vertex segment (segments are sorted by
+//            row index; round 1: its position, set by ph_warm);
+//   propose  (row pass) an uncolored row proposes the rank-th color free at
+//            all of its dynamic vertices (rank = max over the vertices), so
+//            the rows of a clique propose distinct colors;
+//   conflict (vertex pass) a proposal loses if an earlier uncolored entry of
+//            one of its segments proposed the same color;
+//   commit   (row pass) the winners take their color and mark it in the
+//            color masks of their vertices.
+// The oracle's or_color_device (oracle/or_constraints.c) states the same
+// rounds row by row.
+__device__ __forceinline__ long long gwarp() { return gtid() >> 5; }
+__device__ __forceinline__ long long gwarps() { return gstride() >> 5; }
+
+__device__ void ph_color_rank(const Params& P) {
+    const int lane = threadIdx.x & 31;
+    for (long long v = gwarp(); v < P.nv; v += gwarps()) {
+        const int b = P.voff[v], e = P.voff[v + 1];
+        int run = 0;
+        for (int t0 = b; t0 < e; t0 += 32) {
+            const int t = t0 + lane;
+            int ent = 0;
+            bool unc = false;
+            if (t < e) {
+                ent = P.vinc[t];
+                unc = P.c_stamp[ent >> 2] == 0;
             }
+            const unsigned bal = __ballot_sync(0xffffffffu, unc);
+            if (unc) P.erank[ent] = run + __popc(bal & ((1u << lane) - 1u));
+            run += __popc(bal);
         }
-        if (lose) continue;
+    }
+}
+
+__device__ void ph_color_conflict(const Params& P, int k) {
+    __shared__ unsigned long long seen[TPB / 32][4];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (long long v = gwarp(); v < P.nv; v += gwarps()) {
+        const int b = P.voff[v], e = P.voff[v + 1];
+        if (b == e) continue;
+        if (lane < 4) seen[w][lane] = 0ull;
+        __syncwarp();
+        for (int t0 = b; t0 < e; t0 += 32) {
+            const int t = t0 + lane;
+            int row = -1, tc = -1;
+            if (t < e) {
+                row = P.vinc[t] >> 2;
+                if (P.c_stamp[row] == 0) tc = P.c_tent[row];
+            }
+            const bool unc = tc >= 0;
+            const unsigned um = __ballot_sync(0xffffffffu, unc);
+            const unsigned peers = __match_any_sync(0xffffffffu, tc);
+            if (unc) {
+                bool dup = (peers & um & ((1u << lane) - 1u)) != 0u;
+                if (!dup) {
+                    if (tc < 256) {
+                        dup = (seen[w][tc >> 6] >> (tc & 63)) & 1ull;
+                    } else {
+                        for (int s = b; s < t0 && !dup; ++s) {
+                            const int r2 = P.vinc[s] >> 2;
+                            dup = P.c_stamp[r2] == 0 && P.c_tent[r2] == tc;
+                        }
+                    }
+                }
+                if (dup) P.c_lost[row] = k;
+            }
+            __syncwarp();
+            if (unc && tc < 256) atomicOr(&seen[w][tc >> 6], 1ull << (tc & 63));
+            __syncwarp();
+        }
+    }
+}
+
+__device__ void ph_color_commit(const Params& P, long long nc, int k) {
+    int ncolored = 0, maxc = -1;
+    for (long long i = gtid(); i < nc; i += gstride()) {
+        if (P.c_stamp[i] != 0 || P.c_lost[i] == k) continue;
+        const int ti = P.c_tent[i];
         P.c_color[i] = ti;
         P.c_stamp[i] = k;
-        atomicAdd(&P.g->colored, 1);
-        atomicMax(&P.g->max_color, ti);
+        ++ncolored;
+        maxc = max(maxc, ti);
         if (ti < P.colcap) atomicAdd(&P.ccount[ti], 1);
         else atomicOr(&P.g->error, ERR_CAP_COLORS);
+        const int4 id = P.c_ids[i];
+        const int vv[4] = {id.x, id.y, id.z, id.w};
+        for (int m = 0; m < 4; ++m) {
+            const int v = vv[m];
+            if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
+            if (ti < 256) atomicOr(&P.vmask[4LL * v + (ti >> 6)], 1ull << (ti & 63));
+            else P.vbig[v] = 1;
+        }
+    }
+    const int wn = __reduce_add_sync(0xffffffffu, (unsigned)ncolored);
+    const int wm = __reduce_max_sync(0xffffffffu, maxc);
+    if ((threadIdx.x & 31) == 0 && wn > 0) {
+        atomicAdd(&P.g->colored, wn);
+        atomicMax(&P.g->max_color, wm);
     }
 }
 
@@ -764,36 +846,15 @@ __device__ void ph_color_propose(const Params& P, long long nc, int k) {
         const int vv[4] = {id.x, id.y, id.z, id.w};
         unsigned long long used[4] = {0, 0, 0, 0};
         bool big = false;
-        auto mark = [&](int c) {
-            if (c < 256) used[c >> 6] |= 1ull << (c & 63);
-            else big = true;
-        };
         int rank = 0;  // max over vertices of the uncolored rows there that beat this row
         for (int m = 0; m < 4; ++m) {
             const int v = vv[m];
             if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
-            const int b = P.voff[v], e = P.voff[v + 1], pos = P.erank[4 * i + m];
-            if (k == 1) {
-                rank = max(rank, pos);  // round 1: everything uncolored, nothing colored
-            } else {
-                int rank_v = 0;
-                for (int t = b; t < e; ++t) {
-                    const int j = P.vinc[t] >> 2;
-                    if (j == i) continue;
-                    const int sj = P.c_stamp[j];
-                    if (sj == 0) {
-                        rank_v += t < b + pos;  // rows before this entry have a lower index
-                        continue;
-                    }
-                    if (sj < k) mark(P.c_color[j]);
-                }
-                rank = max(rank, rank_v);
-            }
-            if (P.cfg.edge_constraints)
-                for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
-                    const int ec = P.edge_color[P.vedge[q]];
-                    if (ec >= 0) mark(ec);
-                }
+            rank = max(rank, P.erank[4 * i + m]);
+            const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(P.vmask + 4LL * v);
+            const ulonglong2 c = *reinterpret_cast<const ulonglong2*>(P.vmask + 4LL * v + 2);
+            used[0] |= a.x, used[1] |= a.y, used[2] |= c.x, used[3] |= c.y;
+            big |= P.vbig[v] != 0;
         }
         // propose the rank-th free color: a clique of uncolored rows takes
         // distinct colors in priority order within one round
@@ -1173,15 +1234,54 @@ __device__ __forceinline__ void pgs_edge_row(const Params& P, int e) {
     P.edge_lambda[e] = lam;
 }
 
+// rows of color c: contact rows first, then edge rows (any order inside a
+// color gives the same result: its rows touch disjoint dynamic vertices)
+__device__ __forceinline__ void pgs_color_range(const Params& P, int c, int ncol_contact, int ncol_edge,
+                                                long long* c0, long long* nci, long long* e0, long long* n) {
+    *c0 = c < ncol_contact ? P.coff[c] : 0;
+    *nci = c < ncol_contact ? P.coff[c + 1] - *c0 : 0;
+    long long e1 = 0;
+    *e0 = 0;
+    if (P.cfg.edge_constraints && c < ncol_edge) *e0 = P.er_color_off[c], e1 = P.er_color_off[c + 1];
+    *n = *nci + (e1 - *e0);
+}
+
 __device__ void ph_pgs_color(const Params& P, int c, int ncol_contact, int ncol_edge) {
-    const long long c0 = c < ncol_contact ? P.coff[c] : 0, c1 = c < ncol_contact ? P.coff[c + 1] : 0;
-    const long long nci = c1 - c0;
-    long long e0 = 0, e1 = 0;
-    if (P.cfg.edge_constraints && c < ncol_edge) e0 = P.er_color_off[c], e1 = P.er_color_off[c + 1];
-    const long long n = nci + (e1 - e0);
+    long long c0, nci, e0, n;
+    pgs_color_range(P, c, ncol_contact, ncol_edge, &c0, &nci, &e0, &n);
     for (long long k = gtid(); k < n; k += gstride()) {
         if (k < nci) pgs_contact_row(P, P.c_by_color[c0 + k]);
         else pgs_edge_row(P, P.er_by_color[e0 + (k - nci)]);
+    }
+}
+
+// The trailing colors of a coloring are small (greedy coloring: the last
+// colors pick up the few rows of the densest cliques): a grid-wide phase per
+// color would cost a grid barrier for a handful of rows. first_tail_color
+// returns the first color of the longest suffix of colors with at most
+// `tail_rows` rows each; ph_pgs_tail runs those colors in order on CTA 0
+// alone, with CTA barriers between colors.
+__device__ int first_tail_color(const Params& P, int ncol, int ncol_contact, int ncol_edge, long long tail_rows) {
+    int c = ncol;
+    while (c > 0) {
+        long long c0, nci, e0, n;
+        pgs_color_range(P, c - 1, ncol_contact, ncol_edge, &c0, &nci, &e0, &n);
+        if (n > tail_rows) break;
+        --c;
+    }
+    return c;
+}
+
+__device__ void ph_pgs_tail(const Params& P, int cfirst, int ncol, int ncol_contact, int ncol_edge) {
+    if (blockIdx.x != 0) return;
+    for (int c = cfirst; c < ncol; ++c) {
+        long long c0, nci, e0, n;
+        pgs_color_range(P, c, ncol_contact, ncol_edge, &c0, &nci, &e0, &n);
+        for (long long k = threadIdx.x; k < n; k += TPB) {
+            if (k < nci) pgs_contact_row(P, P.c_by_color[c0 + k]);
+            else pgs_edge_row(P, P.er_by_color[e0 + (k - nci)]);
+        }
+        __syncthreads();
     }
 }
 
@@ -1426,6 +1526,35 @@ __device__ void ph_refresh(const Params& P, double bound, bool next_search, bool
         atomicAdd(&P.g->nactive, (int)na);
         atomicAdd((unsigned long long*)&P.g->pairs_evaluated, (unsigned long long)(hi - lo));
     }
+}
+
+// E2' (no trace requested, the next step re-searches): the refreshed pair
+// records are discarded by the search, and the vertex bound is not needed, so
+// the only lasting effect of refresh_distances + the erase loop
+// (resolve.cpp:120-123) is on the multipliers stored for pairs of the set.
+// Evaluate just the pairs whose key has a live archive entry (the archive is
+// a subset of all contact rows ever solved, the set is sorted by key) and
+// tombstone the ones that become inactive.
+__device__ void ph_refresh_archive(const Params& P, double bound, int sel, long long narch) {
+    const long long np = P.g->np;
+    const uint64_t* akey = P.arch_key[sel];
+    double* aval = P.arch_val[sel];
+    long long evals = 0;
+    for (long long a = gtid(); a < narch; a += gstride()) {
+        if (isnan(aval[a])) continue;
+        const uint64_t key = akey[a];
+        const long long p = arch_lower_bound(P.pkey, np, key);
+        if (p >= np || P.pkey[p] != key) continue;  // not in the set: kept (erase walks the set)
+        const int ka = key_ka(key), kb = key_kb(key);
+        int va[3], vb[3];
+        split_ids(ka, kb, P.pids[p], va, vb);
+        Closest c;
+        const int h = pair_closest(ka, va, kb, vb, XLoad{P.x}, c);
+        ++evals;
+        if (!(h == 1 && c.dist < bound)) aval[a] = __longlong_as_double(0x7ff8000000000000ll);
+    }
+    const long long ev = block_sum(evals);
+    if (threadIdx.x == 0) atomicAdd((unsigned long long*)&P.g->pairs_evaluated, (unsigned long long)ev);
 }
 
 }  // namespace tw

@@ -1,0 +1,126 @@
+// Grid-barrier microbenchmark: cost per barrier of the persistent kernel's
+// grid_sync variants at 148 / 296 / 592 CTAs of 256 threads (cooperative launch).
+#include <cooperative_groups.h>
+#include <cstdio>
+
+namespace cg = cooperative_groups;
+
+struct Bar {
+    unsigned count;
+    unsigned gen;
+    unsigned sub[16 * 32];
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int V>
+__device__ __forceinline__ void bar(Bar* b) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (V == 0 || V == 1) {
+            volatile unsigned* genp = &b->gen;
+            const unsigned gen = *genp;
+            __threadfence();
+            const unsigned arrived = atomicAdd(&b->count, 1u);
+            if (arrived == gridDim.x - 1) {
+                atomicExch(&b->count, 0u);
+                __threadfence();
+                atomicAdd(&b->gen, 1u);
+            } else {
+                while (*genp == gen)
+                    if (V == 0) __nanosleep(32);
+            }
+            __threadfence();
+        } else if (V == 2) {
+            const unsigned gen = ld_acquire(&b->gen);
+            const unsigned arrived = atom_add_acqrel(&b->count, 1u);
+            if (arrived == gridDim.x - 1) {
+                b->count = 0;
+                st_release(&b->gen, gen + 1);
+            } else {
+                while (ld_acquire(&b->gen) == gen) {
+                }
+            }
+        } else if (V == 3) {  // two-level arrival, 16 groups
+            const unsigned gen = ld_acquire(&b->gen);
+            const unsigned grp = blockIdx.x & 15;
+            const unsigned gsize = (gridDim.x - grp + 15) / 16;
+            const unsigned a = atom_add_acqrel(&b->sub[grp * 32], 1u);
+            bool last = false;
+            if (a == gsize - 1) {
+                b->sub[grp * 32] = 0;
+                const unsigned t = atom_add_acqrel(&b->count, 1u);
+                if (t == 15) {
+                    b->count = 0;
+                    last = true;
+                }
+            }
+            if (last) {
+                st_release(&b->gen, gen + 1);
+            } else {
+                while (ld_acquire(&b->gen) == gen) {
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+template <int V>
+__global__ void k(Bar* b, int n, unsigned long long* ns, float* sink) {
+    float acc = threadIdx.x;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int i = 0; i < n; ++i) {
+        acc = acc * 1.0001f + 1.f;
+        if (V == 4) cg::this_grid().sync();
+        else bar<V>(b);
+    }
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ns = t1 - t0;
+    if (acc == 12345.f) *sink = acc;
+}
+
+template <int V>
+void run(int nblocks, Bar* b, unsigned long long* ns, float* sink) {
+    int n = 2000;
+    void* args[] = {&b, &n, &ns, &sink};
+    cudaMemset(b, 0, sizeof(Bar));
+    cudaLaunchCooperativeKernel((const void*)k<V>, dim3(nblocks), dim3(256), args, 0, 0);
+    cudaMemset(b, 0, sizeof(Bar));
+    cudaLaunchCooperativeKernel((const void*)k<V>, dim3(nblocks), dim3(256), args, 0, 0);
+    cudaError_t e = cudaDeviceSynchronize();
+    unsigned long long h = 0;
+    cudaMemcpy(&h, ns, 8, cudaMemcpyDeviceToHost);
+    printf("variant %d blocks %4d: %s %.3f us/barrier\n", V, nblocks, cudaGetErrorString(e), h / 1e3 / n);
+}
+
+int main() {
+    Bar* b;
+    unsigned long long* ns;
+    float* sink;
+    cudaMalloc(&b, sizeof(Bar));
+    cudaMalloc(&ns, 8);
+    cudaMalloc(&sink, 4);
+    for (int nb : {148, 296, 592}) {
+        run<0>(nb, b, ns, sink);
+        run<1>(nb, b, ns, sink);
+        run<2>(nb, b, ns, sink);
+        run<3>(nb, b, ns, sink);
+        run<4>(nb, b, ns, sink);
+    }
+    return 0;
+}
