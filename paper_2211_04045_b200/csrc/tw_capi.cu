@@ -46,11 +46,10 @@ struct DevMem {
 };
 
 struct BvhMem {
-    DevMem prim, child, parent, lo, hi, flag;
+    DevMem prim, child, parent, node, flag;
     int n = 0;
     Bvh view() const {
-        return Bvh{n, prim.as<int>(), child.as<int2>(), parent.as<int>(), lo.as<float4>(), hi.as<float4>(),
-                   flag.as<unsigned>()};
+        return Bvh{n, prim.as<int>(), child.as<int2>(), parent.as<int>(), node.as<float4>(), flag.as<unsigned>()};
     }
 };
 
@@ -78,7 +77,7 @@ struct tw_ctx {
     DevMem x, yk1, r, imp, dmin, voff, vcnt, vinc, c_slot, erank, part_v;
     DevMem ly, is_er, er_edge, er_index, er_value, er_g, er_q, edge_lambda, er_color, er_by_color, er_color_off,
         er_color_cnt;
-    DevMem pkey, pids, pdd, pw, pflag, qcount, qslot, qoff;
+    DevMem pkey, pids, pdd, pw, pflag, qcount, qslot;
     DevMem c_key, c_ids, c_jac, c_value, c_diag, c_q, c_lambda, c_next, c_color, c_stamp, c_arch, c_lost, c_by_color,
         c_tent, vmask, vbig;
     DevMem ccount, coff;
@@ -215,7 +214,6 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     CK(ctx->pflag.ensure(P));
     CK(ctx->qcount.ensure((size_t)std::max(1LL, nq) * 4));
     CK(ctx->qslot.ensure((size_t)std::max(1LL, nq) * ctx->K * 4));
-    CK(ctx->qoff.ensure((size_t)(nq + 1) * 8));
     CK(ctx->c_key.ensure(P * 8));
     CK(ctx->c_ids.ensure(P * 16));
     CK(ctx->c_jac.ensure(P * 96));
@@ -321,7 +319,6 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.pflag = ctx->pflag.as<uint8_t>();
     P.qcount = ctx->qcount.as<int>();
     P.qslot = ctx->qslot.as<int>();
-    P.qoff = ctx->qoff.as<long long>();
     P.c_key = ctx->c_key.as<uint64_t>();
     P.c_ids = ctx->c_ids.as<int4>();
     P.c_jac = ctx->c_jac.as<double>();
@@ -569,7 +566,7 @@ void tw_ctx_destroy(tw_ctx* ctx) {
                      &ctx->vcnt, &ctx->ly, &ctx->is_er, &ctx->er_edge, &ctx->er_index, &ctx->er_value, &ctx->er_g,
                      &ctx->er_q, &ctx->edge_lambda, &ctx->er_color, &ctx->er_by_color, &ctx->er_color_off,
                      &ctx->er_color_cnt, &ctx->pkey, &ctx->pids, &ctx->pdd, &ctx->pw, &ctx->pflag, &ctx->qcount,
-                     &ctx->qslot, &ctx->qoff, &ctx->c_key, &ctx->c_ids, &ctx->c_jac, &ctx->c_value, &ctx->c_diag, &ctx->c_q,
+                     &ctx->qslot, &ctx->c_key, &ctx->c_ids, &ctx->c_jac, &ctx->c_value, &ctx->c_diag, &ctx->c_q,
                      &ctx->c_lambda, &ctx->c_next, &ctx->c_color, &ctx->c_stamp, &ctx->c_tent, &ctx->c_arch,
                      &ctx->c_lost, &ctx->vmask, &ctx->vbig,
                      &ctx->c_by_color, &ctx->ccount, &ctx->coff, &ctx->arch_key0, &ctx->arch_key1,
@@ -666,8 +663,7 @@ int tw_mesh_create(tw_ctx* ctx, int32_t nv, const double* inv_mass, int32_t ne_e
         if (e == cudaSuccess) e = B.prim.ensure(n * 4);
         if (e == cudaSuccess) e = B.child.ensure(n * 8);
         if (e == cudaSuccess) e = B.parent.ensure(2 * n * 4);
-        if (e == cudaSuccess) e = B.lo.ensure(2 * n * 16);
-        if (e == cudaSuccess) e = B.hi.ensure(2 * n * 16);
+        if (e == cudaSuccess) e = B.node.ensure(n * 64);  // max(1, n - 1) internal nodes
         if (e == cudaSuccess) e = B.flag.ensure(n * 4);
         if (e == cudaSuccess) e = cudaMemsetAsync(B.flag.p, 0, n * 4, s);
     }
@@ -733,7 +729,7 @@ void tw_mesh_destroy(tw_mesh* m) {
     DevMem* all[] = {&m->d_inv_mass, &m->d_edges, &m->d_tris, &m->d_iso, &m->d_vedge_off, &m->d_vedge, &m->d_edge_color};
     for (DevMem* d : all) d->release();
     for (auto& B : m->bvh) {
-        B.prim.release(), B.child.release(), B.parent.release(), B.lo.release(), B.hi.release(), B.flag.release();
+        B.prim.release(), B.child.release(), B.parent.release(), B.node.release(), B.flag.release();
     }
     delete m;
 }

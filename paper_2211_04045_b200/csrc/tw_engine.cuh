@@ -41,8 +41,13 @@ struct Bvh {
     int* prim;        // leaf slot -> primitive index
     int2* child;      // internal node -> (left, right) node ids
     int* parent;      // node -> parent (-1 for root)
-    float4* lo;       // node box lo (xyz)
-    float4* hi;       // node box hi (xyz)
+    // Traversal layout: internal node i (max(1, n-1) of them) holds the boxes
+    // of BOTH children in one 64 B line, so a traversal step is one load
+    // round: node[4i + 2s] = (lo.xyz, ref), node[4i + 2s + 1] = (hi.xyz, 0)
+    // for child slot s; ref = internal node id, or ~index for a leaf (index =
+    // triangle / edge / vertex id of the primitive). With n == 1 the single
+    // leaf sits in slot 0 of node 0 and slot 1 is an empty box.
+    float4* node;
     unsigned* flag;   // refit arrival counters (internal nodes)
 };
 
@@ -53,7 +58,6 @@ struct Globals {
     int nonfinite;
     int internal_line;
     unsigned long long work_q;  // dynamic query counter of the traversal (reset by the refit)
-    unsigned long long work_s;  // dynamic query counter of the partner sort (reset by the refit)
     int ner;             // edge rows of this call (set by the prologue)
     int needed_k;
     long long np;        // pairs in the set
@@ -145,7 +149,6 @@ struct Params {
     uint8_t* pflag;
     int* qcount;
     int* qslot;     // nq * K
-    long long* qoff;  // nq + 1 output offsets
     // ---- contact rows
     uint64_t* c_key;
     int4* c_ids;

@@ -127,32 +127,46 @@ __device__ __forceinline__ void prim_box(const Params& P, int cls, int prim, dou
     }
 }
 
+__device__ __forceinline__ int prim_to_index(const Params& P, int cls, int prim) {
+    return cls == 2 ? P.iso[prim] : prim;
+}
+
 // A1: bottom-up refit of all three hierarchies at the current positions
-// (node flags are zero on entry; the second child to arrive builds the parent)
+// (node flags are zero on entry; the second child to arrive builds the
+// parent's box). Every finished box is written into its slot of the parent's
+// packed node (Bvh::node).
 __device__ void ph_refit(const Params& P) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) P.g->work_q = 0ull, P.g->work_s = 0ull;  // traverse / sort
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.g->work_q = 0ull;  // traversal query counter
     for (int cls = 0; cls < 3; ++cls) {
         const Bvh& B = P.bvh[cls];
         if (B.n == 0) continue;
         for (long long j = gtid(); j < B.n; j += gstride()) {
             double lo[3], hi[3];
-            prim_box(P, cls, B.prim[j], lo, hi);
+            const int prim = B.prim[j];
+            prim_box(P, cls, prim, lo, hi);
+            float4 blo = make_float4(__double2float_rd(lo[0]), __double2float_rd(lo[1]), __double2float_rd(lo[2]),
+                                     __int_as_float(~prim_to_index(P, cls, prim)));
+            float4 bhi = make_float4(__double2float_ru(hi[0]), __double2float_ru(hi[1]), __double2float_ru(hi[2]), 0.f);
+            if (B.n == 1) {
+                B.node[0] = blo, B.node[1] = bhi;
+                B.node[2] = make_float4(INFINITY, INFINITY, INFINITY, __int_as_float(~0));
+                B.node[3] = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+                continue;
+            }
             int node = B.n - 1 + (int)j;
-            B.lo[node] = make_float4(__double2float_rd(lo[0]), __double2float_rd(lo[1]),
-                                     __double2float_rd(lo[2]), 0.f);
-            B.hi[node] = make_float4(__double2float_ru(hi[0]), __double2float_ru(hi[1]),
-                                     __double2float_ru(hi[2]), 0.f);
             for (;;) {
                 const int par = B.parent[node];
                 if (par < 0) break;
+                const int slot = B.child[par].x == node ? 0 : 1;
+                float4* pn = B.node + 4LL * par + 2 * slot;
+                pn[0] = blo, pn[1] = bhi;
                 __threadfence();
                 if (atomicAdd(&B.flag[par], 1u) == 0u) break;
                 __threadfence();
-                const int2 ch = B.child[par];
-                const float4 a0 = __ldcg(&B.lo[ch.x]), a1 = __ldcg(&B.hi[ch.x]);
-                const float4 b0 = __ldcg(&B.lo[ch.y]), b1 = __ldcg(&B.hi[ch.y]);
-                B.lo[par] = make_float4(fminf(a0.x, b0.x), fminf(a0.y, b0.y), fminf(a0.z, b0.z), 0.f);
-                B.hi[par] = make_float4(fmaxf(a1.x, b1.x), fmaxf(a1.y, b1.y), fmaxf(a1.z, b1.z), 0.f);
+                const float4* q = B.node + 4LL * par;
+                const float4 a0 = __ldcg(q), a1 = __ldcg(q + 1), b0 = __ldcg(q + 2), b1 = __ldcg(q + 3);
+                blo = make_float4(fminf(a0.x, b0.x), fminf(a0.y, b0.y), fminf(a0.z, b0.z), __int_as_float(par));
+                bhi = make_float4(fmaxf(a1.x, b1.x), fmaxf(a1.y, b1.y), fmaxf(a1.z, b1.z), 0.f);
                 node = par;
             }
         }
@@ -197,11 +211,6 @@ __device__ __forceinline__ void simplex_ids(const Params& P, int k, int idx, int
     }
 }
 
-// primitive -> simplex index of the b side for class cls
-__device__ __forceinline__ int prim_to_index(const Params& P, int cls, int prim) {
-    return cls == 2 ? P.iso[prim] : prim;
-}
-
 // The exact narrow-phase test of the reference search (proximity.cpp:162-167):
 // canonical candidate, non-adjacent, has a closest point, distance < d_max.
 __device__ __forceinline__ bool candidate_keep(const Params& P, int ka, int ia, const int* va,
@@ -212,6 +221,46 @@ __device__ __forceinline__ bool candidate_keep(const Params& P, int ka, int ia, 
     simplex_ids(P, kb, ib, vb);
     const int h = pair_closest(ka, va, kb, vb, XLoad{P.x}, c);
     return h == 1 && c.dist < P.cfg.d_max;
+}
+
+// ascending bitonic sort of 64 ints held as (a, b) = elements (lane, lane + 32)
+__device__ __forceinline__ void bitonic64(int& a, int& b, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {  // k == 64: partner is the other register of this lane
+                const int lo = min(a, b), hi = max(a, b);
+                a = lo, b = hi;
+                continue;
+            }
+            const int pa = __shfl_xor_sync(0xffffffffu, a, j);
+            const int pb = __shfl_xor_sync(0xffffffffu, b, j);
+            const bool low = (lane & j) == 0;
+            const bool up_a = (lane & k) == 0, up_b = ((lane + 32) & k) == 0;
+            a = (up_a == low) ? min(a, pa) : max(a, pa);
+            b = (up_b == low) ? min(b, pb) : max(b, pb);
+        }
+    }
+}
+
+// warp-cooperative ascending sort of one query's partner list (n >= 2)
+__device__ __forceinline__ void sort_partners(int* s, int n, int lane) {
+    if (n <= 64) {
+        int a = lane < n ? s[lane] : 0x7fffffff;
+        int b = lane + 32 < n ? s[lane + 32] : 0x7fffffff;
+        bitonic64(a, b, lane);
+        if (lane < n) s[lane] = a;
+        if (lane + 32 < n) s[lane + 32] = b;
+    } else if (lane == 0) {
+        for (int i = 1; i < n; ++i) {
+            const int v = s[i];
+            int j = i - 1;
+            while (j >= 0 && s[j] > v) s[j + 1] = s[j], --j;
+            s[j + 1] = v;
+        }
+    }
+    __syncwarp();
 }
 
 // A2: traverse every query and record the surviving partners. A warp takes 32
@@ -258,8 +307,7 @@ __device__ void ph_traverse(const Params& P) {
                               __double2float_ru(hi3[2] + infl), 0.f);
         }
         int* slots = P.qslot + q * P.K;
-        auto visit_leaf = [&](int node) {
-            const int ib = prim_to_index(P, cls, B.prim[node - (B.n - 1)]);
+        auto visit_leaf = [&](int ib) {
             Closest c;
             ++evals;
             if (candidate_keep(P, ka, ia, va, kb, ib, c)) {
@@ -267,9 +315,7 @@ __device__ void ph_traverse(const Params& P) {
                 ++cnt;
             }
         };
-        if (B.n == 1) {
-            if (ia >= 0 && box_hit(qlo, qhi, B.lo[0], B.hi[0])) visit_leaf(0);
-        } else if (B.n > 1 && __any_sync(0xffffffffu, ia >= 0)) {
+        if (B.n > 0 && __any_sync(0xffffffffu, ia >= 0)) {
             int sp = 0;
             if (lane == 0) stack[0] = 0;
             sp = 1;
@@ -277,16 +323,18 @@ __device__ void ph_traverse(const Params& P) {
             while (sp > 0) {
                 const int node = stack[--sp];
                 __syncwarp();
-                const int2 ch = B.child[node];
+                const float4* nd = B.node + 4LL * node;  // both child boxes: one 64 B line
+                const float4 l0 = nd[0], h0 = nd[1], l1 = nd[2], h1 = nd[3];
+                const bool hit0 = box_hit(qlo, qhi, l0, h0), hit1 = box_hit(qlo, qhi, l1, h1);
+                const unsigned any0 = __ballot_sync(0xffffffffu, hit0), any1 = __ballot_sync(0xffffffffu, hit1);
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
-                    const int cn = k ? ch.y : ch.x;
-                    const bool hit = box_hit(qlo, qhi, B.lo[cn], B.hi[cn]);
-                    if (!__any_sync(0xffffffffu, hit)) continue;
-                    if (cn >= B.n - 1) {
-                        if (hit) visit_leaf(cn);
+                    if (!(k ? any1 : any0)) continue;
+                    const int ref = __float_as_int(k ? l1.w : l0.w);
+                    if (ref < 0) {
+                        if (k ? hit1 : hit0) visit_leaf(~ref);
                     } else if (sp < TRAV_STACK) {
-                        if (lane == 0) stack[sp] = cn;
+                        if (lane == 0) stack[sp] = ref;
                         ++sp;
                     } else if (lane == 0) {
                         atomicOr(&P.g->error, ERR_CAP_STACK);
@@ -299,6 +347,13 @@ __device__ void ph_traverse(const Params& P) {
         if (cnt > P.K) {
             atomicOr(&P.g->error, ERR_CAP_SLOTS);
             atomicMax(&P.g->needed_k, cnt);
+        }
+        // key order of each query's partners: the warp sorts its 32 lists
+        __syncwarp();
+        for (int j = 0; j < 32; ++j) {
+            const int cj = __shfl_sync(0xffffffffu, cnt, j);
+            if (cj < 2 || cj > P.K) continue;
+            sort_partners(P.qslot + (base + j) * P.K, cj, lane);
         }
     }
     const long long ev = block_sum(evals);
@@ -338,30 +393,9 @@ __device__ __forceinline__ bool contact_pred(const Params& P, int ka, int kb, co
     return !(row_jnorm(c) < 1e-28);
 }
 
-// ascending bitonic sort of 64 ints held as (a, b) = elements (lane, lane + 32)
-__device__ __forceinline__ void bitonic64(int& a, int& b, int lane) {
-#pragma unroll
-    for (int k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j == 32) {  // k == 64: partner is the other register of this lane
-                const int lo = min(a, b), hi = max(a, b);
-                a = lo, b = hi;
-                continue;
-            }
-            const int pa = __shfl_xor_sync(0xffffffffu, a, j);
-            const int pb = __shfl_xor_sync(0xffffffffu, b, j);
-            const bool low = (lane & j) == 0;
-            const bool up_a = (lane & k) == 0, up_b = ((lane + 32) & k) == 0;
-            a = (up_a == low) ? min(a, pa) : max(a, pa);
-            b = (up_b == low) ? min(b, pb) : max(b, pb);
-        }
-    }
-}
-
-// A3: prefix the per-query counts, sort each query's partners, evaluate and
-// write the pair records in key order; seed the vertex bound, the contact
-// predicate for the coming linearization, and reset the refit flags.
+// A3: prefix the per-query counts and write the pair keys in key order (the
+// query order is the key order of (ka, kb, ia), the partners of a query are
+// sorted by the traversal); reset the refit flags.
 __device__ void ph_emit_pairs(const Params& P) {
     const long long nq = num_queries(P);
     long long lo, hi;
@@ -374,7 +408,7 @@ __device__ void ph_emit_pairs(const Params& P) {
         }
         return;
     }
-    // pass 1 (this phase): per-query output offsets ...
+    const int lane = threadIdx.x & 31;
     long long base = prefix_of(P.part_q, blockIdx.x);
     for (long long t = lo; t < hi; t += TPB) {
         const long long q = t + threadIdx.x;
@@ -382,39 +416,18 @@ __device__ void ph_emit_pairs(const Params& P) {
         long long tile_tot;
         const long long off = base + block_scan(cnt, &tile_tot);
         base += tile_tot;
-        if (q >= hi) continue;
-        P.qoff[q] = off;
-    }
-    // ... and the key order of each query's partners: one warp per query
-    // (bitonic sort of up to 64 in registers), queries handed out dynamically
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-        long long qb = 0;
-        if (lane == 0) qb = (long long)atomicAdd(&P.g->work_s, 8ull);
-        qb = __shfl_sync(0xffffffffu, qb, 0);
-        if (qb >= nq) break;
-        for (long long q = qb; q < qb + 8 && q < nq; ++q) {
-            const int cnt = P.qcount[q];
-            if (cnt < 2) continue;
-            int* s = P.qslot + q * P.K;
-            if (cnt <= 64) {
-                int a = lane < cnt ? s[lane] : 0x7fffffff;
-                int b = lane + 32 < cnt ? s[lane + 32] : 0x7fffffff;
-                bitonic64(a, b, lane);
-                if (lane < cnt) s[lane] = a;
-                if (lane + 32 < cnt) s[lane + 32] = b;
-            } else if (lane == 0) {
-                for (int i = 1; i < cnt; ++i) {
-                    const int v = s[i];
-                    int j = i - 1;
-                    while (j >= 0 && s[j] > v) s[j + 1] = s[j], --j;
-                    s[j + 1] = v;
-                }
-            }
-            __syncwarp();
+        // the warp writes the keys of its 32 queries, lanes over the partners
+        for (int j = 0; j < 32; ++j) {
+            const int cj = __shfl_sync(0xffffffffu, cnt, j);
+            if (cj == 0) continue;
+            const long long oj = __shfl_sync(0xffffffffu, off, j);
+            const long long qj = __shfl_sync(0xffffffffu, q, j);
+            int ka, ia, kb, cls;
+            query_of(P, qj, &ka, &ia, &kb, &cls);
+            const int* s = P.qslot + qj * P.K;
+            for (int k = lane; k < cj; k += 32) P.pkey[oj + k] = pair_key(ka, ia, kb, s[k]);
         }
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) P.qoff[nq] = total;
     if (blockIdx.x == 0 && threadIdx.x == 0) P.g->np = total;
     // reset refit flags for the next search
     for (int cls = 0; cls < 3; ++cls) {
@@ -424,26 +437,16 @@ __device__ void ph_emit_pairs(const Params& P) {
 }
 
 // A3b: the pair records, balanced over the output: CTA b writes pairs
-// [b P / nb, (b+1) P / nb) — the query of pair p is found by binary search on
-// the query offsets.
+// [b P / nb, (b+1) P / nb), each decoded from its key.
 __device__ void ph_emit_records(const Params& P, bool first_search) {
-    const long long nq = num_queries(P);
     const long long np = P.g->np;
     long long lo, hi;
     chunk_of(np, &lo, &hi);
     long long ncontact = 0;
     int touching = 0;
     for (long long p = lo + threadIdx.x; p < hi; p += TPB) {
-        long long a = 0, b = nq;  // last query with qoff <= p
-        while (b - a > 1) {
-            const long long mid = (a + b) >> 1;
-            if (P.qoff[mid] <= p) a = mid;
-            else b = mid;
-        }
-        const long long q = a;
-        int ka, ia, kb, cls;
-        query_of(P, q, &ka, &ia, &kb, &cls);
-        const int ib = P.qslot[q * P.K + (p - P.qoff[q])];
+        const uint64_t key = P.pkey[p];
+        const int ka = key_ka(key), kb = key_kb(key), ia = key_ia(key), ib = key_ib(key);
         int va[3], vb[3];
         simplex_ids(P, ka, ia, va);
         simplex_ids(P, kb, ib, vb);
@@ -460,7 +463,6 @@ __device__ void ph_emit_records(const Params& P, bool first_search) {
             fl |= PF_CONTACT;
             ++ncontact;
         }
-        P.pkey[p] = pair_key(ka, ia, kb, ib);
         P.pids[p] = ids;
         P.pdd[p] = dd;
         P.pw[p] = w;
