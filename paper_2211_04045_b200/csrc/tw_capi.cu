@@ -68,6 +68,7 @@ struct tw_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk = nullptr;
     // capacities
     long long pcap = 0;
+    long long ccap = 0;  // broad-phase candidate capacity
     int K = 64;
     long long arch_cap = 0;
     int colcap = 1024;
@@ -77,7 +78,7 @@ struct tw_ctx {
     DevMem x, yk1, r, imp, dmin, voff, vcnt, vinc, c_slot, erank, part_v;
     DevMem ly, is_er, er_edge, er_index, er_value, er_g, er_q, edge_lambda, er_color, er_by_color, er_color_off,
         er_color_cnt;
-    DevMem pkey, pids, pdd, pw, pflag, qcount, qslot;
+    DevMem pkey, pids, pdd, pw, pflag, qcount, qslot, cand;
     DevMem c_key, c_ids, c_jac, c_value, c_diag, c_q, c_lambda, c_next, c_color, c_stamp, c_arch, c_lost, c_by_color,
         c_tent, vmask, vbig;
     DevMem ccount, coff;
@@ -182,6 +183,8 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     const long long nq = 2 * pad32(m->niso) + pad32(m->nv) + pad32(m->ne);  // = num_queries
     if (ctx->pcap == 0) ctx->pcap = 8LL * (m->nv + m->ne) + 4096;
     if (ctx->arch_cap < ctx->pcap) ctx->arch_cap = ctx->pcap;
+    if (ctx->ccap == 0) ctx->ccap = 4 * ctx->pcap;
+    CK(ctx->cand.ensure((size_t)ctx->ccap * 8));
     const size_t P = (size_t)ctx->pcap;
     CK(ctx->xs.ensure(nv * 24));
     CK(ctx->ys.ensure(nv * 24));
@@ -311,6 +314,8 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.er_color_cnt = ctx->er_color_cnt.as<int>();
     P.er_ncolors = m->edge_ncolors;
     P.pcap = ctx->pcap;
+    P.ccap = ctx->ccap;
+    P.cand = ctx->cand.as<int2>();
     P.K = ctx->K;
     P.pkey = ctx->pkey.as<uint64_t>();
     P.pids = ctx->pids.as<int4>();
@@ -356,6 +361,7 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.refpool = ctx->refpool.as<int>();
     P.nblocks = ctx->nblocks;
     P.pgs_tail_rows = ctx->pgs_tail_rows;
+    P.experiment = std::getenv("TW_EXPERIMENT") ? std::atoi(std::getenv("TW_EXPERIMENT")) : 0;
     P.part_q = ctx->part_q.as<long long>();
     P.part_c = ctx->part_c.as<long long>();
     P.part_k = ctx->part_k.as<long long>();
@@ -426,12 +432,13 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
                                            std::to_string(G.internal_line) + " (step " +
                                            std::to_string(G.steps) + ")");
         const int cap = G.error & (ERR_CAP_SLOTS | ERR_CAP_PAIRS | ERR_CAP_ARCH | ERR_CAP_COLORS | ERR_CAP_REFPOOL |
-                                   ERR_CAP_STACK);
+                                   ERR_CAP_STACK | ERR_CAP_CAND);
         if (!cap) break;
         if (++retries > 12) return fail(ctx, TW_ECAPACITY, "resolve: capacity growth did not converge");
         if (G.error & ERR_CAP_STACK) return fail(ctx, TW_ECAPACITY, "resolve: BVH traversal stack overflow");
         if (G.error & ERR_CAP_SLOTS) ctx->K = std::max(ctx->K * 2, ((G.needed_k + 31) / 32) * 32);
         if (G.error & ERR_CAP_PAIRS) grow_ll(ctx->pcap, G.needed_pairs + G.needed_pairs / 4);
+        if (G.error & ERR_CAP_CAND) grow_ll(ctx->ccap, (long long)G.ncand + (long long)G.ncand / 4);
         if (G.error & ERR_CAP_ARCH) grow_ll(ctx->arch_cap, ctx->arch_cap * 2);
         if (G.error & ERR_CAP_COLORS) ctx->colcap *= 4;
         if (G.error & ERR_CAP_REFPOOL) ctx->refpool_cap *= 4;
@@ -566,7 +573,7 @@ void tw_ctx_destroy(tw_ctx* ctx) {
                      &ctx->vcnt, &ctx->ly, &ctx->is_er, &ctx->er_edge, &ctx->er_index, &ctx->er_value, &ctx->er_g,
                      &ctx->er_q, &ctx->edge_lambda, &ctx->er_color, &ctx->er_by_color, &ctx->er_color_off,
                      &ctx->er_color_cnt, &ctx->pkey, &ctx->pids, &ctx->pdd, &ctx->pw, &ctx->pflag, &ctx->qcount,
-                     &ctx->qslot, &ctx->c_key, &ctx->c_ids, &ctx->c_jac, &ctx->c_value, &ctx->c_diag, &ctx->c_q,
+                     &ctx->qslot, &ctx->cand, &ctx->c_key, &ctx->c_ids, &ctx->c_jac, &ctx->c_value, &ctx->c_diag, &ctx->c_q,
                      &ctx->c_lambda, &ctx->c_next, &ctx->c_color, &ctx->c_stamp, &ctx->c_tent, &ctx->c_arch,
                      &ctx->c_lost, &ctx->vmask, &ctx->vbig,
                      &ctx->c_by_color, &ctx->ccount, &ctx->coff, &ctx->arch_key0, &ctx->arch_key1,
@@ -880,10 +887,11 @@ int tw_stage_search(tw_ctx* ctx, tw_mesh* m, const double* x, double d_max, int6
         CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof G, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         if (G.error & ERR_TIMEOUT) return fail(ctx, TW_ETIMEOUT, "search: watchdog");
-        if (!(G.error & (ERR_CAP_SLOTS | ERR_CAP_PAIRS))) break;
+        if (!(G.error & (ERR_CAP_SLOTS | ERR_CAP_PAIRS | ERR_CAP_CAND))) break;
         if (attempt > 10) return fail(ctx, TW_ECAPACITY, "search: capacity");
         if (G.error & ERR_CAP_SLOTS) ctx->K = std::max(ctx->K * 2, ((G.needed_k + 31) / 32) * 32);
         if (G.error & ERR_CAP_PAIRS) grow_ll(ctx->pcap, G.needed_pairs + G.needed_pairs / 4);
+        if (G.error & ERR_CAP_CAND) grow_ll(ctx->ccap, (long long)G.ncand + (long long)G.ncand / 4);
     }
     *np = G.np;
     if (G.np > cap) return fail(ctx, TW_ECAPACITY, "search: output capacity too small");

@@ -32,6 +32,7 @@ enum : int {
     ERR_TIMEOUT = 32,     // grid barrier watchdog fired
     ERR_CAP_STACK = 64,   // BVH traversal stack overflow
     ERR_INTERNAL = 128,   // invariant violated (line in Globals::internal_line)
+    ERR_CAP_CAND = 256,   // broad-phase candidate buffer full (count in Globals::ncand)
 };
 
 enum : uint8_t { PF_ACTIVE = 1, PF_ALL_STATIC = 2, PF_DEGENERATE = 4, PF_CONTACT = 8 };
@@ -58,6 +59,8 @@ struct Globals {
     int nonfinite;
     int internal_line;
     unsigned long long work_q;  // dynamic query counter of the traversal (reset by the refit)
+    unsigned long long ncand;   // broad-phase candidates of the current search (reset by the refit)
+    unsigned long long work_s;  // dynamic query counter of the partner sort (reset by the refit)
     int ner;             // edge rows of this call (set by the prologue)
     int needed_k;
     long long np;        // pairs in the set
@@ -149,6 +152,8 @@ struct Params {
     uint8_t* pflag;
     int* qcount;
     int* qslot;     // nq * K
+    long long ccap;
+    int2* cand;     // broad-phase candidates (query, partner index)
     // ---- contact rows
     uint64_t* c_key;
     int4* c_ids;
@@ -191,6 +196,7 @@ struct Params {
     // PGS colors with at most this many rows at the end of the color order run
     // on one CTA (ph_pgs_tail); 0 disables
     long long pgs_tail_rows;
+    int experiment;  // TW_EXPERIMENT (profiling experiments only; 0 in production)
     // per block scratch
     int nblocks;
     long long* part_q;

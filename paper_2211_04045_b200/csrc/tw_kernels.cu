@@ -299,6 +299,8 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
             SYNC();
             ph_traverse(P);
             SYNC();
+            ph_cand_eval(P);
+            SYNC();
             ph_query_totals(P);
             SYNC();
             ph_emit_pairs(P);
@@ -458,6 +460,8 @@ __global__ void __launch_bounds__(TPB, 4) k_stage_search(Params P) {
     ph_refit(P);
     if (!grid_sync(P.g)) return;
     ph_traverse(P);
+    if (!grid_sync(P.g)) return;
+    ph_cand_eval(P);
     if (!grid_sync(P.g)) return;
     ph_query_totals(P);
     if (!grid_sync(P.g)) return;

@@ -136,7 +136,7 @@ __device__ __forceinline__ int prim_to_index(const Params& P, int cls, int prim)
 // parent's box). Every finished box is written into its slot of the parent's
 // packed node (Bvh::node).
 __device__ void ph_refit(const Params& P) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) P.g->work_q = 0ull;  // traversal query counter
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.g->work_q = 0ull, P.g->work_s = 0ull, P.g->ncand = 0ull;
     for (int cls = 0; cls < 3; ++cls) {
         const Bvh& B = P.bvh[cls];
         if (B.n == 0) continue;
@@ -263,20 +263,21 @@ __device__ __forceinline__ void sort_partners(int* s, int n, int lane) {
     __syncwarp();
 }
 
-// A2: traverse every query and record the surviving partners. A warp takes 32
-// consecutive queries (spatially coherent: consecutive vertices / edges of
-// the mesh) from a global counter and walks the hierarchy as a packet: one
-// shared DFS stack, a node is descended when any lane's query box overlaps
-// it (ballot), so the walk itself never diverges; at a leaf only the lanes
-// whose box overlaps run the exact FP64 test. The per-block totals for the
-// order-preserving prefix are summed afterwards (ph_query_totals).
-constexpr int TRAV_STACK = 64;
+// A2: broad phase. A warp takes 32 consecutive queries (spatially coherent:
+// consecutive vertices / edges of the mesh) from a global counter and walks
+// the hierarchy as a packet: one shared DFS stack, a node is descended when
+// any lane's query box overlaps it (ballot), so the walk never diverges. A
+// leaf hit by a lane's box (and canonical for the query: EE and VV keep
+// a < b, proximity.cpp:125-140) becomes a (query, partner) candidate, queued
+// per warp and written out 32 at a time. The walk holds no FP64 state, which
+// keeps it light on registers; the exact tests run in ph_cand_eval.
+constexpr int TRAV_STACK = 128;
 __device__ void ph_traverse(const Params& P) {
     __shared__ int sstack[TPB / 32][TRAV_STACK];
+    __shared__ int2 cq[TPB / 32][64];
     const long long nq = num_queries(P);
-    long long evals = 0;
-    const double infl = P.cfg.d_max * (1.0 + 1e-6) + 1e-12;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
     int* stack = sstack[warp];
     for (;;) {
         long long base = 0;
@@ -287,10 +288,10 @@ __device__ void ph_traverse(const Params& P) {
         int ka, ia, kb, cls;
         query_of(P, q, &ka, &ia, &kb, &cls);  // ka, kb, cls are warp-uniform
         const Bvh& B = P.bvh[cls];
-        int cnt = 0;
-        int va[3] = {-1, -1, -1};
+        P.qcount[q] = 0;
         float4 qlo = make_float4(1.f, 1.f, 1.f, 0.f), qhi = make_float4(0.f, 0.f, 0.f, 0.f);  // empty box
         if (ia >= 0) {
+            int va[3];
             simplex_ids(P, ka, ia, va);
             double lo3[3], hi3[3];
             const d3 p0 = ld3(P.x, va[0]);
@@ -301,19 +302,38 @@ __device__ void ph_traverse(const Params& P) {
                 lo3[1] = fmin(lo3[1], p1.y), hi3[1] = fmax(hi3[1], p1.y);
                 lo3[2] = fmin(lo3[2], p1.z), hi3[2] = fmax(hi3[2], p1.z);
             }
-            qlo = make_float4(__double2float_rd(lo3[0] - infl), __double2float_rd(lo3[1] - infl),
-                              __double2float_rd(lo3[2] - infl), 0.f);
-            qhi = make_float4(__double2float_ru(hi3[0] + infl), __double2float_ru(hi3[1] + infl),
-                              __double2float_ru(hi3[2] + infl), 0.f);
+            // float box of the query inflated by d_max, rounded outwards
+            const double dinfl = P.cfg.d_max * (1.0 + 1e-6) + 1e-12;
+            qlo = make_float4(__double2float_rd(lo3[0] - dinfl), __double2float_rd(lo3[1] - dinfl),
+                              __double2float_rd(lo3[2] - dinfl), 0.f);
+            qhi = make_float4(__double2float_ru(hi3[0] + dinfl), __double2float_ru(hi3[1] + dinfl),
+                              __double2float_ru(hi3[2] + dinfl), 0.f);
         }
-        int* slots = P.qslot + q * P.K;
-        auto visit_leaf = [&](int ib) {
-            Closest c;
-            ++evals;
-            if (candidate_keep(P, ka, ia, va, kb, ib, c)) {
-                if (cnt < P.K) slots[cnt] = ib;
-                ++cnt;
+        // canonical partners only: EE (a = lower edge index) and VV (a < b)
+        const bool ordered = (ka == KE) || (ka == KV && kb == KV);
+        int qn = 0;  // queued candidates (warp-uniform)
+        auto flush = [&](bool all) {
+            while (qn >= 32 || (all && qn > 0)) {
+                const int take = min(qn, 32);
+                unsigned long long gb = 0;
+                if (lane == 0) gb = atomicAdd(&P.g->ncand, (unsigned long long)take);
+                gb = __shfl_sync(0xffffffffu, gb, 0);
+                if (lane < take && (long long)(gb + lane) < P.ccap) {
+                    const int2 e = cq[warp][qn - take + lane];
+                    P.cand[gb + lane] = make_int2((int)(base + e.x), e.y);
+                }
+                if (lane == 0 && (long long)(gb + take) > P.ccap) atomicOr(&P.g->error, ERR_CAP_CAND);
+                qn -= take;
+                __syncwarp();
             }
+        };
+        auto leaf = [&](bool hit, int ib) {
+            const bool take = hit && !(ordered && ib <= ia);
+            const unsigned m = __ballot_sync(0xffffffffu, take);
+            if (take) cq[warp][qn + __popc(m & lt)] = make_int2(lane, ib);
+            qn += __popc(m);
+            __syncwarp();
+            if (qn >= 32) flush(false);
         };
         if (B.n > 0 && __any_sync(0xffffffffu, ia >= 0)) {
             int sp = 0;
@@ -326,13 +346,14 @@ __device__ void ph_traverse(const Params& P) {
                 const float4* nd = B.node + 4LL * node;  // both child boxes: one 64 B line
                 const float4 l0 = nd[0], h0 = nd[1], l1 = nd[2], h1 = nd[3];
                 const bool hit0 = box_hit(qlo, qhi, l0, h0), hit1 = box_hit(qlo, qhi, l1, h1);
-                const unsigned any0 = __ballot_sync(0xffffffffu, hit0), any1 = __ballot_sync(0xffffffffu, hit1);
+                const bool any0 = __any_sync(0xffffffffu, hit0), any1 = __any_sync(0xffffffffu, hit1);
+                const int r0 = __float_as_int(l0.w), r1 = __float_as_int(l1.w);
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     if (!(k ? any1 : any0)) continue;
-                    const int ref = __float_as_int(k ? l1.w : l0.w);
+                    const int ref = k ? r1 : r0;
                     if (ref < 0) {
-                        if (k ? hit1 : hit0) visit_leaf(~ref);
+                        leaf(k ? hit1 : hit0, ~ref);
                     } else if (sp < TRAV_STACK) {
                         if (lane == 0) stack[sp] = ref;
                         ++sp;
@@ -342,34 +363,62 @@ __device__ void ph_traverse(const Params& P) {
                 }
                 __syncwarp();
             }
+            flush(true);
         }
-        P.qcount[q] = cnt;
-        if (cnt > P.K) {
-            atomicOr(&P.g->error, ERR_CAP_SLOTS);
-            atomicMax(&P.g->needed_k, cnt);
-        }
-        // key order of each query's partners: the warp sorts its 32 lists
-        __syncwarp();
-        for (int j = 0; j < 32; ++j) {
-            const int cj = __shfl_sync(0xffffffffu, cnt, j);
-            if (cj < 2 || cj > P.K) continue;
-            sort_partners(P.qslot + (base + j) * P.K, cj, lane);
+    }
+}
+
+// A2b: the exact narrow-phase test of every candidate (all lanes busy);
+// survivors are appended to their query's partner list.
+__device__ void ph_cand_eval(const Params& P) {
+    const long long n = min((long long)P.g->ncand, P.ccap);
+    long long evals = 0;
+    for (long long i = gtid(); i < n; i += gstride()) {
+        const int2 e = P.cand[i];
+        int ka, ia, kb, cls;
+        query_of(P, e.x, &ka, &ia, &kb, &cls);
+        int va[3];
+        simplex_ids(P, ka, ia, va);
+        Closest c;
+        ++evals;
+        if (candidate_keep(P, ka, ia, va, kb, e.y, c)) {
+            const int pos = atomicAdd(&P.qcount[e.x], 1);
+            if (pos < P.K) {
+                P.qslot[(long long)e.x * P.K + pos] = e.y;
+            } else {
+                atomicOr(&P.g->error, ERR_CAP_SLOTS);
+                atomicMax(&P.g->needed_k, pos + 1);
+            }
         }
     }
     const long long ev = block_sum(evals);
     if (threadIdx.x == 0) atomicAdd((unsigned long long*)&P.g->pairs_evaluated, (unsigned long long)ev);
 }
 
-// A2b: per-block totals of the query counts over the block's chunk (the
-// chunking ph_emit_pairs uses)
+// A2c: per-block totals of the query counts over the block's chunk (the
+// chunking ph_emit_pairs uses), and the key order of each query's partners
+// (one warp per query, queries handed out dynamically)
 __device__ void ph_query_totals(const Params& P) {
     const long long nq = num_queries(P);
     long long lo, hi;
     chunk_of(nq, &lo, &hi);
     long long s = 0;
-    for (long long q = lo + threadIdx.x; q < hi; q += TPB) s += P.qcount[q];
+    for (long long q = lo + threadIdx.x; q < hi; q += TPB) s += min(P.qcount[q], P.K);
     const long long tot = block_sum(s);
     if (threadIdx.x == 0) P.part_q[blockIdx.x] = tot;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        long long qb = 0;
+        if (lane == 0) qb = (long long)atomicAdd(&P.g->work_s, 32ull);
+        qb = __shfl_sync(0xffffffffu, qb, 0);
+        if (qb >= nq) break;
+        const int cnt = P.qcount[qb + lane];
+        for (int j = 0; j < 32; ++j) {
+            const int cj = __shfl_sync(0xffffffffu, cnt, j);
+            if (cj < 2 || cj > P.K) continue;
+            sort_partners(P.qslot + (qb + j) * P.K, cj, lane);
+        }
+    }
 }
 
 __device__ __forceinline__ void vertex_min(const Params& P, int v, double d) {
@@ -412,7 +461,7 @@ __device__ void ph_emit_pairs(const Params& P) {
     long long base = prefix_of(P.part_q, blockIdx.x);
     for (long long t = lo; t < hi; t += TPB) {
         const long long q = t + threadIdx.x;
-        const int cnt = q < hi ? P.qcount[q] : 0;
+        const int cnt = q < hi ? min(P.qcount[q], P.K) : 0;
         long long tile_tot;
         const long long off = base + block_scan(cnt, &tile_tot);
         base += tile_tot;

@@ -1,0 +1,19 @@
+"""Phase profile of one bow-knot resolve for experiments (TW_EXPERIMENT=1
+skips the exact candidate test: traversal walk cost only; results invalid)."""
+import os
+import sys
+
+sys.path.insert(0, os.getcwd())
+from paper_2211_04045_b200 import capi, scenes as S
+
+sc = S.bow_knot()
+ctx = capi.Context(0)
+m = capi.Mesh.from_scene(ctx, sc)
+for i in range(3):
+    x, st = capi.resolve(ctx, m, sc.x, sc.y, delta=5e-4)
+prof = capi.phase_profile(ctx)
+print(f"experiment={os.environ.get('TW_EXPERIMENT', '0')} kernel_ms {st['kernel_ms']:.3f} "
+      f"steps {st['steps']} searches {st['searches']}")
+for k in ("ph_refit", "ph_traverse", "ph_emit_pairs", "ph_emit_records"):
+    if k in prof:
+        print(f"  {k}: {prof[k][0] / prof[k][1]:.3f} ms per call ({prof[k][1]} calls)")
