@@ -80,7 +80,7 @@ struct tw_ctx {
         er_color_cnt;
     DevMem pkey, pids, pdd, pw, pflag, qcount, qslot, cand;
     DevMem c_key, c_ids, c_jac, c_value, c_diag, c_q, c_lambda, c_next, c_color, c_stamp, c_arch, c_lost, c_by_color,
-        c_tent, vmask, vbig;
+        c_tent, vmask, vbig, pk_ids, pk_jac, pk_q, pk_diag, pk_lam;
     DevMem ccount, coff;
     DevMem arch_key0, arch_key1, arch_val0, arch_val1, new_lb, new_key, new_val;
     DevMem refpool;
@@ -232,6 +232,13 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     CK(ctx->c_lost.ensure(P * 4));
     CK(ctx->vmask.ensure(nv * 32));
     CK(ctx->vbig.ensure(nv * 4));
+    if (cfg.solver == TW_SOLVER_PGS) {
+        CK(ctx->pk_ids.ensure(P * 16));
+        CK(ctx->pk_jac.ensure(P * 96));
+        CK(ctx->pk_q.ensure(P * 8));
+        CK(ctx->pk_diag.ensure(P * 8));
+        CK(ctx->pk_lam.ensure(P * 8));
+    }
     CK(ctx->c_by_color.ensure(P * 4));
     CK(ctx->ccount.ensure((size_t)ctx->colcap * 4));
     CK(ctx->coff.ensure(((size_t)ctx->colcap + 1) * 4));
@@ -339,6 +346,11 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.c_lost = ctx->c_lost.as<int>();
     P.vmask = ctx->vmask.as<unsigned long long>();
     P.vbig = ctx->vbig.as<int>();
+    P.pk_ids = ctx->pk_ids.as<int4>();
+    P.pk_jac = ctx->pk_jac.as<double>();
+    P.pk_q = ctx->pk_q.as<double>();
+    P.pk_diag = ctx->pk_diag.as<double>();
+    P.pk_lam = ctx->pk_lam.as<double>();
     P.c_by_color = ctx->c_by_color.as<int>();
     P.voff = ctx->voff.as<int>();
     P.vinc = ctx->vinc.as<int>();
@@ -575,7 +587,7 @@ void tw_ctx_destroy(tw_ctx* ctx) {
                      &ctx->er_color_cnt, &ctx->pkey, &ctx->pids, &ctx->pdd, &ctx->pw, &ctx->pflag, &ctx->qcount,
                      &ctx->qslot, &ctx->cand, &ctx->c_key, &ctx->c_ids, &ctx->c_jac, &ctx->c_value, &ctx->c_diag, &ctx->c_q,
                      &ctx->c_lambda, &ctx->c_next, &ctx->c_color, &ctx->c_stamp, &ctx->c_tent, &ctx->c_arch,
-                     &ctx->c_lost, &ctx->vmask, &ctx->vbig,
+                     &ctx->c_lost, &ctx->vmask, &ctx->vbig, &ctx->pk_ids, &ctx->pk_jac, &ctx->pk_q, &ctx->pk_diag, &ctx->pk_lam,
                      &ctx->c_by_color, &ctx->ccount, &ctx->coff, &ctx->arch_key0, &ctx->arch_key1,
                      &ctx->arch_val0, &ctx->arch_val1, &ctx->new_lb, &ctx->new_key, &ctx->new_val, &ctx->refpool,
                      &ctx->part_q, &ctx->part_c, &ctx->part_k, &ctx->blk_lo, &ctx->blk_hi, &ctx->globals, &ctx->box,

@@ -169,6 +169,13 @@ struct Params {
     long long* c_arch;  // archive index, or -(lower_bound)-1
     int* c_lost;        // coloring: round in which the row's proposal lost
     int* c_by_color;
+    // contact rows copied into color-bucket order for the PGS (position in
+    // c_by_color): one coalesced read per row instead of an indirection
+    int4* pk_ids;
+    double* pk_jac;   // 12 per position
+    double* pk_q;
+    double* pk_diag;
+    double* pk_lam;
     // coloring: per-vertex mask of the colors < 256 taken around the vertex
     // (edge rows + contact rows colored so far), and a flag for colors >= 256
     unsigned long long* vmask;  // 4 per vertex

@@ -762,7 +762,7 @@ __device__ void ph_warm(const Params& P, long long nc) {
                 }
             }
         }
-        P.imp[v] = make_double4(a.x, a.y, a.z, 0.0);
+        P.imp[v] = make_double4(a.x, a.y, a.z, im);  // w: inv_mass, read with the impulse by the PGS
         if (P.cfg.coloring_mode == 1) {
             // device coloring: the vertex starts with the colors of its edge rows
             unsigned long long mk4[4] = {0, 0, 0, 0};
@@ -1199,10 +1199,22 @@ __device__ void ph_bucket_scatter(const Params& P, long long nc, int ncol, bool 
 
 __device__ void ph_bucket_place(const Params& P, long long nc, bool edges_too) {
     // counting down leaves the count tables zeroed for the next step
+    const bool pack = P.cfg.solver == 0;
     for (long long i = gtid(); i < nc; i += gstride()) {
         const int c = P.c_color[i];
         const int slot = atomicSub(&P.ccount[c], 1) - 1;
-        P.c_by_color[P.coff[c] + slot] = (int)i;
+        const long long pos = P.coff[c] + slot;
+        P.c_by_color[pos] = (int)i;
+        if (pack) {
+            P.pk_ids[pos] = P.c_ids[i];
+            const double2* s = reinterpret_cast<const double2*>(P.c_jac + i * 12);
+            double2* d = reinterpret_cast<double2*>(P.pk_jac + pos * 12);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) d[k] = s[k];
+            P.pk_q[pos] = P.c_q[i];
+            P.pk_diag[pos] = P.c_diag[i];
+            P.pk_lam[pos] = P.c_lambda[i];
+        }
     }
     if (edges_too)
         for (long long k = gtid(); k < P.g->ner; k += gstride()) {
@@ -1247,6 +1259,46 @@ __device__ __forceinline__ void pgs_contact_row(const Params& P, int i) {
         }
     }
     P.c_lambda[i] = lam;
+}
+
+// The same row from its color-ordered copy (position pos of c_by_color):
+// static row data is one coalesced read, each dynamic vertex's impulse (with
+// its inverse mass in w) is gathered once and written back once.
+__device__ __forceinline__ void pgs_contact_packed(const Params& P, long long pos) {
+    const int4 id = P.pk_ids[pos];
+    const int vv[4] = {id.x, id.y, id.z, id.w};
+    const double2* J2 = reinterpret_cast<const double2*>(P.pk_jac + pos * 12);
+    double J[12];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const double2 t = J2[k];
+        J[2 * k] = t.x, J[2 * k + 1] = t.y;
+    }
+    double4 a[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) a[m] = vv[m] >= 0 ? P.imp[vv[m]] : make_double4(0, 0, 0, 0);
+    double s = 0.0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+        if (a[m].w > 0.0) s += dot(mk(J[3 * m], J[3 * m + 1], J[3 * m + 2]), mk(a[m].x, a[m].y, a[m].z));
+    const double w = P.pk_q[pos] + s;
+    const double lam0 = P.pk_lam[pos];
+    const double t = lam0 - w / P.pk_diag[pos];
+    const double lam = 0.0 < t ? t : 0.0;
+    const double d = lam - lam0;
+    if (d != 0.0) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            if (!(a[m].w > 0.0)) continue;
+            const double sc = a[m].w * d;
+            a[m].x = a[m].x + sc * J[3 * m];
+            a[m].y = a[m].y + sc * J[3 * m + 1];
+            a[m].z = a[m].z + sc * J[3 * m + 2];
+            P.imp[vv[m]] = a[m];
+        }
+    }
+    P.pk_lam[pos] = lam;
+    P.c_lambda[P.c_by_color[pos]] = lam;
 }
 
 __device__ __forceinline__ void pgs_edge_row(const Params& P, int e) {
@@ -1301,7 +1353,7 @@ __device__ void ph_pgs_color(const Params& P, int c, int ncol_contact, int ncol_
     long long c0, nci, e0, n;
     pgs_color_range(P, c, ncol_contact, ncol_edge, &c0, &nci, &e0, &n);
     for (long long k = gtid(); k < n; k += gstride()) {
-        if (k < nci) pgs_contact_row(P, P.c_by_color[c0 + k]);
+        if (k < nci) pgs_contact_packed(P, c0 + k);
         else pgs_edge_row(P, P.er_by_color[e0 + (k - nci)]);
     }
 }
@@ -1329,7 +1381,7 @@ __device__ void ph_pgs_tail(const Params& P, int cfirst, int ncol, int ncol_cont
         long long c0, nci, e0, n;
         pgs_color_range(P, c, ncol_contact, ncol_edge, &c0, &nci, &e0, &n);
         for (long long k = threadIdx.x; k < n; k += TPB) {
-            if (k < nci) pgs_contact_row(P, P.c_by_color[c0 + k]);
+            if (k < nci) pgs_contact_packed(P, c0 + k);
             else pgs_edge_row(P, P.er_by_color[e0 + (k - nci)]);
         }
         __syncthreads();

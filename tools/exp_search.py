@@ -14,6 +14,5 @@ for i in range(3):
 prof = capi.phase_profile(ctx)
 print(f"experiment={os.environ.get('TW_EXPERIMENT', '0')} kernel_ms {st['kernel_ms']:.3f} "
       f"steps {st['steps']} searches {st['searches']}")
-for k in ("ph_refit", "ph_traverse", "ph_emit_pairs", "ph_emit_records"):
-    if k in prof:
-        print(f"  {k}: {prof[k][0] / prof[k][1]:.3f} ms per call ({prof[k][1]} calls)")
+for k, (ms, n) in prof.items():
+    print(f"  {k:20s} {ms:7.3f} ms total, {ms / n:.4f} ms per call ({n} calls)")
