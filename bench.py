@@ -253,6 +253,10 @@ def run_ours(args):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = algo_bytes / (kern_avg_ms / 1e3) / 1e9
+    # DRAM bytes per k_resolve launch from the committed ncu --set full capture
+    # of the same resolve (tools/gpu_measure.sh -> tools/make_profiles.py)
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic = json.load(open(tpath)) if os.path.exists(tpath) else None
     out = None
     if rank == 0:
         out = {
@@ -274,7 +278,9 @@ def run_ours(args):
                     "d2h_bytes_per_step": sc.nv * 24 + 160},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4),
+                         "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                         "traffic_source": traffic["source"] if traffic else "no ncu capture committed",
                          "kernel": "tw::k_resolve (persistent cooperative Alg.-1 kernel)",
                          "algorithmic_bytes_per_launch": algo_bytes,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},

@@ -12,10 +12,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 echo "launches rc=$?"
 timeout 300 python tools/prof_drive.py > gpurun_out/plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_resolve -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_resolve -c 1 \
     -o gpurun_out/prof_resolve -f python tools/prof_drive.py > gpurun_out/ncu_full.log 2>&1
 echo "ncu resolve rc=$?"; tail -2 gpurun_out/ncu_full.log
 timeout 300 python tools/prof_search.py > gpurun_out/plain2.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stage -s 1 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_stage -c 2 \
     -o gpurun_out/prof_search -f python tools/prof_search.py > gpurun_out/ncu_search.log 2>&1
 echo "ncu search rc=$?"; tail -2 gpurun_out/ncu_search.log
