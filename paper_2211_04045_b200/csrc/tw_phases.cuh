@@ -83,6 +83,21 @@ __device__ __forceinline__ long long block_sum(long long v) {
     return t;
 }
 
+// max over the CTA (every thread gets it)
+__device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v) {
+    __shared__ unsigned long long wm[TPB / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane == 0) wm[warp] = v;
+    __syncthreads();
+    unsigned long long m = wm[0];
+#pragma unroll
+    for (int w = 1; w < TPB / 32; ++w) m = max(m, wm[w]);
+    return m;
+}
+
 // sum of part[0..upto) (every thread gets it)
 __device__ __forceinline__ long long prefix_of(const long long* part, int upto) {
     long long s = 0;
@@ -595,13 +610,22 @@ __device__ void ph_rows(const Params& P, int sel, long long narch) {
     long long base = prefix_of(P.part_c, blockIdx.x);
     const uint64_t* akey = P.arch_key[sel];
     const double* aval = P.arch_val[sel];
-    for (long long t = lo; t < hi; t += TPB) {
-        const long long p = t + threadIdx.x;
-        const int flag = (p < hi && (P.pflag[p] & PF_CONTACT)) ? 1 : 0;
+    // each thread scans 16 consecutive pairs per tile (one block scan per
+    // 4096 pairs), then builds the rows of its contact pairs in pair order
+    constexpr int PER = 16;
+    for (long long t = lo; t < hi; t += (long long)TPB * PER) {
+        const long long p0 = t + (long long)threadIdx.x * PER;
+        unsigned fm = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (p0 + j < hi && (P.pflag[p0 + j] & PF_CONTACT)) fm |= 1u << j;
         long long tile_tot;
-        const long long pos = base + block_scan(flag, &tile_tot);
+        long long pos = base + block_scan(__popc(fm), &tile_tot) - 1;
         base += tile_tot;
-        if (!flag) continue;
+        while (fm) {
+        const long long p = p0 + (__ffs(fm) - 1);
+        fm &= fm - 1;
+        ++pos;
         const uint64_t key = P.pkey[p];
         const int ka = key_ka(key), kb = key_kb(key);
         int va[3], vb[3];
@@ -645,6 +669,7 @@ __device__ void ph_rows(const Params& P, int sel, long long narch) {
             const int e = (int)(pos * 4 + m);
             if (m < c.nverts && P.inv_mass[c.v[m]] > 0.0) record_incidence(P, c.v[m], e);
             else P.c_slot[e] = -1;
+        }
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) P.g->nc = nc_total;
@@ -1467,6 +1492,9 @@ __device__ void ph_jacobi_commit(const Params& P, long long nc) {
 // store (resolve.cpp:106-111); resets per-vertex scratch for the next step.
 __device__ void ph_advance(const Params& P, double bound, int step, long long nc, int sel) {
     const double half_gamma = 0.5 * P.cfg.gamma;
+    // maxima as bit patterns of non-negative doubles (NaN skipped), reduced
+    // per CTA before the one atomic per CTA
+    unsigned long long md_bits = 0ull, rs_bits = 0ull;
     for (long long v = gtid(); v < P.nv; v += gstride()) {
         const double4 x4 = P.x[v];
         const unsigned long long db = P.dmin[v];
@@ -1500,15 +1528,21 @@ __device__ void ph_advance(const Params& P, double bound, int step, long long nc
                 P.r[v] = P.r[v] * (1.0 - alpha);
                 // std::max(max_disp, |disp|) ignores a NaN operand (advance.cpp:37)
                 const double nd = nrm(disp);
-                if (!isnan(nd)) atomicMax(&P.g->maxdisp_bits, to_b(nd));
+                if (!isnan(nd)) md_bits = max(md_bits, to_b(nd));
             }
         }
-        if (!isnan(P.r[v])) atomicMax(&P.g->resid_bits, to_b(P.r[v]));  // max_remainder, advance.hpp:21-25
+        if (!isnan(P.r[v])) rs_bits = max(rs_bits, to_b(P.r[v]));  // max_remainder, advance.hpp:21-25
         if (P.cfg.record_path) {
             const double4 xn = P.x[v];
             double* o = P.path + ((long long)(step + 1) * P.nv + v) * 3;
             o[0] = xn.x, o[1] = xn.y, o[2] = xn.z;
         }
+    }
+    md_bits = block_max_u64(md_bits);
+    rs_bits = block_max_u64(rs_bits);
+    if (threadIdx.x == 0) {
+        if (md_bits) atomicMax(&P.g->maxdisp_bits, md_bits);
+        if (rs_bits) atomicMax(&P.g->resid_bits, rs_bits);
     }
     // contact multipliers -> archive (update in place; count new keys)
     long long lo, hi;
