@@ -761,46 +761,142 @@ __device__ __forceinline__ void imp_add(d3& a, double s, d3 j) {
 // B3: warm-start impulse M^-1 J^T lambda accumulated per vertex in row order
 // (lcp.cpp:16-23: contact rows in pair order, then edge rows in edge order)
 // and the coloring priorities of the contact rows
+// edge-row part of the warm start at v (after its contact rows, lcp.cpp:16-23)
+__device__ __forceinline__ void warm_edges(const Params& P, int v, double im, d3& a) {
+    if (!P.cfg.edge_constraints) return;
+    for (int k = P.vedge_off[v]; k < P.vedge_off[v + 1]; ++k) {
+        const int e = P.vedge[k];
+        if (!P.is_er[e]) continue;
+        const double lam = P.edge_lambda[e];
+        if (lam != 0.0) imp_add(a, im * lam, edge_jac(P.er_g[e], P.edges[e].x == v ? 0 : 1));
+    }
+}
+
+// Segments longer than this are sorted by a warp (rank by counting in shared
+// memory); shorter ones by their vertex's thread.
+constexpr int WARM_SHORT = 32, WARM_WARP_MAX = 256;
+
 __device__ void ph_warm(const Params& P, long long nc) {
-    for (long long v = gtid(); v < P.nv; v += gstride()) {
-        const double im = P.inv_mass[v];
-        d3 a = mk(0, 0, 0);
-        if (im > 0.0) {
+    __shared__ int longv[TPB];
+    __shared__ int nlong;
+    __shared__ int sseg[TPB / 32][WARM_WARP_MAX];
+    if (threadIdx.x == 0) nlong = 0;
+    __syncthreads();
+    long long lo, hi;
+    chunk_of(P.nv, &lo, &hi);
+    for (long long base = lo; base < hi; base += TPB) {
+        const long long v = base + threadIdx.x;
+        if (v < hi) {
+            const double im = P.inv_mass[v];
             const int b = P.voff[v], n = P.voff[v + 1] - b;
-            sort_segment(P.vinc + b, n);
-            // entry rank inside the vertex clique (round-1 coloring proposal)
-            for (int k = 0; k < n; ++k) P.erank[P.vinc[b + k]] = k;
-            for_sorted_entries(P, (int)v, [&](int e) {
-                const int row = e >> 2, m = e & 3;
-                const double lam = P.c_lambda[row];
-                if (lam != 0.0) {
-                    const double* J = P.c_jac + (long long)row * 12 + 3 * m;
-                    imp_add(a, im * lam, mk(J[0], J[1], J[2]));
+            if (im > 0.0 && n > WARM_SHORT) {
+                longv[atomicAdd(&nlong, 1)] = (int)v;  // sorted + summed by a warp below
+            } else {
+                d3 a = mk(0, 0, 0);
+                if (im > 0.0) {
+                    sort_segment(P.vinc + b, n);
+                    // entry rank inside the vertex clique (round-1 coloring proposal)
+                    for (int k = 0; k < n; ++k) P.erank[P.vinc[b + k]] = k;
+                    for_sorted_entries(P, (int)v, [&](int e) {
+                        const int row = e >> 2, m = e & 3;
+                        const double lam = P.c_lambda[row];
+                        if (lam != 0.0) {
+                            const double* J = P.c_jac + (long long)row * 12 + 3 * m;
+                            imp_add(a, im * lam, mk(J[0], J[1], J[2]));
+                        }
+                    });
+                    warm_edges(P, (int)v, im, a);
                 }
-            });
-            if (P.cfg.edge_constraints) {
-                for (int k = P.vedge_off[v]; k < P.vedge_off[v + 1]; ++k) {
-                    const int e = P.vedge[k];
-                    if (!P.is_er[e]) continue;
-                    const double lam = P.edge_lambda[e];
-                    if (lam != 0.0) imp_add(a, im * lam, edge_jac(P.er_g[e], P.edges[e].x == v ? 0 : 1));
-                }
+                P.imp[v] = make_double4(a.x, a.y, a.z, im);  // w: inv_mass, read with the impulse by the PGS
+            }
+            if (P.cfg.coloring_mode == 1) {
+                // device coloring: the vertex starts with the colors of its edge rows
+                unsigned long long mk4[4] = {0, 0, 0, 0};
+                int big = 0;
+                if (im > 0.0 && P.cfg.edge_constraints)
+                    for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
+                        const int ec = P.edge_color[P.vedge[q]];
+                        if (ec >= 256) big = 1;
+                        else if (ec >= 0) mk4[ec >> 6] |= 1ull << (ec & 63);
+                    }
+                for (int w = 0; w < 4; ++w) P.vmask[4 * v + w] = mk4[w];
+                P.vbig[v] = big;
             }
         }
-        P.imp[v] = make_double4(a.x, a.y, a.z, im);  // w: inv_mass, read with the impulse by the PGS
-        if (P.cfg.coloring_mode == 1) {
-            // device coloring: the vertex starts with the colors of its edge rows
-            unsigned long long mk4[4] = {0, 0, 0, 0};
-            int big = 0;
-            if (im > 0.0 && P.cfg.edge_constraints)
-                for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
-                    const int ec = P.edge_color[P.vedge[q]];
-                    if (ec >= 256) big = 1;
-                    else if (ec >= 0) mk4[ec >> 6] |= 1ull << (ec & 63);
+        __syncthreads();
+        // long segments: one warp per vertex
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int j = w; j < nlong; j += TPB / 32) {
+            const int vv = longv[j];
+            const double im = P.inv_mass[vv];
+            const int b = P.voff[vv], n = P.voff[vv + 1] - b;
+            int* seg = P.vinc + b;
+            if (n <= WARM_WARP_MAX) {
+                for (int i = lane; i < n; i += 32) sseg[w][i] = seg[i];
+                __syncwarp();
+                int rk[WARM_WARP_MAX / 32], ev[WARM_WARP_MAX / 32];
+#pragma unroll
+                for (int r = 0; r < WARM_WARP_MAX / 32; ++r) {
+                    const int i = lane + 32 * r;
+                    rk[r] = -1;
+                    if (i < n) {
+                        const int e = sseg[w][i];
+                        int c = 0;
+                        for (int t = 0; t < n; ++t) c += sseg[w][t] < e;
+                        rk[r] = c, ev[r] = e;
+                    }
                 }
-            for (int w = 0; w < 4; ++w) P.vmask[4 * v + w] = mk4[w];
-            P.vbig[v] = big;
+                __syncwarp();
+#pragma unroll
+                for (int r = 0; r < WARM_WARP_MAX / 32; ++r)
+                    if (rk[r] >= 0) {
+                        sseg[w][rk[r]] = ev[r];
+                        seg[rk[r]] = ev[r];
+                        P.erank[ev[r]] = rk[r];
+                    }
+                __syncwarp();
+            } else {
+                if (lane == 0) {
+                    sort_segment(seg, n);
+                    for (int k = 0; k < n; ++k) P.erank[seg[k]] = k;
+                }
+                __syncwarp();
+            }
+            // ordered sum of the contact terms: lanes form the terms, lane 0 adds them in row order
+            d3 a = mk(0, 0, 0);
+            for (int k0 = 0; k0 < n; k0 += 32) {
+                const int k = k0 + lane;
+                bool nz = false;
+                d3 t = mk(0, 0, 0);
+                if (k < n) {
+                    const int e = n <= WARM_WARP_MAX ? sseg[w][k] : seg[k];
+                    const int row = e >> 2, m = e & 3;
+                    const double lam = P.c_lambda[row];
+                    if (lam != 0.0) {
+                        const double* J = P.c_jac + (long long)row * 12 + 3 * m;
+                        const double sc = im * lam;
+                        t = mk(sc * J[0], sc * J[1], sc * J[2]);
+                        nz = true;
+                    }
+                }
+                const unsigned nzm = __ballot_sync(0xffffffffu, nz);
+                for (int q = 0; q < 32; ++q) {
+                    if (!((nzm >> q) & 1u)) continue;
+                    const double tx = __shfl_sync(0xffffffffu, t.x, q);
+                    const double ty = __shfl_sync(0xffffffffu, t.y, q);
+                    const double tz = __shfl_sync(0xffffffffu, t.z, q);
+                    a.x = a.x + tx, a.y = a.y + ty, a.z = a.z + tz;
+                }
+            }
+            if (lane == 0) {
+                warm_edges(P, vv, im, a);
+                P.imp[vv] = make_double4(a.x, a.y, a.z, im);
+            }
+            __syncwarp();
         }
+        __syncthreads();
+        if (threadIdx.x == 0) nlong = 0;
+        __syncthreads();
     }
     for (long long i = gtid(); i < nc; i += gstride()) {
         P.c_stamp[i] = 0;
