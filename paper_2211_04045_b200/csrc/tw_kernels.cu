@@ -418,8 +418,12 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
         // before a re-search only its multiplier erasures matter.
         const bool final_step = residual < C.eps || l + 1 == C.step_limit;
         if (P.trace || (!final_step && !next_search)) {
-            ph_refresh(P, bound, next_search, true, sel, narch);
+            ph_refresh(P, bound, next_search);
             SYNC();
+            if (narch > 0) {
+                ph_arch_erase(P, sel, narch);
+                SYNC();
+            }
         } else if (!final_step && narch > 0) {
             ph_refresh_archive(P, bound, sel, narch);
             SYNC();
@@ -472,7 +476,7 @@ __global__ void __launch_bounds__(TPB, 4) k_stage_search(Params P) {
 
 // refresh + per-vertex bound into P.r (min(bound, dmin))
 __global__ void __launch_bounds__(TPB, 4) k_stage_refresh(Params P, double bound) {
-    ph_refresh(P, bound, false, false, 0, 0);
+    ph_refresh(P, bound, false);
     if (!grid_sync(P.g)) return;
     for (long long v = gtid(); v < P.nv; v += gstride()) P.r[v] = mind(bound, to_d(P.dmin[v]));
 }

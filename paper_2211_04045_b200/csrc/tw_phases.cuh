@@ -355,6 +355,14 @@ __device__ void ph_traverse(const Params& P) {
             if (lane == 0) stack[0] = 0;
             sp = 1;
             __syncwarp();
+            auto push = [&](int ref) {
+                if (sp < TRAV_STACK) {
+                    if (lane == 0) stack[sp] = ref;
+                    ++sp;
+                } else if (lane == 0) {
+                    atomicOr(&P.g->error, ERR_CAP_STACK);
+                }
+            };
             while (sp > 0) {
                 const int node = stack[--sp];
                 __syncwarp();
@@ -367,14 +375,8 @@ __device__ void ph_traverse(const Params& P) {
                 for (int k = 0; k < 2; ++k) {
                     if (!(k ? any1 : any0)) continue;
                     const int ref = k ? r1 : r0;
-                    if (ref < 0) {
-                        leaf(k ? hit1 : hit0, ~ref);
-                    } else if (sp < TRAV_STACK) {
-                        if (lane == 0) stack[sp] = ref;
-                        ++sp;
-                    } else if (lane == 0) {
-                        atomicOr(&P.g->error, ERR_CAP_STACK);
-                    }
+                    if (ref < 0) leaf(k ? hit1 : hit0, ~ref);
+                    else push(ref);
                 }
                 __syncwarp();
             }
@@ -1696,11 +1698,10 @@ __device__ void ph_arch_merge(const Params& P, long long nnew, int sel, long lon
 
 // ============================================================ refresh (H)
 // refresh_distances (proximity.cpp:190-202) with the pre-shrink bound, the
-// inactive-pair erase (resolve.cpp:122-123), the vertex bound of the next
-// step (proximity.cpp:204-211) and, when no search follows, the contact
-// predicate of the next linearization.
-__device__ void ph_refresh(const Params& P, double bound, bool next_search, bool erase, int sel,
-                           long long narch) {
+// vertex bound of the next step (proximity.cpp:204-211) and, when no search
+// follows, the contact predicate of the next linearization. The erase of
+// the multipliers of inactive pairs runs from the archive side (ph_arch_erase).
+__device__ void ph_refresh(const Params& P, double bound, bool next_search) {
     const long long np = P.g->np;
     long long lo, hi;
     chunk_of(np, &lo, &hi);
@@ -1739,10 +1740,6 @@ __device__ void ph_refresh(const Params& P, double bound, bool next_search, bool
                 for (int k = 0; k <= ka; ++k) vertex_min(P, va[k], dd.w);
                 for (int k = 0; k <= kb; ++k) vertex_min(P, vb[k], dd.w);
             }
-        } else if (erase && narch > 0) {
-            const long long at = arch_lower_bound(P.arch_key[sel], narch, key);
-            if (at < narch && P.arch_key[sel][at] == key)
-                P.arch_val[sel][at] = __longlong_as_double(0x7ff8000000000000ll);
         }
         if (!next_search && contact_pred(P, ka, kb, va, vb, dd, w, fl)) {
             fl |= PF_CONTACT;
@@ -1758,6 +1755,23 @@ __device__ void ph_refresh(const Params& P, double bound, bool next_search, bool
         P.blk_hi[blockIdx.x] = hi;
         atomicAdd(&P.g->nactive, (int)na);
         atomicAdd((unsigned long long*)&P.g->pairs_evaluated, (unsigned long long)(hi - lo));
+    }
+}
+
+// H2: the erase loop of resolve.cpp:122-123 (multipliers of pairs that left
+// the active set are dropped), walked from the archive side: each live entry
+// looks its key up in the (sorted) pair set and is tombstoned when that pair
+// is inactive. Keys not in the set are kept, as in the reference.
+__device__ void ph_arch_erase(const Params& P, int sel, long long narch) {
+    const long long np = P.g->np;
+    const uint64_t* akey = P.arch_key[sel];
+    double* aval = P.arch_val[sel];
+    for (long long a = gtid(); a < narch; a += gstride()) {
+        if (isnan(aval[a])) continue;
+        const uint64_t key = akey[a];
+        const long long p = arch_lower_bound(P.pkey, np, key);
+        if (p < np && P.pkey[p] == key && !(P.pflag[p] & PF_ACTIVE))
+            aval[a] = __longlong_as_double(0x7ff8000000000000ll);
     }
 }
 
