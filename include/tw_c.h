@@ -125,6 +125,7 @@ int tw_mesh_create(tw_ctx* ctx, int32_t nv, const double* inv_mass, int32_t ne_e
                    const int32_t* triangles, tw_mesh** out);
 int32_t tw_mesh_num_edges(const tw_mesh* mesh);
 int tw_mesh_edges(const tw_mesh* mesh, int32_t* out_edges /* 2 * ne */);
+/* A mesh and its context may be destroyed in either order. */
 void tw_mesh_destroy(tw_mesh* mesh);
 
 /* resolve(x_start, y_target, mesh, cfg) — resolve.cpp:36-144. Host buffers.

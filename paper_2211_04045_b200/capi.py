@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 
@@ -96,6 +97,11 @@ def lib():
         L.tw_stage_search.argtypes = [P, P, P, C.c_double, C.c_int64, P, P, P, P, P, P, P]
         L.tw_stage_refresh.argtypes = [P, P, P, C.c_double, C.c_int64, P, P, P, P, P, P, P]
         L.tw_stage_advance.argtypes = [P, C.c_int32, P, P, P, C.c_double, P, P, P]
+        L.tw_stage_linearize.argtypes = [P, P, P, C.c_int64, P, P, P, P, P, P, P, C.c_double, C.c_double,
+                                         C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P, P, P]
+        L.tw_stage_color.argtypes = [P, P, C.c_int64, P, P, P, P, C.c_uint64, C.c_int32, C.c_int32, P, P]
+        L.tw_stage_backward.argtypes = [P, C.c_int32, P, C.c_int64, P, P, P, P, P, C.c_int32, P, P, C.c_int32,
+                                        C.c_int32, C.c_double, P, P, P]
         _LIB = L
     return _LIB
 
@@ -127,6 +133,7 @@ class Context:
 
     def __init__(self, device: int = 0, stream: int | None = None):
         self.h = C.c_void_p()
+        self._meshes = weakref.WeakSet()  # meshes are destroyed before their context
         rc = lib().tw_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(self.h))
         if rc != TW_OK:
             raise TwError(rc, "tw_ctx_create failed (no CUDA device?)")
@@ -141,6 +148,8 @@ class Context:
 
     def close(self):
         if self.h:
+            for m in list(self._meshes):
+                m.close()
             lib().tw_ctx_destroy(self.h)
             self.h = C.c_void_p()
 
@@ -166,6 +175,7 @@ class Mesh:
         self.h = C.c_void_p()
         ctx.check(lib().tw_mesh_create(ctx.h, self.nv, _p(im), len(e), _p(e), len(s), _p(s), len(t), _p(t),
                                        C.byref(self.h)))
+        ctx._meshes.add(self)
         ne = lib().tw_mesh_num_edges(self.h)
         self.edges = np.zeros((ne, 2), np.int32)
         lib().tw_mesh_edges(self.h, _p(self.edges))
@@ -316,3 +326,78 @@ def advance(ctx: Context, inv_mass, y, D, gamma, x, r):
                                      _p(np.ascontiguousarray(y, np.float64)), _p(np.ascontiguousarray(D, np.float64)),
                                      gamma, _p(x), _p(r), C.byref(md)))
     return x, r, md.value
+
+
+class Rows:
+    """Constraint rows as tw_stage_linearize returns them (contact rows in pair
+    order, then edge rows in edge order): kind (0 VT, 1 EE, 2 VE, 3 VV, 4 edge),
+    verts (R, 4; -1 padded), value, jac (R, 4, 3), diag, pair_key, edge_index."""
+
+    def __init__(self, n):
+        self.kind = np.zeros(n, np.uint8)
+        self.verts = np.full((n, 4), -1, np.int32)
+        self.value = np.zeros(n)
+        self.jac = np.zeros((n, 4, 3))
+        self.diag = np.zeros(n)
+        self.pair_key = np.zeros(n, np.uint64)
+        self.edge_index = np.full(n, -1, np.int32)
+
+    def __len__(self):
+        return len(self.kind)
+
+    def take(self, n):
+        r = Rows(0)
+        for k in ("kind", "verts", "value", "jac", "diag", "pair_key", "edge_index"):
+            setattr(r, k, getattr(self, k)[:n].copy())
+        return r
+
+
+def linearize(ctx: Context, mesh: Mesh, x, pairs: Pairs, edge_targets, delta=1e-3, sigma=1.1, family=0,
+              edge_constraints=True) -> Rows:
+    """linearize_all (constraints.cpp:181-220) on the device."""
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    et = np.ascontiguousarray(edge_targets if edge_targets is not None else np.zeros(1), np.float64)
+    family = FAMILIES[family] if isinstance(family, str) else family
+    cap = len(pairs) + len(mesh.edges) + 16
+    R = Rows(cap)
+    n = C.c_int64(0)
+    ctx.check(lib().tw_stage_linearize(ctx.h, mesh.h, _p(x), len(pairs), _p(pairs.keys), _p(pairs.dist),
+                                       _p(pairs.wa), _p(pairs.wb), _p(pairs.dir), _p(pairs.flags), _p(et), delta,
+                                       sigma, family, int(bool(edge_constraints)), cap, _p(R.kind), _p(R.verts),
+                                       _p(R.value), _p(R.jac), _p(R.diag), _p(R.pair_key), _p(R.edge_index),
+                                       C.byref(n)))
+    return R.take(n.value)
+
+
+def color(ctx: Context, mesh: Mesh, rows: Rows, seed=0x5EED, mode="device", edge_constraints=True):
+    """color_constraints on the device; returns (ncolors, color per row)."""
+    mode = COLORINGS[mode] if isinstance(mode, str) else mode
+    out = np.zeros(len(rows), np.int32)
+    nco = C.c_int32(0)
+    ctx.check(lib().tw_stage_color(ctx.h, mesh.h, len(rows), _p(np.ascontiguousarray(rows.kind, np.uint8)),
+                                   _p(np.ascontiguousarray(rows.verts, np.int32)),
+                                   _p(np.ascontiguousarray(rows.pair_key, np.uint64)),
+                                   _p(np.ascontiguousarray(rows.edge_index, np.int32)), seed, mode,
+                                   int(bool(edge_constraints)), _p(out), C.byref(nco)))
+    return nco.value, out
+
+
+def backward(ctx: Context, inv_mass, rows: Rows, colors, ncolors, x, y, lam=None, solver="pgs", sweeps=1,
+             under_relax=0.5):
+    """assemble_lcp + sweeps + recover_target on the device; returns dict
+    (lambda, q, y) like the oracle's backward."""
+    inv = np.ascontiguousarray(inv_mass, np.float64)
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    y = np.ascontiguousarray(y, np.float64).reshape(-1, 3)
+    n = len(rows)
+    lam = np.zeros(n) if lam is None else np.ascontiguousarray(lam, np.float64).copy()
+    q = np.zeros(max(1, n))
+    yo = np.zeros_like(x)
+    solver = SOLVERS[solver] if isinstance(solver, str) else solver
+    col = np.ascontiguousarray(colors if colors is not None else np.zeros(n), np.int32)
+    ctx.check(lib().tw_stage_backward(ctx.h, len(inv), _p(inv), n, _p(np.ascontiguousarray(rows.verts, np.int32)),
+                                      _p(np.ascontiguousarray(rows.value, np.float64)),
+                                      _p(np.ascontiguousarray(rows.jac, np.float64)),
+                                      _p(np.ascontiguousarray(rows.diag, np.float64)), _p(col), int(ncolors),
+                                      _p(x), _p(y), solver, sweeps, under_relax, _p(lam), _p(q), _p(yo)))
+    return {"lambda": lam, "q": q[:n], "y": yo}

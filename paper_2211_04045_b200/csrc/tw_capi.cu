@@ -96,6 +96,7 @@ struct tw_ctx {
 
 struct tw_mesh {
     tw_ctx* ctx = nullptr;
+    int device = 0;  // destroy does not touch the context (either may be destroyed first)
     int nv = 0, ne = 0, nt = 0, niso = 0;
     std::vector<int32_t> edges;  // 2 ne, finalized order
     std::vector<double> inv_mass;
@@ -612,6 +613,7 @@ int tw_mesh_create(tw_ctx* ctx, int32_t nv, const double* inv_mass, int32_t ne_e
     CK(cudaSetDevice(ctx->device));
     tw_mesh* m = new tw_mesh();
     m->ctx = ctx;
+    m->device = ctx->device;
     m->nv = nv;
     m->nt = nt;
     m->inv_mass.assign(nv, 1.0);
@@ -743,8 +745,8 @@ int tw_mesh_edges(const tw_mesh* m, int32_t* out) {
 
 void tw_mesh_destroy(tw_mesh* m) {
     if (!m) return;
-    cudaSetDevice(m->ctx->device);
-    cudaStreamSynchronize(m->ctx->stream);
+    cudaSetDevice(m->device);
+    cudaDeviceSynchronize();
     DevMem* all[] = {&m->d_inv_mass, &m->d_edges, &m->d_tris, &m->d_iso, &m->d_vedge_off, &m->d_vedge, &m->d_edge_color};
     for (DevMem* d : all) d->release();
     for (auto& B : m->bvh) {
@@ -845,6 +847,56 @@ int stage_upload_x(tw_ctx* ctx, tw_mesh* m, const double* x) {
     return TW_OK;
 }
 
+// pair records in the layout the search writes (ids from the key, VT triangle
+// ids from the device triangle table)
+int stage_upload_pairs(tw_ctx* ctx, tw_mesh* m, int64_t np, const uint64_t* keys, const double* dist,
+                       const double* wa, const double* wb, const double* dir, const uint8_t* flags) {
+    // pack the pair records as the search writes them
+    std::vector<int4> ids(np);
+    std::vector<double4> dd(np), w(np);
+    for (int64_t i = 0; i < np; ++i) {
+        const uint64_t k = keys[i];
+        const int ka = (int)(k >> 62), kb = (int)((k >> 60) & 3), ia = (int)((k >> 30) & 0x3fffffff),
+                  ib = (int)(k & 0x3fffffff);
+        int va[3] = {-1, -1, -1}, vb[3] = {-1, -1, -1};
+        auto ids_of = [&](int kind, int idx, int* v) {
+            if (kind == 0) v[0] = idx;
+            else if (kind == 1) v[0] = m->edges[2 * idx], v[1] = m->edges[2 * idx + 1];
+            else v[0] = v[1] = v[2] = -1;  // triangle ids: filled from the device table below
+        };
+        ids_of(ka, ia, va);
+        ids_of(kb, ib, vb);
+        ids[i] = ka == 1 ? make_int4(va[0], va[1], vb[0], vb[1]) : make_int4(va[0], vb[0], vb[1], vb[2]);
+        dd[i] = make_double4(dir[3 * i], dir[3 * i + 1], dir[3 * i + 2], dist[i]);
+        if (ka == 1) w[i] = make_double4(wa[3 * i], wa[3 * i + 1], wb[3 * i], wb[3 * i + 1]);
+        else w[i] = make_double4(wb[3 * i], wb[3 * i + 1], wb[3 * i + 2], 0.0);
+    }
+    cudaStream_t s = ctx->stream;
+    if (np) {
+        CK(cudaMemcpyAsync(ctx->pkey.p, keys, np * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->pids.p, ids.data(), np * 16, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->pdd.p, dd.data(), np * 32, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->pw.p, w.data(), np * 32, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->pflag.p, flags, np, cudaMemcpyHostToDevice, s));
+    }
+    // triangle ids for VT pairs come from the device triangle table
+    std::vector<int4> tris(m->nt);
+    if (m->nt) CK(cudaMemcpyAsync(tris.data(), m->d_tris.p, (size_t)m->nt * 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    bool fix = false;
+    for (int64_t i = 0; i < np; ++i) {
+        const uint64_t k = keys[i];
+        if (((k >> 60) & 3) == 2) {
+            const int4 t = tris[k & 0x3fffffff];
+            ids[i] = make_int4((int)((k >> 30) & 0x3fffffff), t.x, t.y, t.z);
+            fix = true;
+        }
+    }
+    if (fix && np) CK(cudaMemcpyAsync(ctx->pids.p, ids.data(), np * 16, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    return TW_OK;
+}
+
 int stage_download_pairs(tw_ctx* ctx, int64_t np, uint64_t* keys, double* dist, double* wa, double* wb, double* dir,
                          uint8_t* flags) {
     std::vector<int4> ids(np);
@@ -922,51 +974,9 @@ int tw_stage_refresh(tw_ctx* ctx, tw_mesh* m, const double* x, double bound, int
     if (rc) return rc;
     rc = stage_upload_x(ctx, m, x);
     if (rc) return rc;
-    // pack the pair records as the search writes them
-    std::vector<int4> ids(np);
-    std::vector<double4> dd(np), w(np);
-    for (int64_t i = 0; i < np; ++i) {
-        const uint64_t k = keys[i];
-        const int ka = (int)(k >> 62), kb = (int)((k >> 60) & 3), ia = (int)((k >> 30) & 0x3fffffff),
-                  ib = (int)(k & 0x3fffffff);
-        int va[3] = {-1, -1, -1}, vb[3] = {-1, -1, -1};
-        auto ids_of = [&](int kind, int idx, int* v) {
-            if (kind == 0) v[0] = idx;
-            else if (kind == 1) v[0] = m->edges[2 * idx], v[1] = m->edges[2 * idx + 1];
-            else {
-                // triangles are only on device; keep a host copy via the tris upload? use edges path
-                v[0] = v[1] = v[2] = -1;
-            }
-        };
-        ids_of(ka, ia, va);
-        ids_of(kb, ib, vb);
-        ids[i] = ka == 1 ? make_int4(va[0], va[1], vb[0], vb[1]) : make_int4(va[0], vb[0], vb[1], vb[2]);
-        dd[i] = make_double4(dir[3 * i], dir[3 * i + 1], dir[3 * i + 2], dist[i]);
-        if (ka == 1) w[i] = make_double4(wa[3 * i], wa[3 * i + 1], wb[3 * i], wb[3 * i + 1]);
-        else w[i] = make_double4(wb[3 * i], wb[3 * i + 1], wb[3 * i + 2], 0.0);
-    }
+    rc = stage_upload_pairs(ctx, m, np, keys, dist, wa, wb, dir, flags);
+    if (rc) return rc;
     cudaStream_t s = ctx->stream;
-    if (np) {
-        CK(cudaMemcpyAsync(ctx->pkey.p, keys, np * 8, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(ctx->pids.p, ids.data(), np * 16, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(ctx->pdd.p, dd.data(), np * 32, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(ctx->pw.p, w.data(), np * 32, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(ctx->pflag.p, flags, np, cudaMemcpyHostToDevice, s));
-    }
-    // triangle ids for VT pairs come from the device triangle table
-    std::vector<int4> tris(m->nt);
-    if (m->nt) CK(cudaMemcpyAsync(tris.data(), m->d_tris.p, (size_t)m->nt * 16, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    bool fix = false;
-    for (int64_t i = 0; i < np; ++i) {
-        const uint64_t k = keys[i];
-        if (((k >> 60) & 3) == 2) {
-            const int4 t = tris[k & 0x3fffffff];
-            ids[i] = make_int4((int)((k >> 30) & 0x3fffffff), t.x, t.y, t.z);
-            fix = true;
-        }
-    }
-    if (fix && np) CK(cudaMemcpyAsync(ctx->pids.p, ids.data(), np * 16, cudaMemcpyHostToDevice, s));
     Params P = make_params(ctx, m, cfg);
     CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), s));
     CK(cudaMemsetAsync(ctx->dmin.p, 0x7f, (size_t)m->nv * 8, s));
@@ -1046,21 +1056,257 @@ int tw_stage_advance(tw_ctx* ctx, int32_t nv, const double* inv_mass, const doub
     return TW_OK;
 }
 
-int tw_stage_linearize(tw_ctx* ctx, tw_mesh*, const double*, int64_t, const uint64_t*, const double*, const double*,
-                       const double*, const double*, const uint8_t*, const double*, double, double, int32_t, int32_t,
-                       int64_t, uint8_t*, int32_t*, double*, double*, double*, uint64_t*, int32_t*, int64_t*) {
-    return fail(ctx, TW_EUNSUPPORTED, "tw_stage_linearize: not yet wired");
+int tw_stage_linearize(tw_ctx* ctx, tw_mesh* m, const double* x, int64_t np, const uint64_t* keys,
+                       const double* dist, const double* wa, const double* wb, const double* dir,
+                       const uint8_t* flags, const double* edge_targets, double delta, double sigma, int32_t family,
+                       int32_t edge_constraints, int64_t cap, uint8_t* kind, int32_t* verts, double* value,
+                       double* jac, double* diag, uint64_t* pair_key, int32_t* edge_index, int64_t* nrows) {
+    if (!ctx || !m || !x || np < 0 || (np && (!keys || !dist || !wa || !wb || !dir || !flags)) || !nrows ||
+        (m->ne && edge_constraints && !edge_targets) || !(delta > 0.0) || (family != 0 && family != 1))
+        return fail(ctx, TW_EINVAL, "linearize: bad argument");
+    CK(cudaSetDevice(ctx->device));
+    tw_resolve_config cfg;
+    tw_default_config(&cfg);
+    cfg.step_limit = 1;
+    cfg.delta = delta;
+    cfg.sigma = sigma;
+    cfg.family = family;
+    cfg.edge_constraints = edge_constraints ? 1 : 0;
+    if (ctx->pcap < np) grow_ll(ctx->pcap, np);
+    int rc = ensure_buffers(ctx, m, cfg);
+    if (rc) return rc;
+    rc = stage_upload_x(ctx, m, x);
+    if (rc) return rc;
+    rc = stage_upload_pairs(ctx, m, np, keys, dist, wa, wb, dir, flags);
+    if (rc) return rc;
+    cudaStream_t s = ctx->stream;
+    const int ne = m->ne;
+    // frozen edge targets and the edge-row set (constraints.cpp:152-153)
+    std::vector<double> ly(std::max(1, ne), 0.0);
+    std::vector<uint8_t> is_er(std::max(1, ne), 0);
+    for (int e = 0; e < ne && edge_constraints; ++e) {
+        ly[e] = edge_targets[e];
+        const int i = m->edges[2 * e], j = m->edges[2 * e + 1];
+        is_er[e] = (ly[e] > 1e-12 && !(m->inv_mass[i] == 0.0 && m->inv_mass[j] == 0.0)) ? 1 : 0;
+    }
+    if (ne) {
+        CK(cudaMemcpyAsync(ctx->ly.p, ly.data(), (size_t)ne * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->is_er.p, is_er.data(), (size_t)ne, cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaMemcpyAsync(ctx->yk1.p, ctx->x.p, (size_t)m->nv * 32, cudaMemcpyDeviceToDevice, s));  // q unused
+    CK(cudaMemsetAsync(ctx->vcnt.p, 0, (size_t)std::max(1, m->nv) * 4, s));
+    CK(cudaMemsetAsync(ctx->er_color_cnt.p, 0, (size_t)ctx->colcap * 4, s));
+    Params P = make_params(ctx, m, cfg);
+    P.cfg.coloring_mode = 0;  // no device-mode edge buckets in the prologue
+    Globals G;
+    std::memset(&G, 0, sizeof G);
+    G.np = np;
+    CK(cudaMemcpyAsync(ctx->globals.p, &G, sizeof G, cudaMemcpyHostToDevice, s));
+    CK(coop_stage_linearize(s, P, ctx->nblocks));
+    ++ctx->launches;
+    CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof G, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (G.error) return fail(ctx, TW_ETIMEOUT, "linearize: device error");
+    const long long nc = G.nc, ner = G.ner, R = nc + ner;
+    *nrows = R;
+    if (R > cap) return fail(ctx, TW_ECAPACITY, "linearize: output capacity too small");
+    std::vector<uint64_t> ck(nc);
+    std::vector<int4> cid(nc);
+    std::vector<double> cval(nc), cjac(nc * 12), cdiag(nc), erv(std::max(1, ne));
+    std::vector<double4> erg(std::max(1, ne));
+    std::vector<int> ere(std::max(1LL, ner));
+    if (nc) {
+        CK(cudaMemcpyAsync(ck.data(), ctx->c_key.p, nc * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(cid.data(), ctx->c_ids.p, nc * 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(cval.data(), ctx->c_value.p, nc * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(cjac.data(), ctx->c_jac.p, nc * 96, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(cdiag.data(), ctx->c_diag.p, nc * 8, cudaMemcpyDeviceToHost, s));
+    }
+    if (ner) {
+        CK(cudaMemcpyAsync(ere.data(), ctx->er_edge.p, ner * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(erv.data(), ctx->er_value.p, (size_t)ne * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(erg.data(), ctx->er_g.p, (size_t)ne * 32, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    static const uint8_t row_kind[3][3] = {{3, 2, 0}, {255, 1, 255}, {255, 255, 255}};  // [ka][kb]: VV VE VT / EE
+    for (long long i = 0; i < nc; ++i) {
+        kind[i] = row_kind[ck[i] >> 62][(ck[i] >> 60) & 3];
+        verts[4 * i] = cid[i].x, verts[4 * i + 1] = cid[i].y, verts[4 * i + 2] = cid[i].z, verts[4 * i + 3] = cid[i].w;
+        value[i] = cval[i];
+        for (int k = 0; k < 12; ++k) jac[12 * i + k] = cjac[12 * i + k];
+        diag[i] = cdiag[i];
+        pair_key[i] = ck[i];
+        edge_index[i] = -1;
+    }
+    for (long long k = 0; k < ner; ++k) {
+        const long long i = nc + k;
+        const int e = ere[k];
+        const double4 g = erg[e];
+        const bool zero = g.x == 0.0 && g.y == 0.0 && g.z == 0.0;  // edge length <= 1e-12: zero rows
+        kind[i] = 4;
+        verts[4 * i] = m->edges[2 * e], verts[4 * i + 1] = m->edges[2 * e + 1];
+        verts[4 * i + 2] = verts[4 * i + 3] = -1;
+        value[i] = erv[e];
+        const double j0[3] = {zero ? g.x : -g.x, zero ? g.y : -g.y, zero ? g.z : -g.z};
+        const double j1[3] = {g.x, g.y, g.z};
+        for (int c = 0; c < 3; ++c) jac[12 * i + c] = j0[c], jac[12 * i + 3 + c] = j1[c];
+        for (int c = 6; c < 12; ++c) jac[12 * i + c] = 0.0;
+        diag[i] = g.w;
+        pair_key[i] = 0;
+        edge_index[i] = e;
+    }
+    return TW_OK;
 }
 
-int tw_stage_color(tw_ctx* ctx, tw_mesh*, int64_t, const uint8_t*, const int32_t*, const uint64_t*, const int32_t*,
-                   uint64_t, int32_t, int32_t, int32_t*, int32_t*) {
-    return fail(ctx, TW_EUNSUPPORTED, "tw_stage_color: not yet wired");
+int tw_stage_color(tw_ctx* ctx, tw_mesh* m, int64_t nrows, const uint8_t* kind, const int32_t* verts,
+                   const uint64_t* pair_key, const int32_t* edge_index, uint64_t seed, int32_t mode,
+                   int32_t edge_constraints, int32_t* color, int32_t* ncolors) {
+    if (!ctx || !m || nrows < 0 || (nrows && (!kind || !verts || !edge_index || !color)) || !ncolors ||
+        (mode != TW_COLOR_REFERENCE && mode != TW_COLOR_DEVICE))
+        return fail(ctx, TW_EINVAL, "color: bad argument");
+    long long nc = 0;
+    while (nc < nrows && kind[nc] != 4) ++nc;
+    for (long long i = nc; i < nrows; ++i)
+        if (kind[i] != 4 || edge_index[i] < 0 || edge_index[i] >= m->ne)
+            return fail(ctx, TW_EINVAL, "color: contact rows must precede the edge rows");
+    CK(cudaSetDevice(ctx->device));
+    tw_resolve_config cfg;
+    tw_default_config(&cfg);
+    cfg.step_limit = 1;
+    cfg.coloring_mode = mode;
+    cfg.color_seed = seed;
+    cfg.edge_constraints = edge_constraints ? 1 : 0;
+    if (ctx->pcap < nc) grow_ll(ctx->pcap, nc);
+    cudaStream_t s = ctx->stream;
+    const int ne = m->ne;
+    std::vector<int4> ids(std::max(1LL, nc));
+    std::vector<uint64_t> keys(std::max(1LL, nc), 0);
+    for (long long i = 0; i < nc; ++i) {
+        ids[i] = make_int4(verts[4 * i], verts[4 * i + 1], verts[4 * i + 2], verts[4 * i + 3]);
+        if (pair_key) keys[i] = pair_key[i];
+    }
+    std::vector<uint8_t> is_er(std::max(1, ne), 0);
+    for (long long i = nc; i < nrows; ++i) is_er[edge_index[i]] = 1;
+    Globals G;
+    for (int attempt = 0;; ++attempt) {
+        int rc = ensure_buffers(ctx, m, cfg);
+        if (rc) return rc;
+        if (nc) {
+            CK(cudaMemcpyAsync(ctx->c_ids.p, ids.data(), nc * 16, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(ctx->c_key.p, keys.data(), nc * 8, cudaMemcpyHostToDevice, s));
+            CK(cudaMemsetAsync(ctx->c_lambda.p, 0, nc * 8, s));
+        }
+        if (ne) {
+            CK(cudaMemcpyAsync(ctx->is_er.p, is_er.data(), (size_t)ne, cudaMemcpyHostToDevice, s));
+            CK(cudaMemsetAsync(ctx->edge_lambda.p, 0, (size_t)ne * 8, s));
+            CK(cudaMemcpyAsync(ctx->er_color.p, m->d_edge_color.p, (size_t)ne * 4, cudaMemcpyDeviceToDevice, s));
+        }
+        CK(cudaMemsetAsync(ctx->vcnt.p, 0, (size_t)std::max(1, m->nv) * 4, s));
+        CK(cudaMemsetAsync(ctx->ccount.p, 0, (size_t)ctx->colcap * 4, s));
+        CK(cudaMemsetAsync(ctx->er_color_cnt.p, 0, (size_t)ctx->colcap * 4, s));
+        std::memset(&G, 0, sizeof G);
+        G.max_color = -1;  // no contact row colored yet
+        CK(cudaMemcpyAsync(ctx->globals.p, &G, sizeof G, cudaMemcpyHostToDevice, s));
+        Params P = make_params(ctx, m, cfg);
+        CK(coop_stage_color(s, P, ctx->nblocks, nc));
+        ++ctx->launches;
+        CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof G, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int capbits = G.error & (ERR_CAP_COLORS | ERR_CAP_REFPOOL);
+        if (G.error & ~(ERR_CAP_COLORS | ERR_CAP_REFPOOL)) return fail(ctx, TW_ETIMEOUT, "color: device error");
+        if (!capbits) break;
+        if (attempt > 8) return fail(ctx, TW_ECAPACITY, "color: capacity growth did not converge");
+        if (G.error & ERR_CAP_COLORS) ctx->colcap *= 4;
+        if (G.error & ERR_CAP_REFPOOL) ctx->refpool_cap *= 4;
+    }
+    std::vector<int> cc(std::max(1LL, nc)), ec(std::max(1, ne));
+    if (nc) CK(cudaMemcpyAsync(cc.data(), ctx->c_color.p, nc * 4, cudaMemcpyDeviceToHost, s));
+    if (ne) CK(cudaMemcpyAsync(ec.data(), ctx->er_color.p, (size_t)ne * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int nco = G.max_color + 1;
+    for (long long i = 0; i < nc; ++i) color[i] = cc[i];
+    for (long long i = nc; i < nrows; ++i) {
+        color[i] = ec[edge_index[i]];
+        nco = std::max(nco, color[i] + 1);
+    }
+    *ncolors = nco;
+    return TW_OK;
 }
 
-int tw_stage_backward(tw_ctx* ctx, int32_t, const double*, int64_t, const int32_t*, const double*, const double*,
-                      const double*, const int32_t*, int32_t, const double*, const double*, int32_t, int32_t, double,
-                      double*, double*, double*) {
-    return fail(ctx, TW_EUNSUPPORTED, "tw_stage_backward: not yet wired");
+int tw_stage_backward(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t nrows, const int32_t* verts,
+                      const double* value, const double* jac, const double* diag, const int32_t* color,
+                      int32_t ncolors, const double* x, const double* y_target, int32_t solver, int32_t sweeps,
+                      double under_relax, double* lambda, double* q_out, double* y_out) {
+    if (!ctx || nv < 0 || !inv_mass || nrows < 0 ||
+        (nrows && (!verts || !value || !jac || !diag || !lambda)) || !x || !y_target || !y_out || sweeps < 1 ||
+        (solver == TW_SOLVER_PGS && nrows && (!color || ncolors < 1)))
+        return fail(ctx, TW_EINVAL, "backward: bad argument");
+    if (solver != TW_SOLVER_PGS && solver != TW_SOLVER_JACOBI)
+        return fail(ctx, TW_EUNSUPPORTED, "backward: only pgs and jacobi run on the device");
+    for (int64_t i = 0; i < nrows; ++i) {
+        if (solver == TW_SOLVER_PGS && (color[i] < 0 || color[i] >= ncolors))
+            return fail(ctx, TW_EINVAL, "backward: color out of range");
+        for (int k = 0; k < 4; ++k)
+            if (verts[4 * i + k] >= nv) return fail(ctx, TW_EINVAL, "backward: vertex id out of range");
+    }
+    CK(cudaSetDevice(ctx->device));
+    // rows carry their own vertex ids: a vertex-only mesh sizes the buffers
+    tw_mesh* m = nullptr;
+    int rc = tw_mesh_create(ctx, nv, inv_mass, 0, nullptr, 0, nullptr, 0, nullptr, &m);
+    if (rc) return rc;
+    struct Guard {
+        tw_mesh* m;
+        ~Guard() { tw_mesh_destroy(m); }
+    } guard{m};
+    tw_resolve_config cfg;
+    tw_default_config(&cfg);
+    cfg.step_limit = 1;
+    cfg.solver = solver;
+    cfg.sweeps = sweeps;
+    cfg.under_relax = under_relax;
+    cfg.edge_constraints = 0;
+    cfg.coloring_mode = TW_COLOR_REFERENCE;  // colors are given
+    if (ctx->pcap < nrows) grow_ll(ctx->pcap, nrows);
+    if (ctx->colcap < ncolors + 1) ctx->colcap = ncolors + 1024;
+    rc = ensure_buffers(ctx, m, cfg);
+    if (rc) return rc;
+    cudaStream_t s = ctx->stream;
+    const size_t n = (size_t)std::max(1, nv);
+    std::vector<double4> x4(n), y4(n);
+    for (int v = 0; v < nv; ++v) {
+        x4[v] = make_double4(x[3 * v], x[3 * v + 1], x[3 * v + 2], inv_mass[v]);
+        y4[v] = make_double4(y_target[3 * v], y_target[3 * v + 1], y_target[3 * v + 2], inv_mass[v]);
+    }
+    std::vector<int4> ids(std::max<int64_t>(1, nrows));
+    for (int64_t i = 0; i < nrows; ++i)
+        ids[i] = make_int4(verts[4 * i], verts[4 * i + 1], verts[4 * i + 2], verts[4 * i + 3]);
+    CK(cudaMemcpyAsync(ctx->x.p, x4.data(), n * 32, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->yk1.p, y4.data(), n * 32, cudaMemcpyHostToDevice, s));
+    if (nrows) {
+        CK(cudaMemcpyAsync(ctx->c_ids.p, ids.data(), nrows * 16, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->c_jac.p, jac, nrows * 96, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->c_value.p, value, nrows * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->c_diag.p, diag, nrows * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->c_lambda.p, lambda, nrows * 8, cudaMemcpyHostToDevice, s));
+        if (solver == TW_SOLVER_PGS) CK(cudaMemcpyAsync(ctx->c_color.p, color, nrows * 4, cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaMemsetAsync(ctx->vcnt.p, 0, n * 4, s));
+    CK(cudaMemsetAsync(ctx->ccount.p, 0, (size_t)ctx->colcap * 4, s));
+    CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), s));
+    Params P = make_params(ctx, m, cfg);
+    CK(coop_stage_backward(s, P, ctx->nblocks, nrows, solver == TW_SOLVER_PGS ? ncolors : 0));
+    ++ctx->launches;
+    Globals G;
+    CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof G, cudaMemcpyDeviceToHost, s));
+    if (nrows) {
+        CK(cudaMemcpyAsync(lambda, ctx->c_lambda.p, nrows * 8, cudaMemcpyDeviceToHost, s));
+        if (q_out) CK(cudaMemcpyAsync(q_out, ctx->c_q.p, nrows * 8, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaMemcpyAsync(x4.data(), ctx->x.p, n * 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (G.error) return fail(ctx, TW_ETIMEOUT, "backward: device error");
+    for (int v = 0; v < nv; ++v) y_out[3 * v] = x4[v].x, y_out[3 * v + 1] = x4[v].y, y_out[3 * v + 2] = x4[v].z;
+    return TW_OK;
 }
 
 }  // extern "C"

@@ -486,6 +486,146 @@ __global__ void k_stage_advance(Params P, double* max_disp) {
     (void)max_disp;
 }
 
+#define STAGE_SYNC() \
+    do {                           \
+        if (!grid_sync(P.g)) return; \
+    } while (0)
+
+// contact predicate of linearize_all over an uploaded pair set (the flags
+// carry active / all_static), block totals for the compaction of ph_rows
+__device__ void ph_stage_contact_flags(const Params& P) {
+    const long long np = P.g->np;
+    long long lo, hi;
+    chunk_of(np, &lo, &hi);
+    long long ncontact = 0;
+    for (long long p = lo + threadIdx.x; p < hi; p += TPB) {
+        const uint64_t key = P.pkey[p];
+        const int ka = key_ka(key), kb = key_kb(key);
+        int va[3], vb[3];
+        split_ids(ka, kb, P.pids[p], va, vb);
+        uint8_t fl = P.pflag[p] & (PF_ACTIVE | PF_ALL_STATIC | PF_DEGENERATE);
+        if (contact_pred(P, ka, kb, va, vb, P.pdd[p], P.pw[p], fl)) {
+            fl |= PF_CONTACT;
+            ++ncontact;
+        }
+        P.pflag[p] = fl;
+    }
+    const long long nct = block_sum(ncontact);
+    if (threadIdx.x == 0) {
+        P.part_c[blockIdx.x] = nct;
+        P.blk_lo[blockIdx.x] = lo;
+        P.blk_hi[blockIdx.x] = hi;
+    }
+}
+
+// vertex -> row incidence of uploaded rows (dynamic vertices only)
+__device__ void ph_stage_incidence(const Params& P, long long nc) {
+    for (long long e = gtid(); e < 4 * nc; e += gstride()) {
+        const int v = (&P.c_ids[e >> 2].x)[e & 3];
+        if (v >= 0 && P.inv_mass[v] > 0.0) record_incidence(P, v, (int)e);
+        else P.c_slot[e] = -1;
+    }
+}
+
+// q = value + sum_m jac_m . (y_k1 - x) of uploaded rows (lcp.cpp:16-20)
+__device__ void ph_stage_q(const Params& P, long long nc) {
+    for (long long i = gtid(); i < nc; i += gstride()) {
+        const int4 id = P.c_ids[i];
+        const int vv[4] = {id.x, id.y, id.z, id.w};
+        const double* J = P.c_jac + i * 12;
+        double q = P.c_value[i];
+        for (int m = 0; m < 4 && vv[m] >= 0; ++m) {
+            const double4 xv = P.x[vv[m]];
+            q += dot(mk(J[3 * m], J[3 * m + 1], J[3 * m + 2]), sub(ld3(P.yk1, vv[m]), mk(xv.x, xv.y, xv.z)));
+        }
+        P.c_q[i] = q;
+    }
+}
+
+// linearize_all on an uploaded pair set (tw_stage_linearize)
+__global__ void __launch_bounds__(TPB, 4) k_stage_linearize(Params P) {
+    if (!prologue(P)) return;  // edge-row list from is_er
+    ph_stage_contact_flags(P);
+    STAGE_SYNC();
+    ph_rows(P, 0, 0);
+}
+
+// color_constraints on uploaded rows (tw_stage_color): incidence, sorted
+// vertex segments, then the reference replica or the device rounds
+__global__ void __launch_bounds__(TPB, 4) k_stage_color(Params P, long long nc) {
+    if (!prologue(P)) return;
+    ph_stage_incidence(P, nc);
+    STAGE_SYNC();
+    ph_inc_totals(P);
+    STAGE_SYNC();
+    ph_inc_offsets(P);
+    STAGE_SYNC();
+    ph_inc_scatter(P, nc);
+    STAGE_SYNC();
+    ph_warm(P, nc);
+    STAGE_SYNC();
+    if (P.cfg.coloring_mode == 0) {
+        ph_color_ref(P, nc);
+        return;
+    }
+    for (int k = 1; *((volatile int*)&P.g->colored) < nc; ++k) {
+        if (k > 1) {
+            ph_color_rank(P);
+            STAGE_SYNC();
+        }
+        ph_color_propose(P, nc, k);
+        STAGE_SYNC();
+        ph_color_conflict(P, k);
+        STAGE_SYNC();
+        ph_color_commit(P, nc, k);
+        STAGE_SYNC();
+    }
+}
+
+// assemble_lcp + sweeps + recover_target on uploaded rows (tw_stage_backward);
+// every row is handled as a contact row, y_out is written into P.x
+__global__ void __launch_bounds__(TPB, 4) k_stage_backward(Params P, long long nc, int ncol) {
+    ph_stage_q(P, nc);
+    ph_stage_incidence(P, nc);
+    STAGE_SYNC();
+    ph_inc_totals(P);
+    STAGE_SYNC();
+    ph_inc_offsets(P);
+    STAGE_SYNC();
+    ph_inc_scatter(P, nc);
+    STAGE_SYNC();
+    ph_warm(P, nc, false);
+    STAGE_SYNC();
+    if (P.cfg.solver == 0) {
+        ph_bucket_count(P, nc);
+        STAGE_SYNC();
+        ph_bucket_scatter(P, nc, ncol, false);
+        STAGE_SYNC();
+        ph_bucket_place(P, nc, false);
+        STAGE_SYNC();
+        for (int sw = 0; sw < P.cfg.sweeps; ++sw)
+            for (int c = 0; c < ncol; ++c) {
+                ph_pgs_color(P, c, ncol, 0);
+                STAGE_SYNC();
+            }
+    } else {
+        for (int sw = 0; sw < P.cfg.sweeps; ++sw) {
+            ph_jacobi_next(P, nc);
+            STAGE_SYNC();
+            ph_jacobi_apply(P, nc);
+            STAGE_SYNC();
+            ph_jacobi_commit(P, nc);
+            STAGE_SYNC();
+        }
+    }
+    // recover_target (lcp.cpp:131-136): dynamic y = y_k1 + impulse, static keep y_k1
+    for (long long v = gtid(); v < P.nv; v += gstride()) {
+        const double4 yk = P.yk1[v];
+        const double4 a = P.imp[v];
+        P.x[v] = P.inv_mass[v] > 0.0 ? make_double4(yk.x + a.x, yk.y + a.y, yk.z + a.z, yk.w) : yk;
+    }
+}
+
 }  // namespace tw
 
 // ==================================================== edge precoloring
@@ -642,6 +782,24 @@ cudaError_t coop_refresh(cudaStream_t s, const Params& P, int nblocks, double bo
     double b = bound;
     void* args[] = {&p, &b};
     return coop((const void*)k_stage_refresh, s, nblocks, args);
+}
+cudaError_t coop_stage_linearize(cudaStream_t s, const Params& P, int nblocks) {
+    Params p = P;
+    void* args[] = {&p};
+    return coop((const void*)k_stage_linearize, s, nblocks, args);
+}
+cudaError_t coop_stage_color(cudaStream_t s, const Params& P, int nblocks, long long nc) {
+    Params p = P;
+    long long n = nc;
+    void* args[] = {&p, &n};
+    return coop((const void*)k_stage_color, s, nblocks, args);
+}
+cudaError_t coop_stage_backward(cudaStream_t s, const Params& P, int nblocks, long long nc, int ncol) {
+    Params p = P;
+    long long n = nc;
+    int c = ncol;
+    void* args[] = {&p, &n, &c};
+    return coop((const void*)k_stage_backward, s, nblocks, args);
 }
 cudaError_t launch_advance(cudaStream_t s, const Params& P, int nblocks) {
     double* md = nullptr;

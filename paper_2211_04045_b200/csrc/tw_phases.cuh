@@ -778,7 +778,7 @@ __device__ __forceinline__ void warm_edges(const Params& P, int v, double im, d3
 // memory); shorter ones by their vertex's thread.
 constexpr int WARM_SHORT = 32, WARM_WARP_MAX = 256;
 
-__device__ void ph_warm(const Params& P, long long nc) {
+__device__ void ph_warm(const Params& P, long long nc, bool reset_colors = true) {
     __shared__ int longv[TPB];
     __shared__ int nlong;
     __shared__ int sseg[TPB / 32][WARM_WARP_MAX];
@@ -900,11 +900,12 @@ __device__ void ph_warm(const Params& P, long long nc) {
         if (threadIdx.x == 0) nlong = 0;
         __syncthreads();
     }
-    for (long long i = gtid(); i < nc; i += gstride()) {
-        P.c_stamp[i] = 0;
-        P.c_lost[i] = 0;
-        P.c_color[i] = -1;
-    }
+    if (reset_colors)  // coloring state of the contact rows (colors given: keep them)
+        for (long long i = gtid(); i < nc; i += gstride()) {
+            P.c_stamp[i] = 0;
+            P.c_lost[i] = 0;
+            P.c_color[i] = -1;
+        }
 }
 
 // ============================================================ coloring
