@@ -440,8 +440,11 @@ __device__ void ph_query_totals(const Params& P) {
 
 __device__ __forceinline__ void vertex_min(const Params& P, int v, double d) {
     const unsigned long long b = to_b(d);
-    // the bound only decreases: skip the atomic when it cannot lower it
-    if (b < *((volatile unsigned long long*)&P.dmin[v])) atomicMin(&P.dmin[v], b);
+    // The bound only decreases, so skip the atomic when it cannot lower it. A
+    // plain (L1-cacheable) read: within the phase a stale copy is only ever
+    // larger than the current bound (the atomic then runs needlessly), and
+    // the grid barrier's fences order it after the reset of the previous step.
+    if (b < P.dmin[v]) atomicMin(&P.dmin[v], b);
 }
 
 // contact predicate of linearize_all (constraints.cpp:186-199): active,
