@@ -44,9 +44,11 @@ struct Bvh {
     int* parent;      // node -> parent (-1 for root)
     // Traversal layout: internal node i (max(1, n-1) of them) holds the boxes
     // of BOTH children in one 64 B line, so a traversal step is one load
-    // round: node[4i + 2s] = (lo.xyz, ref), node[4i + 2s + 1] = (hi.xyz, 0)
+    // round: node[4i + 2s] = (lo.xyz, ref), node[4i + 2s + 1] = (hi.xyz, top)
     // for child slot s; ref = internal node id, or ~index for a leaf (index =
-    // triangle / edge / vertex id of the primitive). With n == 1 the single
+    // triangle / edge / vertex id of the primitive); top = the largest index
+    // in the child's subtree (prunes EE / VV queries, which only need
+    // partners above their own index). With n == 1 the single
     // leaf sits in slot 0 of node 0 and slot 1 is an empty box.
     float4* node;
     unsigned* flag;   // refit arrival counters (internal nodes)

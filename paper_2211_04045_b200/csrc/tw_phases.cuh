@@ -161,11 +161,13 @@ __device__ void ph_refit(const Params& P) {
             prim_box(P, cls, prim, lo, hi);
             float4 blo = make_float4(__double2float_rd(lo[0]), __double2float_rd(lo[1]), __double2float_rd(lo[2]),
                                      __int_as_float(~prim_to_index(P, cls, prim)));
-            float4 bhi = make_float4(__double2float_ru(hi[0]), __double2float_ru(hi[1]), __double2float_ru(hi[2]), 0.f);
+            const int idx = prim_to_index(P, cls, prim);
+            float4 bhi = make_float4(__double2float_ru(hi[0]), __double2float_ru(hi[1]), __double2float_ru(hi[2]),
+                                     __int_as_float(idx));  // w: largest primitive index below
             if (B.n == 1) {
                 B.node[0] = blo, B.node[1] = bhi;
                 B.node[2] = make_float4(INFINITY, INFINITY, INFINITY, __int_as_float(~0));
-                B.node[3] = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+                B.node[3] = make_float4(-INFINITY, -INFINITY, -INFINITY, __int_as_float(-1));
                 continue;
             }
             int node = B.n - 1 + (int)j;
@@ -181,7 +183,8 @@ __device__ void ph_refit(const Params& P) {
                 const float4* q = B.node + 4LL * par;
                 const float4 a0 = __ldcg(q), a1 = __ldcg(q + 1), b0 = __ldcg(q + 2), b1 = __ldcg(q + 3);
                 blo = make_float4(fminf(a0.x, b0.x), fminf(a0.y, b0.y), fminf(a0.z, b0.z), __int_as_float(par));
-                bhi = make_float4(fmaxf(a1.x, b1.x), fmaxf(a1.y, b1.y), fmaxf(a1.z, b1.z), 0.f);
+                bhi = make_float4(fmaxf(a1.x, b1.x), fmaxf(a1.y, b1.y), fmaxf(a1.z, b1.z),
+                                  __int_as_float(max(__float_as_int(a1.w), __float_as_int(b1.w))));
                 node = par;
             }
         }
@@ -368,7 +371,11 @@ __device__ void ph_traverse(const Params& P) {
                 __syncwarp();
                 const float4* nd = B.node + 4LL * node;  // both child boxes: one 64 B line
                 const float4 l0 = nd[0], h0 = nd[1], l1 = nd[2], h1 = nd[3];
-                const bool hit0 = box_hit(qlo, qhi, l0, h0), hit1 = box_hit(qlo, qhi, l1, h1);
+                // ordered classes (EE, VV) only need partners above the query's own index:
+                // subtrees whose largest index is <= ia are skipped
+                const int need = ordered ? ia : -0x7fffffff - 1;
+                const bool hit0 = box_hit(qlo, qhi, l0, h0) && __float_as_int(h0.w) > need;
+                const bool hit1 = box_hit(qlo, qhi, l1, h1) && __float_as_int(h1.w) > need;
                 const bool any0 = __any_sync(0xffffffffu, hit0), any1 = __any_sync(0xffffffffu, hit1);
                 const int r0 = __float_as_int(l0.w), r1 = __float_as_int(l1.w);
 #pragma unroll
