@@ -317,10 +317,12 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
             g->max_color = -1;
         }
         // ---- backward step at x^(l)
-        ph_rows(P, sel, narch);
+        ph_rows(P);
         SYNC();
         const long long nc = g->nc;
         if (lead) g->nactive = 0;
+        ph_rows_build(P, sel, narch, nc);
+        SYNC();
         ph_inc_totals(P);
         SYNC();
         ph_inc_offsets(P);
@@ -547,7 +549,9 @@ __global__ void __launch_bounds__(TPB, 4) k_stage_linearize(Params P) {
     if (!prologue(P)) return;  // edge-row list from is_er
     ph_stage_contact_flags(P);
     STAGE_SYNC();
-    ph_rows(P, 0, 0);
+    ph_rows(P);
+    STAGE_SYNC();
+    ph_rows_build(P, 0, 0, P.g->nc);
 }
 
 // color_constraints on uploaded rows (tw_stage_color): incidence, sorted

@@ -113,6 +113,8 @@ __device__ __forceinline__ void chunk_of(long long n, long long* lo, long long* 
 
 __device__ __forceinline__ long long gtid() { return (long long)blockIdx.x * TPB + threadIdx.x; }
 __device__ __forceinline__ long long gstride() { return (long long)gridDim.x * TPB; }
+__device__ __forceinline__ long long gwarp() { return gtid() >> 5; }
+__device__ __forceinline__ long long gwarps() { return gstride() >> 5; }
 
 struct XLoad {
     const double4* x;
@@ -616,14 +618,13 @@ __device__ __forceinline__ d3 edge_jac(const double4& g4, int m) {
 // B2: order-preserving compaction of the contact rows (pair order), their
 // q = c + J (y_k1 - x), warm-start multiplier from the archive, vertex
 // incidence lists; plus every edge row's value / jacobian / diag / q.
-__device__ void ph_rows(const Params& P, int sel, long long narch) {
+__device__ void ph_rows(const Params& P) {
     const long long lo = P.blk_lo[blockIdx.x], hi = P.blk_hi[blockIdx.x];
     const long long nc_total = prefix_of(P.part_c, gridDim.x);
     long long base = prefix_of(P.part_c, blockIdx.x);
-    const uint64_t* akey = P.arch_key[sel];
-    const double* aval = P.arch_val[sel];
-    // each thread scans 16 consecutive pairs per tile (one block scan per
-    // 4096 pairs), then builds the rows of its contact pairs in pair order
+    // pass 1: the contact pairs in pair order (= row order). Each thread scans
+    // 16 consecutive pairs per tile (one block scan per 4096 pairs) and
+    // records the pair of each row (c_arch holds it until ph_rows_build).
     constexpr int PER = 16;
     for (long long t = lo; t < hi; t += (long long)TPB * PER) {
         const long long p0 = t + (long long)threadIdx.x * PER;
@@ -632,12 +633,26 @@ __device__ void ph_rows(const Params& P, int sel, long long narch) {
         for (int j = 0; j < PER; ++j)
             if (p0 + j < hi && (P.pflag[p0 + j] & PF_CONTACT)) fm |= 1u << j;
         long long tile_tot;
-        long long pos = base + block_scan(__popc(fm), &tile_tot) - 1;
+        long long pos = base + block_scan(__popc(fm), &tile_tot);
         base += tile_tot;
         while (fm) {
-        const long long p = p0 + (__ffs(fm) - 1);
-        fm &= fm - 1;
-        ++pos;
+            P.c_arch[pos++] = p0 + (__ffs(fm) - 1);
+            fm &= fm - 1;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.g->nc = nc_total;
+    if (P.cfg.edge_constraints)
+        for (long long k = gtid(); k < P.g->ner; k += gstride()) edge_row(P, P.er_edge[k]);
+}
+
+// B2': the contact rows, one thread per row over the whole grid (the contact
+// pairs cluster where the knot is tight: building them in their pair chunks
+// left most CTAs idle)
+__device__ void ph_rows_build(const Params& P, int sel, long long narch, long long nc) {
+    const uint64_t* akey = P.arch_key[sel];
+    const double* aval = P.arch_val[sel];
+    for (long long pos = gtid(); pos < nc; pos += gstride()) {
+        const long long p = P.c_arch[pos];
         const uint64_t key = P.pkey[p];
         const int ka = key_ka(key), kb = key_kb(key);
         int va[3], vb[3];
@@ -682,11 +697,7 @@ __device__ void ph_rows(const Params& P, int sel, long long narch) {
             if (m < c.nverts && P.inv_mass[c.v[m]] > 0.0) record_incidence(P, c.v[m], e);
             else P.c_slot[e] = -1;
         }
-        }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) P.g->nc = nc_total;
-    if (P.cfg.edge_constraints)
-        for (long long k = gtid(); k < P.g->ner; k += gstride()) edge_row(P, P.er_edge[k]);
 }
 
 // B2b: per-block totals of the incidence counts over the block's vertex chunk
@@ -784,131 +795,119 @@ __device__ __forceinline__ void warm_edges(const Params& P, int v, double im, d3
     }
 }
 
-// Segments longer than this are sorted by a warp (rank by counting in shared
-// memory); shorter ones by their vertex's thread.
+// Short vertex segments (<= 32 entries) are handled by one thread per
+// vertex; long ones by one warp per vertex (rank-by-counting sort in shared
+// memory up to WARM_WARP_MAX entries, lane 0 beyond; lanes form the terms,
+// lane 0 adds them in row order). Both loops stride over the vertices, so
+// the busy contact region spreads over the whole grid.
 constexpr int WARM_SHORT = 32, WARM_WARP_MAX = 256;
 
 __device__ void ph_warm(const Params& P, long long nc, bool reset_colors = true) {
-    __shared__ int longv[TPB];
-    __shared__ int nlong;
     __shared__ int sseg[TPB / 32][WARM_WARP_MAX];
-    if (threadIdx.x == 0) nlong = 0;
-    __syncthreads();
-    long long lo, hi;
-    chunk_of(P.nv, &lo, &hi);
-    for (long long base = lo; base < hi; base += TPB) {
-        const long long v = base + threadIdx.x;
-        if (v < hi) {
-            const double im = P.inv_mass[v];
-            const int b = P.voff[v], n = P.voff[v + 1] - b;
-            if (im > 0.0 && n > WARM_SHORT) {
-                longv[atomicAdd(&nlong, 1)] = (int)v;  // sorted + summed by a warp below
-            } else {
-                d3 a = mk(0, 0, 0);
-                if (im > 0.0) {
-                    sort_segment(P.vinc + b, n);
-                    // entry rank inside the vertex clique (round-1 coloring proposal)
-                    for (int k = 0; k < n; ++k) P.erank[P.vinc[b + k]] = k;
-                    for_sorted_entries(P, (int)v, [&](int e) {
-                        const int row = e >> 2, m = e & 3;
-                        const double lam = P.c_lambda[row];
-                        if (lam != 0.0) {
-                            const double* J = P.c_jac + (long long)row * 12 + 3 * m;
-                            imp_add(a, im * lam, mk(J[0], J[1], J[2]));
-                        }
-                    });
-                    warm_edges(P, (int)v, im, a);
-                }
-                P.imp[v] = make_double4(a.x, a.y, a.z, im);  // w: inv_mass, read with the impulse by the PGS
-            }
-            if (P.cfg.coloring_mode == 1) {
-                // device coloring: the vertex starts with the colors of its edge rows
-                unsigned long long mk4[4] = {0, 0, 0, 0};
-                int big = 0;
-                if (im > 0.0 && P.cfg.edge_constraints)
-                    for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
-                        const int ec = P.edge_color[P.vedge[q]];
-                        if (ec >= 256) big = 1;
-                        else if (ec >= 0) mk4[ec >> 6] |= 1ull << (ec & 63);
-                    }
-                for (int w = 0; w < 4; ++w) P.vmask[4 * v + w] = mk4[w];
-                P.vbig[v] = big;
-            }
-        }
-        __syncthreads();
-        // long segments: one warp per vertex
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        for (int j = w; j < nlong; j += TPB / 32) {
-            const int vv = longv[j];
-            const double im = P.inv_mass[vv];
-            const int b = P.voff[vv], n = P.voff[vv + 1] - b;
-            int* seg = P.vinc + b;
-            if (n <= WARM_WARP_MAX) {
-                for (int i = lane; i < n; i += 32) sseg[w][i] = seg[i];
-                __syncwarp();
-                int rk[WARM_WARP_MAX / 32], ev[WARM_WARP_MAX / 32];
-#pragma unroll
-                for (int r = 0; r < WARM_WARP_MAX / 32; ++r) {
-                    const int i = lane + 32 * r;
-                    rk[r] = -1;
-                    if (i < n) {
-                        const int e = sseg[w][i];
-                        int c = 0;
-                        for (int t = 0; t < n; ++t) c += sseg[w][t] < e;
-                        rk[r] = c, ev[r] = e;
-                    }
-                }
-                __syncwarp();
-#pragma unroll
-                for (int r = 0; r < WARM_WARP_MAX / 32; ++r)
-                    if (rk[r] >= 0) {
-                        sseg[w][rk[r]] = ev[r];
-                        seg[rk[r]] = ev[r];
-                        P.erank[ev[r]] = rk[r];
-                    }
-                __syncwarp();
-            } else {
-                if (lane == 0) {
-                    sort_segment(seg, n);
-                    for (int k = 0; k < n; ++k) P.erank[seg[k]] = k;
-                }
-                __syncwarp();
-            }
-            // ordered sum of the contact terms: lanes form the terms, lane 0 adds them in row order
+    for (long long vl = gtid(); vl < P.nv; vl += gstride()) {
+        const int v = (int)vl;
+        const double im = P.inv_mass[v];
+        const int b = P.voff[v], n = P.voff[v + 1] - b;
+        if (!(im > 0.0) || n <= WARM_SHORT) {
             d3 a = mk(0, 0, 0);
-            for (int k0 = 0; k0 < n; k0 += 32) {
-                const int k = k0 + lane;
-                bool nz = false;
-                d3 t = mk(0, 0, 0);
-                if (k < n) {
-                    const int e = n <= WARM_WARP_MAX ? sseg[w][k] : seg[k];
+            if (im > 0.0) {
+                sort_segment(P.vinc + b, n);
+                for (int k = 0; k < n; ++k) P.erank[P.vinc[b + k]] = k;  // rank inside the vertex clique
+                for_sorted_entries(P, v, [&](int e) {
                     const int row = e >> 2, m = e & 3;
                     const double lam = P.c_lambda[row];
                     if (lam != 0.0) {
                         const double* J = P.c_jac + (long long)row * 12 + 3 * m;
-                        const double sc = im * lam;
-                        t = mk(sc * J[0], sc * J[1], sc * J[2]);
-                        nz = true;
+                        imp_add(a, im * lam, mk(J[0], J[1], J[2]));
                     }
+                });
+                warm_edges(P, v, im, a);
+            }
+            P.imp[v] = make_double4(a.x, a.y, a.z, im);  // w: inv_mass, read with the impulse by the PGS
+        }
+        if (P.cfg.coloring_mode == 1) {
+            // device coloring: the vertex starts with the colors of its edge rows
+            unsigned long long mk4[4] = {0, 0, 0, 0};
+            int big = 0;
+            if (im > 0.0 && P.cfg.edge_constraints)
+                for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
+                    const int ec = P.edge_color[P.vedge[q]];
+                    if (ec >= 256) big = 1;
+                    else if (ec >= 0) mk4[ec >> 6] |= 1ull << (ec & 63);
                 }
-                const unsigned nzm = __ballot_sync(0xffffffffu, nz);
-                for (int q = 0; q < 32; ++q) {
-                    if (!((nzm >> q) & 1u)) continue;
-                    const double tx = __shfl_sync(0xffffffffu, t.x, q);
-                    const double ty = __shfl_sync(0xffffffffu, t.y, q);
-                    const double tz = __shfl_sync(0xffffffffu, t.z, q);
-                    a.x = a.x + tx, a.y = a.y + ty, a.z = a.z + tz;
+            for (int k = 0; k < 4; ++k) P.vmask[4LL * v + k] = mk4[k];
+            P.vbig[v] = big;
+        }
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (long long vl = gwarp(); vl < P.nv; vl += gwarps()) {
+        const int v = (int)vl;
+        const int b = P.voff[v], n = P.voff[v + 1] - b;
+        if (n <= WARM_SHORT) continue;  // (static vertices have no entries)
+        const double im = P.inv_mass[v];
+        int* seg = P.vinc + b;
+        if (n <= WARM_WARP_MAX) {
+            for (int i = lane; i < n; i += 32) sseg[w][i] = seg[i];
+            __syncwarp();
+            int rk[WARM_WARP_MAX / 32], ev[WARM_WARP_MAX / 32];
+#pragma unroll
+            for (int r = 0; r < WARM_WARP_MAX / 32; ++r) {
+                const int i = lane + 32 * r;
+                rk[r] = -1;
+                if (i < n) {
+                    const int e = sseg[w][i];
+                    int c = 0;
+                    for (int t = 0; t < n; ++t) c += sseg[w][t] < e;
+                    rk[r] = c, ev[r] = e;
                 }
             }
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < WARM_WARP_MAX / 32; ++r)
+                if (rk[r] >= 0) {
+                    sseg[w][rk[r]] = ev[r];
+                    seg[rk[r]] = ev[r];
+                    P.erank[ev[r]] = rk[r];
+                }
+            __syncwarp();
+        } else {
             if (lane == 0) {
-                warm_edges(P, vv, im, a);
-                P.imp[vv] = make_double4(a.x, a.y, a.z, im);
+                sort_segment(seg, n);
+                for (int k = 0; k < n; ++k) P.erank[seg[k]] = k;
             }
             __syncwarp();
         }
-        __syncthreads();
-        if (threadIdx.x == 0) nlong = 0;
-        __syncthreads();
+        // ordered sum of the contact terms (lcp.cpp:16-23: contact rows in row order)
+        d3 a = mk(0, 0, 0);
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int k = k0 + lane;
+            bool nz = false;
+            d3 t = mk(0, 0, 0);
+            if (k < n) {
+                const int e = n <= WARM_WARP_MAX ? sseg[w][k] : seg[k];
+                const int row = e >> 2, m = e & 3;
+                const double lam = P.c_lambda[row];
+                if (lam != 0.0) {
+                    const double* J = P.c_jac + (long long)row * 12 + 3 * m;
+                    const double sc = im * lam;
+                    t = mk(sc * J[0], sc * J[1], sc * J[2]);
+                    nz = true;
+                }
+            }
+            const unsigned nzm = __ballot_sync(0xffffffffu, nz);
+            for (int q = 0; q < 32; ++q) {
+                if (!((nzm >> q) & 1u)) continue;
+                const double tx = __shfl_sync(0xffffffffu, t.x, q);
+                const double ty = __shfl_sync(0xffffffffu, t.y, q);
+                const double tz = __shfl_sync(0xffffffffu, t.z, q);
+                a.x = a.x + tx, a.y = a.y + ty, a.z = a.z + tz;
+            }
+        }
+        if (lane == 0) {
+            warm_edges(P, v, im, a);
+            P.imp[v] = make_double4(a.x, a.y, a.z, im);
+        }
+        __syncwarp();
     }
     if (reset_colors)  // coloring state of the contact rows (colors given: keep them)
         for (long long i = gtid(); i < nc; i += gstride()) {
@@ -934,8 +933,6 @@ __device__ void ph_warm(const Params& P, long long nc, bool reset_colors = true)
 //            color masks of their vertices.
 // The oracle's or_color_device (oracle/or_constraints.c) states the same
 // rounds row by row.
-__device__ __forceinline__ long long gwarp() { return gtid() >> 5; }
-__device__ __forceinline__ long long gwarps() { return gstride() >> 5; }
 
 __device__ void ph_color_rank(const Params& P) {
     const int lane = threadIdx.x & 31;
