@@ -374,6 +374,7 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.refpool = ctx->refpool.as<int>();
     P.nblocks = ctx->nblocks;
     P.pgs_tail_rows = ctx->pgs_tail_rows;
+    P.pw_all = 1;
     P.experiment = std::getenv("TW_EXPERIMENT") ? std::atoi(std::getenv("TW_EXPERIMENT")) : 0;
     P.part_q = ctx->part_q.as<long long>();
     P.part_c = ctx->part_c.as<long long>();
@@ -417,6 +418,7 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
         if (rc) return rc;
         Params P = make_params(ctx, m, cfg);
         if (!trace_host) P.trace = nullptr;  // lets the kernel skip work only a trace would show
+        P.pw_all = 0;
         CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), ctx->stream));
         // color tables return to zero at the end of every step; an attempt
         // aborted for capacity growth may leave counts behind

@@ -206,6 +206,7 @@ struct Params {
     // on one CTA (ph_pgs_tail); 0 disables
     long long pgs_tail_rows;
     int experiment;  // TW_EXPERIMENT (profiling experiments only; 0 in production)
+    int pw_all;      // store pair weights for every pair (stage entries) or contact pairs only (resolve)
     // per block scratch
     int nblocks;
     long long* part_q;

@@ -543,7 +543,7 @@ __device__ void ph_emit_records(const Params& P, bool first_search) {
         }
         P.pids[p] = ids;
         P.pdd[p] = dd;
-        P.pw[p] = w;
+        if (P.pw_all || (fl & PF_CONTACT)) P.pw[p] = w;  // weights are read for contact rows only
         P.pflag[p] = fl;
         for (int k = 0; k <= ka; ++k) vertex_min(P, va[k], c.dist);
         for (int k = 0; k <= kb; ++k) vertex_min(P, vb[k], c.dist);
@@ -1738,7 +1738,6 @@ __device__ void ph_refresh(const Params& P, double bound, bool next_search) {
             dd = make_double4(dir.x, dir.y, dir.z, c.dist);
             w = pack_weights(ka, kb, c);
             P.pdd[p] = dd;
-            P.pw[p] = w;
             if (c.degenerate) fl |= PF_DEGENERATE;
             if (c.dist < bound) fl |= PF_ACTIVE;
         }
@@ -1753,6 +1752,9 @@ __device__ void ph_refresh(const Params& P, double bound, bool next_search) {
             fl |= PF_CONTACT;
             ++ncontact;
         }
+        // weights are read for contact rows only (ph_rows_build); the stage
+        // entries return them for every pair
+        if (h == 1 && (P.pw_all || (fl & PF_CONTACT))) P.pw[p] = w;
         P.pflag[p] = fl;
     }
     const long long nct = block_sum(ncontact);
