@@ -192,7 +192,13 @@ int tw_stage_backward(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t n
 int tw_stage_advance(tw_ctx* ctx, int32_t nv, const double* inv_mass, const double* y,
                      const double* D, double gamma, double* x, double* r, double* max_disp);
 
-/* ---- CCD certification on the device is out of scope this round ---- */
+/* ccd_certify (proj/src/testkit/ccd.cpp:339-498) of the linear segment
+ * x0 -> x1 (nv * 3 doubles each): the number of vertex-triangle and edge-edge
+ * stencils whose motion crosses (*violations) and how many of those are
+ * certain (*certain, away from the numerical margins). Zero violations
+ * certify the segment intersection-free. Runs on the device. */
+int tw_ccd_certify(tw_ctx* ctx, tw_mesh* mesh, const double* x0, const double* x1, int32_t* violations,
+                   int32_t* certain);
 
 #ifdef __cplusplus
 }

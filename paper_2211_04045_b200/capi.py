@@ -65,7 +65,7 @@ EXPORTS = [
     "tw_ctx_kernel_launches", "tw_ctx_phase_profile", "tw_mesh_create", "tw_mesh_num_edges", "tw_mesh_edges",
     "tw_mesh_destroy", "tw_resolve", "tw_resolve_device", "tw_stage_closest", "tw_stage_search",
     "tw_stage_refresh", "tw_stage_linearize", "tw_stage_color", "tw_stage_backward",
-    "tw_stage_advance",
+    "tw_stage_advance", "tw_ccd_certify",
 ]
 
 _LIB = None
@@ -97,6 +97,7 @@ def lib():
         L.tw_stage_search.argtypes = [P, P, P, C.c_double, C.c_int64, P, P, P, P, P, P, P]
         L.tw_stage_refresh.argtypes = [P, P, P, C.c_double, C.c_int64, P, P, P, P, P, P, P]
         L.tw_stage_advance.argtypes = [P, C.c_int32, P, P, P, C.c_double, P, P, P]
+        L.tw_ccd_certify.argtypes = [P, P, P, P, P, P]
         L.tw_stage_linearize.argtypes = [P, P, P, C.c_int64, P, P, P, P, P, P, P, C.c_double, C.c_double,
                                          C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P, P, P]
         L.tw_stage_color.argtypes = [P, P, C.c_int64, P, P, P, P, C.c_uint64, C.c_int32, C.c_int32, P, P]
@@ -401,3 +402,23 @@ def backward(ctx: Context, inv_mass, rows: Rows, colors, ncolors, x, y, lam=None
                                       _p(np.ascontiguousarray(rows.diag, np.float64)), _p(col), int(ncolors),
                                       _p(x), _p(y), solver, sweeps, under_relax, _p(lam), _p(q), _p(yo)))
     return {"lambda": lam, "q": q[:n], "y": yo}
+
+
+def ccd_certify(ctx: Context, mesh: Mesh, x0, x1):
+    """ccd_certify (testkit/ccd.cpp) of the segment x0 -> x1 on the device:
+    (violations, certain)."""
+    x0 = np.ascontiguousarray(x0, np.float64).reshape(-1, 3)
+    x1 = np.ascontiguousarray(x1, np.float64).reshape(-1, 3)
+    v, c = C.c_int32(0), C.c_int32(0)
+    ctx.check(lib().tw_ccd_certify(ctx.h, mesh.h, _p(x0), _p(x1), C.byref(v), C.byref(c)))
+    return v.value, c.value
+
+
+def ccd_certify_path(ctx: Context, mesh: Mesh, path):
+    """Certify every segment of a recorded resolve path: (violations, certain) totals."""
+    tot, cert = 0, 0
+    for i in range(len(path) - 1):
+        v, c = ccd_certify(ctx, mesh, path[i], path[i + 1])
+        tot += v
+        cert += c
+    return tot, cert

@@ -1058,6 +1058,45 @@ int tw_stage_advance(tw_ctx* ctx, int32_t nv, const double* inv_mass, const doub
     return TW_OK;
 }
 
+int tw_ccd_certify(tw_ctx* ctx, tw_mesh* m, const double* x0, const double* x1, int32_t* violations,
+                   int32_t* certain) {
+    if (!ctx || !m || !x0 || !x1 || !violations) return fail(ctx, TW_EINVAL, "ccd_certify: bad argument");
+    CK(cudaSetDevice(ctx->device));
+    tw_resolve_config cfg;
+    tw_default_config(&cfg);
+    cfg.step_limit = 1;
+    int rc = TW_OK;
+    cudaStream_t s = ctx->stream;
+    Globals G;
+    for (int attempt = 0;; ++attempt) {
+        rc = ensure_buffers(ctx, m, cfg);
+        if (rc) return rc;
+        rc = stage_upload_x(ctx, m, x1);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(ctx->yk1.p, ctx->x.p, (size_t)m->nv * 32, cudaMemcpyDeviceToDevice, s));
+        rc = stage_upload_x(ctx, m, x0);
+        if (rc) return rc;
+        Params P = make_params(ctx, m, cfg);
+        P.ccd_x1 = ctx->yk1.as<double4>();
+        P.niso = 0;  // the certifier has no isolated-vertex classes (VT over every vertex, EE)
+        CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), s));
+        rc = build_bvhs(ctx, m);
+        if (rc) return rc;
+        CK(coop_ccd(s, P, ctx->nblocks));
+        ++ctx->launches;
+        CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof G, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (G.error & ERR_TIMEOUT) return fail(ctx, TW_ETIMEOUT, "ccd_certify: watchdog");
+        if (G.error & ERR_CAP_STACK) return fail(ctx, TW_ECAPACITY, "ccd_certify: traversal stack overflow");
+        if (!(G.error & ERR_CAP_CAND)) break;
+        if (attempt > 10) return fail(ctx, TW_ECAPACITY, "ccd_certify: capacity");
+        grow_ll(ctx->ccap, (long long)G.ncand + (long long)G.ncand / 4);
+    }
+    *violations = G.ccd_violations;
+    if (certain) *certain = G.ccd_certain;
+    return TW_OK;
+}
+
 int tw_stage_linearize(tw_ctx* ctx, tw_mesh* m, const double* x, int64_t np, const uint64_t* keys,
                        const double* dist, const double* wa, const double* wb, const double* dir,
                        const uint8_t* flags, const double* edge_targets, double delta, double sigma, int32_t family,

@@ -63,6 +63,8 @@ struct Globals {
     unsigned long long work_q;  // dynamic query counter of the traversal (reset by the refit)
     unsigned long long ncand;   // broad-phase candidates of the current search (reset by the refit)
     unsigned long long work_s;  // dynamic query counter of the partner sort (reset by the refit)
+    int ccd_violations;         // certification results (k_ccd)
+    int ccd_certain;
     int ner;             // edge rows of this call (set by the prologue)
     int needed_k;
     long long np;        // pairs in the set
@@ -207,6 +209,7 @@ struct Params {
     long long pgs_tail_rows;
     int experiment;  // TW_EXPERIMENT (profiling experiments only; 0 in production)
     int pw_all;      // store pair weights for every pair (stage entries) or contact pairs only (resolve)
+    const double4* ccd_x1;  // certification (k_ccd): end positions of the segment, else null
     // per block scratch
     int nblocks;
     long long* part_q;

@@ -35,6 +35,7 @@ cudaError_t coop_refresh(cudaStream_t s, const Params& P, int nblocks, double bo
 cudaError_t launch_advance(cudaStream_t s, const Params& P, int nblocks);
 // stage kernels for stage-by-stage parity (tw_stage_linearize/color/backward)
 cudaError_t coop_stage_linearize(cudaStream_t s, const Params& P, int nblocks);
+cudaError_t coop_ccd(cudaStream_t s, const Params& P, int nblocks);  // certification of x -> ccd_x1
 cudaError_t coop_stage_color(cudaStream_t s, const Params& P, int nblocks, long long nc);
 cudaError_t coop_stage_backward(cudaStream_t s, const Params& P, int nblocks, long long nc, int ncol);
 cudaError_t launch_closest(cudaStream_t s, int nv, const double4* x, long long n, const int* kinds,

@@ -4,6 +4,7 @@
 // used for stage-by-stage parity. Compiled with -fmad=false.
 #include <cub/device/device_radix_sort.cuh>
 
+#include "tw_ccd.cuh"
 #include "tw_internal.h"
 #include "tw_phases.cuh"
 
@@ -544,6 +545,73 @@ __device__ void ph_stage_q(const Params& P, long long nc) {
     }
 }
 
+// ================================================ CCD certification
+// ccd_certify (testkit/ccd.cpp:339-498) of one segment x -> ccd_x1: swept-box
+// candidates from the LBVH walk (VT: every vertex against the triangles; EE:
+// canonical e1 < e2), the reference's exact double swept-box overlap and
+// adjacency filters, then the per-stencil test (tw_ccd.cuh).
+__device__ __forceinline__ void swept_box_d(const Params& P, const int* ids, int n, double lo[3], double hi[3]) {
+    const d3 s0 = ld3(P.x, ids[0]);
+    lo[0] = hi[0] = s0.x, lo[1] = hi[1] = s0.y, lo[2] = hi[2] = s0.z;
+    for (int i = 0; i < n; ++i) {
+        const d3 p = ld3(P.x, ids[i]), q = ld3(P.ccd_x1, ids[i]);
+        lo[0] = mind(mind(lo[0], p.x), q.x), lo[1] = mind(mind(lo[1], p.y), q.y), lo[2] = mind(mind(lo[2], p.z), q.z);
+        hi[0] = maxd(maxd(hi[0], p.x), q.x), hi[1] = maxd(maxd(hi[1], p.y), q.y), hi[2] = maxd(maxd(hi[2], p.z), q.z);
+    }
+    for (int k = 0; k < 3; ++k) lo[k] = lo[k] - 1e-12, hi[k] = hi[k] + 1e-12;
+}
+
+__device__ void ph_ccd_eval(const Params& P) {
+    const long long n = min((long long)P.g->ncand, P.ccap);
+    int viol = 0, cert = 0;
+    for (long long i = gtid(); i < n; i += gstride()) {
+        const int2 e = P.cand[i];
+        int ka, ia, kb, cls;
+        query_of(P, e.x, &ka, &ia, &kb, &cls);
+        const int ib = e.y;
+        int ids[4];
+        bool is_vt;
+        if (ka == KV) {  // vertex against triangle
+            const int4 t = P.tris[ib];
+            if (ia == t.x || ia == t.y || ia == t.z) continue;
+            ids[0] = ia, ids[1] = t.x, ids[2] = t.y, ids[3] = t.z;
+            is_vt = true;
+        } else {  // edge against edge, ia < ib
+            if (ib <= ia) continue;
+            const int2 a = P.edges[ia], b = P.edges[ib];
+            if (a.x == b.x || a.x == b.y || a.y == b.x || a.y == b.y) continue;
+            ids[0] = a.x, ids[1] = a.y, ids[2] = b.x, ids[3] = b.y;
+            is_vt = false;
+        }
+        double alo[3], ahi[3], blo[3], bhi[3];
+        swept_box_d(P, ids, is_vt ? 1 : 2, alo, ahi);
+        swept_box_d(P, ids + (is_vt ? 1 : 2), is_vt ? 3 : 2, blo, bhi);
+        if (!(alo[0] <= bhi[0] && alo[1] <= bhi[1] && alo[2] <= bhi[2] && blo[0] <= ahi[0] && blo[1] <= ahi[1] &&
+              blo[2] <= ahi[2]))
+            continue;
+        d3 s[4], en[4];
+        for (int k = 0; k < 4; ++k) s[k] = ld3(P.x, ids[k]), en[k] = ld3(P.ccd_x1, ids[k]);
+        const int h = ccd::check_stencil(s, en, is_vt);
+        if (h != ccd::HIT_NONE) {
+            ++viol;
+            cert += h == ccd::HIT_CERTAIN;
+        }
+    }
+    const long long v = block_sum(viol), c = block_sum(cert);
+    if (threadIdx.x == 0 && v) {
+        atomicAdd(&P.g->ccd_violations, (int)v);
+        atomicAdd(&P.g->ccd_certain, (int)c);
+    }
+}
+
+__global__ void __launch_bounds__(TPB, 4) k_ccd(Params P) {
+    ph_refit(P);
+    STAGE_SYNC();
+    ph_traverse(P);
+    STAGE_SYNC();
+    ph_ccd_eval(P);
+}
+
 // linearize_all on an uploaded pair set (tw_stage_linearize)
 __global__ void __launch_bounds__(TPB, 4) k_stage_linearize(Params P) {
     if (!prologue(P)) return;  // edge-row list from is_er
@@ -786,6 +854,11 @@ cudaError_t coop_refresh(cudaStream_t s, const Params& P, int nblocks, double bo
     double b = bound;
     void* args[] = {&p, &b};
     return coop((const void*)k_stage_refresh, s, nblocks, args);
+}
+cudaError_t coop_ccd(cudaStream_t s, const Params& P, int nblocks) {
+    Params p = P;
+    void* args[] = {&p};
+    return coop((const void*)k_ccd, s, nblocks, args);
 }
 cudaError_t coop_stage_linearize(cudaStream_t s, const Params& P, int nblocks) {
     Params p = P;

@@ -142,6 +142,15 @@ __device__ __forceinline__ void prim_box(const Params& P, int cls, int prim, dou
         lo[1] = fmin(lo[1], p.y), hi[1] = fmax(hi[1], p.y);
         lo[2] = fmin(lo[2], p.z), hi[2] = fmax(hi[2], p.z);
     }
+    if (P.ccd_x1) {  // certification: the box swept from x to x1
+        for (int i = 0; i < n; ++i) {
+            const d3 p = ld3(P.ccd_x1, ids[i]);
+            lo[0] = fmin(lo[0], p.x), hi[0] = fmax(hi[0], p.x);
+            lo[1] = fmin(lo[1], p.y), hi[1] = fmax(hi[1], p.y);
+            lo[2] = fmin(lo[2], p.z), hi[2] = fmax(hi[2], p.z);
+        }
+        for (int k = 0; k < 3; ++k) lo[k] -= 1e-12, hi[k] += 1e-12;
+    }
 }
 
 __device__ __forceinline__ int prim_to_index(const Params& P, int cls, int prim) {
@@ -316,14 +325,21 @@ __device__ void ph_traverse(const Params& P) {
             double lo3[3], hi3[3];
             const d3 p0 = ld3(P.x, va[0]);
             lo3[0] = hi3[0] = p0.x, lo3[1] = hi3[1] = p0.y, lo3[2] = hi3[2] = p0.z;
-            if (ka == KE) {
-                const d3 p1 = ld3(P.x, va[1]);
+            for (int k = 0; k <= ka; ++k) {
+                const d3 p1 = ld3(P.x, va[k]);
                 lo3[0] = fmin(lo3[0], p1.x), hi3[0] = fmax(hi3[0], p1.x);
                 lo3[1] = fmin(lo3[1], p1.y), hi3[1] = fmax(hi3[1], p1.y);
                 lo3[2] = fmin(lo3[2], p1.z), hi3[2] = fmax(hi3[2], p1.z);
+                if (P.ccd_x1) {  // certification: swept from x to x1
+                    const d3 p2 = ld3(P.ccd_x1, va[k]);
+                    lo3[0] = fmin(lo3[0], p2.x), hi3[0] = fmax(hi3[0], p2.x);
+                    lo3[1] = fmin(lo3[1], p2.y), hi3[1] = fmax(hi3[1], p2.y);
+                    lo3[2] = fmin(lo3[2], p2.z), hi3[2] = fmax(hi3[2], p2.z);
+                }
             }
-            // float box of the query inflated by d_max, rounded outwards
-            const double dinfl = P.cfg.d_max * (1.0 + 1e-6) + 1e-12;
+            // float box of the query inflated by d_max (certification: 1e-12 on
+            // both boxes), rounded outwards
+            const double dinfl = P.ccd_x1 ? 1e-12 : P.cfg.d_max * (1.0 + 1e-6) + 1e-12;
             qlo = make_float4(__double2float_rd(lo3[0] - dinfl), __double2float_rd(lo3[1] - dinfl),
                               __double2float_rd(lo3[2] - dinfl), 0.f);
             qhi = make_float4(__double2float_ru(hi3[0] + dinfl), __double2float_ru(hi3[1] + dinfl),
