@@ -247,6 +247,22 @@ def run_ours(args):
     clk = clocks.stop()
     barrier()
 
+    # ---- certification of the resolve path on the device (testkit ccd.cpp):
+    # literal CCD stencil tests of every segment, outside the timed regions
+    _, st_path = capi.resolve(ctx, mesh, sc.x, sc.y, record_path=True, **dict(kw, step_limit=64))
+    path = st_path["path"]
+    ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    viol = cert = stencils = 0
+    ca.record(stream)
+    for i in range(len(path) - 1):
+        v, c, n = capi.ccd_certify(ctx, mesh, path[i], path[i + 1], candidates=True)
+        viol, cert, stencils = viol + v, cert + c, stencils + n
+    cb.record(stream)
+    torch.cuda.synchronize()
+    ccd_ms = ca.elapsed_time(cb)
+    ccd = {"segments": len(path) - 1, "violations": viol, "certain_violations": cert,
+           "candidate_stencils": stencils, "ms_incl_host_copies": round(ccd_ms, 3),
+           "stencils_per_s": round(stencils / (ccd_ms / 1e3), 1), "intersection_free": viol == 0}
     dev_ms_max, e2e_ms_max = max_over_ranks([dev_ms, e2e_ms], dist, "cuda")
     value = whole_job_rate(world, args.steps, dev_ms_max)
     e2e_value = whole_job_rate(world, args.steps, e2e_ms_max)
@@ -279,6 +295,7 @@ def run_ours(args):
             "e2e": {"value": round(e2e_value, 3), "unit": "steps/s", "h2d_bytes_per_step": 2 * sc.nv * 24,
                     "d2h_bytes_per_step": sc.nv * 24 + 160},
             "gpu_launches": launches,
+            "ccd_certification": ccd,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": traffic["dram_bytes_per_launch"] if traffic else None,

@@ -196,9 +196,10 @@ int tw_stage_advance(tw_ctx* ctx, int32_t nv, const double* inv_mass, const doub
  * x0 -> x1 (nv * 3 doubles each): the number of vertex-triangle and edge-edge
  * stencils whose motion crosses (*violations) and how many of those are
  * certain (*certain, away from the numerical margins). Zero violations
- * certify the segment intersection-free. Runs on the device. */
+ * certify the segment intersection-free. *candidates (nullable): swept-box
+ * candidate stencils tested. Runs on the device. */
 int tw_ccd_certify(tw_ctx* ctx, tw_mesh* mesh, const double* x0, const double* x1, int32_t* violations,
-                   int32_t* certain);
+                   int32_t* certain, int64_t* candidates);
 
 #ifdef __cplusplus
 }

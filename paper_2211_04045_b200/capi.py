@@ -97,7 +97,7 @@ def lib():
         L.tw_stage_search.argtypes = [P, P, P, C.c_double, C.c_int64, P, P, P, P, P, P, P]
         L.tw_stage_refresh.argtypes = [P, P, P, C.c_double, C.c_int64, P, P, P, P, P, P, P]
         L.tw_stage_advance.argtypes = [P, C.c_int32, P, P, P, C.c_double, P, P, P]
-        L.tw_ccd_certify.argtypes = [P, P, P, P, P, P]
+        L.tw_ccd_certify.argtypes = [P, P, P, P, P, P, P]
         L.tw_stage_linearize.argtypes = [P, P, P, C.c_int64, P, P, P, P, P, P, P, C.c_double, C.c_double,
                                          C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P, P, P]
         L.tw_stage_color.argtypes = [P, P, C.c_int64, P, P, P, P, C.c_uint64, C.c_int32, C.c_int32, P, P]
@@ -404,14 +404,14 @@ def backward(ctx: Context, inv_mass, rows: Rows, colors, ncolors, x, y, lam=None
     return {"lambda": lam, "q": q[:n], "y": yo}
 
 
-def ccd_certify(ctx: Context, mesh: Mesh, x0, x1):
+def ccd_certify(ctx: Context, mesh: Mesh, x0, x1, candidates=False):
     """ccd_certify (testkit/ccd.cpp) of the segment x0 -> x1 on the device:
-    (violations, certain)."""
+    (violations, certain) [, candidate stencils tested]."""
     x0 = np.ascontiguousarray(x0, np.float64).reshape(-1, 3)
     x1 = np.ascontiguousarray(x1, np.float64).reshape(-1, 3)
-    v, c = C.c_int32(0), C.c_int32(0)
-    ctx.check(lib().tw_ccd_certify(ctx.h, mesh.h, _p(x0), _p(x1), C.byref(v), C.byref(c)))
-    return v.value, c.value
+    v, c, n = C.c_int32(0), C.c_int32(0), C.c_int64(0)
+    ctx.check(lib().tw_ccd_certify(ctx.h, mesh.h, _p(x0), _p(x1), C.byref(v), C.byref(c), C.byref(n)))
+    return (v.value, c.value, n.value) if candidates else (v.value, c.value)
 
 
 def ccd_certify_path(ctx: Context, mesh: Mesh, path):

@@ -1059,7 +1059,7 @@ int tw_stage_advance(tw_ctx* ctx, int32_t nv, const double* inv_mass, const doub
 }
 
 int tw_ccd_certify(tw_ctx* ctx, tw_mesh* m, const double* x0, const double* x1, int32_t* violations,
-                   int32_t* certain) {
+                   int32_t* certain, int64_t* candidates) {
     if (!ctx || !m || !x0 || !x1 || !violations) return fail(ctx, TW_EINVAL, "ccd_certify: bad argument");
     CK(cudaSetDevice(ctx->device));
     tw_resolve_config cfg;
@@ -1094,6 +1094,7 @@ int tw_ccd_certify(tw_ctx* ctx, tw_mesh* m, const double* x0, const double* x1, 
     }
     *violations = G.ccd_violations;
     if (certain) *certain = G.ccd_certain;
+    if (candidates) *candidates = (int64_t)G.ncand;
     return TW_OK;
 }
 
