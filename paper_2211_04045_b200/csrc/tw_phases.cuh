@@ -188,9 +188,10 @@ __device__ void ph_refit(const Params& P) {
                 const int slot = B.child[par].x == node ? 0 : 1;
                 float4* pn = B.node + 4LL * par + 2 * slot;
                 pn[0] = blo, pn[1] = bhi;
-                __threadfence();
-                if (atomicAdd(&B.flag[par], 1u) == 0u) break;
-                __threadfence();
+                // acq_rel arrival: the first child's box is visible to the second
+                unsigned prev;
+                asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&B.flag[par]) : "memory");
+                if (prev == 0u) break;
                 const float4* q = B.node + 4LL * par;
                 const float4 a0 = __ldcg(q), a1 = __ldcg(q + 1), b0 = __ldcg(q + 2), b1 = __ldcg(q + 3);
                 blo = make_float4(fminf(a0.x, b0.x), fminf(a0.y, b0.y), fminf(a0.z, b0.z), __int_as_float(par));
@@ -273,9 +274,25 @@ __device__ __forceinline__ void bitonic64(int& a, int& b, int lane) {
     }
 }
 
+// ascending bitonic sort of 32 ints, one per lane
+__device__ __forceinline__ int bitonic32(int a, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const int pa = __shfl_xor_sync(0xffffffffu, a, j);
+            a = (((lane & k) == 0) == ((lane & j) == 0)) ? min(a, pa) : max(a, pa);
+        }
+    }
+    return a;
+}
+
 // warp-cooperative ascending sort of one query's partner list (n >= 2)
 __device__ __forceinline__ void sort_partners(int* s, int n, int lane) {
-    if (n <= 64) {
+    if (n <= 32) {
+        const int a = bitonic32(lane < n ? s[lane] : 0x7fffffff, lane);
+        if (lane < n) s[lane] = a;
+    } else if (n <= 64) {
         int a = lane < n ? s[lane] : 0x7fffffff;
         int b = lane + 32 < n ? s[lane + 32] : 0x7fffffff;
         bitonic64(a, b, lane);
