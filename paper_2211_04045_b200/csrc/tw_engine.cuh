@@ -185,7 +185,7 @@ struct Params {
     unsigned long long* vmask;  // 4 per vertex
     int* vbig;
     // vertex -> contact-row incidence, CSR rebuilt every step (entry = 4*row + m)
-    int* vcnt;      // entries per vertex (nv)
+    int* vcnt;      // entries per vertex (nv); during the device coloring: the uncolored ones
     int* voff;      // segment offsets (nv + 1)
     int* vinc;      // entries, each segment sorted by entry id (4 * rows)
     int* c_slot;    // slot of each entry in its segment before sorting (4 * rows)

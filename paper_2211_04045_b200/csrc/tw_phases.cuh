@@ -970,6 +970,7 @@ __device__ void ph_warm(const Params& P, long long nc, bool reset_colors = true)
 __device__ void ph_color_rank(const Params& P) {
     const int lane = threadIdx.x & 31;
     for (long long v = gwarp(); v < P.nv; v += gwarps()) {
+        if (P.vcnt[v] == 0) continue;  // no uncolored entry left at v
         const int b = P.voff[v], e = P.voff[v + 1];
         int run = 0;
         for (int t0 = b; t0 < e; t0 += 32) {
@@ -991,8 +992,8 @@ __device__ void ph_color_conflict(const Params& P, int k) {
     __shared__ unsigned long long seen[TPB / 32][4];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (long long v = gwarp(); v < P.nv; v += gwarps()) {
+        if (P.vcnt[v] == 0) continue;  // no uncolored entry left at v (also: empty segment)
         const int b = P.voff[v], e = P.voff[v + 1];
-        if (b == e) continue;
         if (lane < 4) seen[w][lane] = 0ull;
         __syncwarp();
         for (int t0 = b; t0 < e; t0 += 32) {
@@ -1044,6 +1045,7 @@ __device__ void ph_color_commit(const Params& P, long long nc, int k) {
             if (v < 0 || !(P.inv_mass[v] > 0.0)) continue;
             if (ti < 256) atomicOr(&P.vmask[4LL * v + (ti >> 6)], 1ull << (ti & 63));
             else P.vbig[v] = 1;
+            atomicSub(&P.vcnt[v], 1);  // uncolored entries left at v
         }
     }
     const int wn = __reduce_add_sync(0xffffffffu, (unsigned)ncolored);
