@@ -63,7 +63,7 @@ struct tw_ctx {
     int sm_count = 0;
     int nblocks = 0;
     int minb = 4;  // resolve-kernel instance (CTAs per SM)
-    long long pgs_tail_rows = 512;  // TW_PGS_TAIL
+    long long pgs_tail_rows = 256;  // TW_PGS_TAIL
     long long launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk = nullptr;
     // capacities

@@ -1518,7 +1518,9 @@ __device__ __forceinline__ void pgs_color_range(const Params& P, int c, int ncol
 __device__ void ph_pgs_color(const Params& P, int c, int ncol_contact, int ncol_edge) {
     long long c0, nci, e0, n;
     pgs_color_range(P, c, ncol_contact, ncol_edge, &c0, &nci, &e0, &n);
-    for (long long k = gtid(); k < n; k += gstride()) {
+    // rows dealt round-robin over the CTAs (row k -> CTA k mod grid): a small
+    // color spreads over all SMs instead of filling the first few
+    for (long long k = blockIdx.x + (long long)threadIdx.x * gridDim.x; k < n; k += gstride()) {
         if (k < nci) pgs_contact_packed(P, c0 + k);
         else pgs_edge_row(P, P.er_by_color[e0 + (k - nci)]);
     }
