@@ -84,7 +84,7 @@ struct tw_ctx {
     DevMem ccount, coff;
     DevMem arch_key0, arch_key1, arch_val0, arch_val1, new_lb, new_key, new_val;
     DevMem refpool;
-    DevMem part_q, part_c, part_k, blk_lo, blk_hi;
+    DevMem part_q, part_c, part_k;
     DevMem globals, box, bvh_tmp, smd, trace, path;
     // stage scratch
     DevMem s_kinds, s_verts, s_out, s_has;
@@ -259,10 +259,8 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     }
     const size_t nb = (size_t)ctx->nblocks;
     CK(ctx->part_q.ensure(nb * 8));
-    CK(ctx->part_c.ensure(nb * 8));
+    CK(ctx->part_c.ensure(((size_t)P / 4096 + 2) * 8));  // per pair tile (PAIR_TILE = TPB * 16)
     CK(ctx->part_k.ensure(nb * 8));
-    CK(ctx->blk_lo.ensure(nb * 8));
-    CK(ctx->blk_hi.ensure(nb * 8));
     CK(ctx->globals.ensure(sizeof(Globals)));
     CK(ctx->box.ensure(64));
     CK(ctx->smd.ensure((size_t)cfg.step_limit * 8));
@@ -379,8 +377,6 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.part_q = ctx->part_q.as<long long>();
     P.part_c = ctx->part_c.as<long long>();
     P.part_k = ctx->part_k.as<long long>();
-    P.blk_lo = ctx->blk_lo.as<long long>();
-    P.blk_hi = ctx->blk_hi.as<long long>();
     P.g = ctx->globals.as<Globals>();
     P.step_max_disp = ctx->smd.as<double>();
     P.path = c.record_path ? ctx->path.as<double>() : nullptr;
@@ -593,7 +589,7 @@ void tw_ctx_destroy(tw_ctx* ctx) {
                      &ctx->c_lost, &ctx->vmask, &ctx->vbig, &ctx->pk_ids, &ctx->pk_jac, &ctx->pk_q, &ctx->pk_diag, &ctx->pk_lam,
                      &ctx->c_by_color, &ctx->ccount, &ctx->coff, &ctx->arch_key0, &ctx->arch_key1,
                      &ctx->arch_val0, &ctx->arch_val1, &ctx->new_lb, &ctx->new_key, &ctx->new_val, &ctx->refpool,
-                     &ctx->part_q, &ctx->part_c, &ctx->part_k, &ctx->blk_lo, &ctx->blk_hi, &ctx->globals, &ctx->box,
+                     &ctx->part_q, &ctx->part_c, &ctx->part_k, &ctx->globals, &ctx->box,
                      &ctx->bvh_tmp, &ctx->smd, &ctx->trace, &ctx->path, &ctx->s_kinds, &ctx->s_verts, &ctx->s_out,
                      &ctx->s_has};
     for (DevMem* d : all) d->release();

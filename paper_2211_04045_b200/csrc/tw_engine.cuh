@@ -213,11 +213,9 @@ struct Params {
     // per block scratch
     int nblocks;
     long long* part_q;
-    long long* part_c;
+    long long* part_c;  // contact pairs per pair tile (for_pair_tiles)
     long long* part_k;
     long long* part_v;
-    long long* blk_lo;  // per block pair range
-    long long* blk_hi;
     // globals + outputs
     Globals* g;
     double* step_max_disp;

@@ -498,27 +498,16 @@ __global__ void k_stage_advance(Params P, double* max_disp) {
 // carry active / all_static), block totals for the compaction of ph_rows
 __device__ void ph_stage_contact_flags(const Params& P) {
     const long long np = P.g->np;
-    long long lo, hi;
-    chunk_of(np, &lo, &hi);
-    long long ncontact = 0;
-    for (long long p = lo + threadIdx.x; p < hi; p += TPB) {
+    for_pair_tiles(P, np, [&](long long p) -> bool {
         const uint64_t key = P.pkey[p];
         const int ka = key_ka(key), kb = key_kb(key);
         int va[3], vb[3];
         split_ids(ka, kb, P.pids[p], va, vb);
         uint8_t fl = P.pflag[p] & (PF_ACTIVE | PF_ALL_STATIC | PF_DEGENERATE);
-        if (contact_pred(P, ka, kb, va, vb, P.pdd[p], P.pw[p], fl)) {
-            fl |= PF_CONTACT;
-            ++ncontact;
-        }
+        if (contact_pred(P, ka, kb, va, vb, P.pdd[p], P.pw[p], fl)) fl |= PF_CONTACT;
         P.pflag[p] = fl;
-    }
-    const long long nct = block_sum(ncontact);
-    if (threadIdx.x == 0) {
-        P.part_c[blockIdx.x] = nct;
-        P.blk_lo[blockIdx.x] = lo;
-        P.blk_hi[blockIdx.x] = hi;
-    }
+        return (fl & PF_CONTACT) != 0;
+    });
 }
 
 // vertex -> row incidence of uploaded rows (dynamic vertices only)

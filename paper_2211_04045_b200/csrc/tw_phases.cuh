@@ -111,8 +111,28 @@ __device__ __forceinline__ void chunk_of(long long n, long long* lo, long long* 
     *hi = min(n, *lo + c);
 }
 
+// Pair passes that feed the row compaction run over tiles of PAIR_TILE
+// consecutive pairs dealt round-robin to the CTAs (the contact pairs cluster
+// where the knot is tight; contiguous chunks would leave that work to a few
+// CTAs). body(p) returns whether pair p is a contact pair; per-tile counts go
+// to part_c[tile] for ph_rows.
+constexpr long long PAIR_TILE = (long long)TPB * 16;
+__device__ __forceinline__ long long pair_tiles(long long np) { return (np + PAIR_TILE - 1) / PAIR_TILE; }
+
 __device__ __forceinline__ long long gtid() { return (long long)blockIdx.x * TPB + threadIdx.x; }
 __device__ __forceinline__ long long gstride() { return (long long)gridDim.x * TPB; }
+
+template <typename F>
+__device__ __forceinline__ void for_pair_tiles(const Params& P, long long np, F&& body) {
+    const long long ntile = pair_tiles(np);
+    for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+        const long long lo = tile * PAIR_TILE, hi = min(np, lo + PAIR_TILE);
+        long long c = 0;
+        for (long long p = lo + threadIdx.x; p < hi; p += TPB) c += body(p) ? 1 : 0;
+        const long long t = block_sum(c);
+        if (threadIdx.x == 0) P.part_c[tile] = t;
+    }
+}
 __device__ __forceinline__ long long gwarp() { return gtid() >> 5; }
 __device__ __forceinline__ long long gwarps() { return gstride() >> 5; }
 
@@ -551,11 +571,8 @@ __device__ void ph_emit_pairs(const Params& P) {
 // [b P / nb, (b+1) P / nb), each decoded from its key.
 __device__ void ph_emit_records(const Params& P, bool first_search) {
     const long long np = P.g->np;
-    long long lo, hi;
-    chunk_of(np, &lo, &hi);
-    long long ncontact = 0;
     int touching = 0;
-    for (long long p = lo + threadIdx.x; p < hi; p += TPB) {
+    for_pair_tiles(P, np, [&](long long p) -> bool {
         const uint64_t key = P.pkey[p];
         const int ka = key_ka(key), kb = key_kb(key), ia = key_ia(key), ib = key_ib(key);
         int va[3], vb[3];
@@ -570,10 +587,7 @@ __device__ void ph_emit_records(const Params& P, bool first_search) {
         uint8_t fl = PF_ACTIVE | (all_static ? PF_ALL_STATIC : 0) | (c.degenerate ? PF_DEGENERATE : 0);
         const double4 dd = make_double4(c.dir.x, c.dir.y, c.dir.z, c.dist);
         const double4 w = pack_weights(ka, kb, c);
-        if (contact_pred(P, ka, kb, va, vb, dd, w, fl)) {
-            fl |= PF_CONTACT;
-            ++ncontact;
-        }
+        if (contact_pred(P, ka, kb, va, vb, dd, w, fl)) fl |= PF_CONTACT;
         P.pids[p] = ids;
         P.pdd[p] = dd;
         if (P.pw_all || (fl & PF_CONTACT)) P.pw[p] = w;  // weights are read for contact rows only
@@ -581,15 +595,10 @@ __device__ void ph_emit_records(const Params& P, bool first_search) {
         for (int k = 0; k <= ka; ++k) vertex_min(P, va[k], c.dist);
         for (int k = 0; k <= kb; ++k) vertex_min(P, vb[k], c.dist);
         if (first_search && c.dist < 1e-10) touching = 1;
-    }
-    const long long nct = block_sum(ncontact);
+        return (fl & PF_CONTACT) != 0;
+    });
     const long long touch = block_sum(touching);
-    if (threadIdx.x == 0) {
-        P.part_c[blockIdx.x] = nct;
-        P.blk_lo[blockIdx.x] = lo;
-        P.blk_hi[blockIdx.x] = hi;
-        if (touch) P.g->start_in_contact = 1;
-    }
+    if (threadIdx.x == 0 && touch) P.g->start_in_contact = 1;
 }
 
 // ============================================================== archive
@@ -652,22 +661,24 @@ __device__ __forceinline__ d3 edge_jac(const double4& g4, int m) {
 // q = c + J (y_k1 - x), warm-start multiplier from the archive, vertex
 // incidence lists; plus every edge row's value / jacobian / diag / q.
 __device__ void ph_rows(const Params& P) {
-    const long long lo = P.blk_lo[blockIdx.x], hi = P.blk_hi[blockIdx.x];
-    const long long nc_total = prefix_of(P.part_c, gridDim.x);
-    long long base = prefix_of(P.part_c, blockIdx.x);
-    // pass 1: the contact pairs in pair order (= row order). Each thread scans
-    // 16 consecutive pairs per tile (one block scan per 4096 pairs) and
-    // records the pair of each row (c_arch holds it until ph_rows_build).
+    const long long np = P.g->np, ntile = pair_tiles(np);
+    const long long nc_total = prefix_of(P.part_c, (int)ntile);
+    // pass 1: the contact pairs in pair order (= row order), tile by tile (the
+    // tiles of the contact-flag pass): each thread scans 16 consecutive
+    // pairs, one block scan per tile, and records the pair of each row
+    // (c_arch holds it until ph_rows_build).
     constexpr int PER = 16;
-    for (long long t = lo; t < hi; t += (long long)TPB * PER) {
-        const long long p0 = t + (long long)threadIdx.x * PER;
+    static_assert(PAIR_TILE == (long long)TPB * PER, "one scan per pair tile");
+    for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+        const long long base = prefix_of(P.part_c, (int)tile);
+        const long long lo = tile * PAIR_TILE, hi = min(np, lo + PAIR_TILE);
+        const long long p0 = lo + (long long)threadIdx.x * PER;
         unsigned fm = 0;
 #pragma unroll
         for (int j = 0; j < PER; ++j)
             if (p0 + j < hi && (P.pflag[p0 + j] & PF_CONTACT)) fm |= 1u << j;
         long long tile_tot;
         long long pos = base + block_scan(__popc(fm), &tile_tot);
-        base += tile_tot;
         while (fm) {
             P.c_arch[pos++] = p0 + (__ffs(fm) - 1);
             fm &= fm - 1;
@@ -1748,10 +1759,9 @@ __device__ void ph_arch_merge(const Params& P, long long nnew, int sel, long lon
 // the multipliers of inactive pairs runs from the archive side (ph_arch_erase).
 __device__ void ph_refresh(const Params& P, double bound, bool next_search) {
     const long long np = P.g->np;
-    long long lo, hi;
-    chunk_of(np, &lo, &hi);
-    long long ncontact = 0, nact = 0;
-    for (long long p = lo + threadIdx.x; p < hi; p += TPB) {
+    long long nact = 0, nev = 0;
+    for_pair_tiles(P, np, [&](long long p) -> bool {
+        ++nev;
         const uint64_t key = P.pkey[p];
         const int ka = key_ka(key), kb = key_kb(key);
         int va[3], vb[3];
@@ -1785,23 +1795,17 @@ __device__ void ph_refresh(const Params& P, double bound, bool next_search) {
                 for (int k = 0; k <= kb; ++k) vertex_min(P, vb[k], dd.w);
             }
         }
-        if (!next_search && contact_pred(P, ka, kb, va, vb, dd, w, fl)) {
-            fl |= PF_CONTACT;
-            ++ncontact;
-        }
+        if (!next_search && contact_pred(P, ka, kb, va, vb, dd, w, fl)) fl |= PF_CONTACT;
         // weights are read for contact rows only (ph_rows_build); the stage
         // entries return them for every pair
         if (h == 1 && (P.pw_all || (fl & PF_CONTACT))) P.pw[p] = w;
         P.pflag[p] = fl;
-    }
-    const long long nct = block_sum(ncontact);
-    const long long na = block_sum(nact);
+        return (fl & PF_CONTACT) != 0;
+    });
+    const long long na = block_sum(nact), ev = block_sum(nev);
     if (threadIdx.x == 0) {
-        P.part_c[blockIdx.x] = nct;
-        P.blk_lo[blockIdx.x] = lo;
-        P.blk_hi[blockIdx.x] = hi;
         atomicAdd(&P.g->nactive, (int)na);
-        atomicAdd((unsigned long long*)&P.g->pairs_evaluated, (unsigned long long)(hi - lo));
+        atomicAdd((unsigned long long*)&P.g->pairs_evaluated, (unsigned long long)ev);
     }
 }
 
