@@ -373,7 +373,6 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.nblocks = ctx->nblocks;
     P.pgs_tail_rows = ctx->pgs_tail_rows;
     P.pw_all = 1;
-    P.experiment = std::getenv("TW_EXPERIMENT") ? std::atoi(std::getenv("TW_EXPERIMENT")) : 0;
     P.part_q = ctx->part_q.as<long long>();
     P.part_c = ctx->part_c.as<long long>();
     P.part_k = ctx->part_k.as<long long>();

@@ -1,5 +1,4 @@
-"""Phase profile of one bow-knot resolve for experiments (TW_EXPERIMENT=1
-skips the exact candidate test: traversal walk cost only; results invalid)."""
+"""Phase profile of one bow-knot resolve (per-phase ms and call counts)."""
 import os
 import sys
 
@@ -12,7 +11,7 @@ m = capi.Mesh.from_scene(ctx, sc)
 for i in range(3):
     x, st = capi.resolve(ctx, m, sc.x, sc.y, delta=5e-4)
 prof = capi.phase_profile(ctx)
-print(f"experiment={os.environ.get('TW_EXPERIMENT', '0')} kernel_ms {st['kernel_ms']:.3f} "
+print(f"kernel_ms {st['kernel_ms']:.3f} "
       f"steps {st['steps']} searches {st['searches']}")
 for k, (ms, n) in prof.items():
     print(f"  {k:20s} {ms:7.3f} ms total, {ms / n:.4f} ms per call ({n} calls)")
