@@ -103,6 +103,10 @@ struct tw_mesh {
     DevMem d_inv_mass, d_edges, d_tris, d_iso, d_vedge_off, d_vedge, d_edge_color;
     int edge_ncolors = 0;
     BvhMem bvh[3];
+    // broad-phase query order (Morton vertex order + per-class choice), fixed
+    // at the first call on this mesh: it only steers performance
+    DevMem vperm, qspread, eperm;
+    bool qorder_ready = false;
 };
 
 namespace {
@@ -266,8 +270,9 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     CK(ctx->smd.ensure((size_t)cfg.step_limit * 8));
     CK(ctx->trace.ensure((size_t)cfg.step_limit * sizeof(Trace)));
     if (cfg.record_path) CK(ctx->path.ensure(((size_t)cfg.step_limit + 1) * nv * 24));
-    size_t tb = 0;
+    size_t tb = bvh_tmp_bytes(m->nv);  // the vertex order sorts nv codes
     for (int c = 0; c < 3; ++c) tb = std::max(tb, bvh_tmp_bytes(m->bvh[c].n));
+
     CK(ctx->bvh_tmp.ensure(tb));
     return TW_OK;
 }
@@ -301,6 +306,9 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.edge_color = m->d_edge_color.as<int>();
     P.edge_ncolors = m->edge_ncolors;
     for (int k = 0; k < 3; ++k) P.bvh[k] = m->bvh[k].view();
+    P.vperm = m->vperm.as<int>();
+    P.qspread = m->qspread.as<double>();
+    P.eperm = m->eperm.as<int>();
     P.x = ctx->x.as<double4>();
     P.yk1 = ctx->yk1.as<double4>();
     P.r = ctx->r.as<double>();
@@ -396,6 +404,23 @@ int build_bvhs(tw_ctx* ctx, tw_mesh* m) {
                          m->d_iso.as<int>(), ctx->x.as<double4>(), m->nv, ctx->bvh_tmp.p, ctx->bvh_tmp.bytes,
                          ctx->box.as<unsigned long long>());
         ctx->launches += launch_count_last();
+    }
+    if (!m->qorder_ready) {
+        // Morton vertex order and edge order (the edge leaf order of this first
+        // build), and which order makes the more compact query packets
+        launch_vertex_order(ctx->stream, m->nv, ctx->x.as<double4>(), ctx->bvh_tmp.p, ctx->bvh_tmp.bytes,
+                            ctx->box.as<unsigned long long>(), m->vperm.as<int>());
+        ctx->launches += launch_count_last();
+        if (m->ne)
+            CK(cudaMemcpyAsync(m->eperm.p, m->bvh[1].prim.p, (size_t)m->ne * 4, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+        CK(cudaMemsetAsync(m->qspread.p, 0, 32, ctx->stream));
+        launch_packet_spread(ctx->stream, m->nv, 0, nullptr, ctx->x.as<double4>(), m->vperm.as<int>(),
+                             m->qspread.as<double>());
+        launch_packet_spread(ctx->stream, m->ne, 1, m->d_edges.as<int2>(), ctx->x.as<double4>(),
+                             m->eperm.as<int>(), m->qspread.as<double>() + 2);
+        ctx->launches += (m->nv > 0) + (m->ne > 0);
+        m->qorder_ready = true;
     }
     CK(cudaGetLastError());
     return TW_OK;
@@ -685,6 +710,10 @@ int tw_mesh_create(tw_ctx* ctx, int32_t nv, const double* inv_mass, int32_t ne_e
         if (e == cudaSuccess) e = B.flag.ensure(n * 4);
         if (e == cudaSuccess) e = cudaMemsetAsync(B.flag.p, 0, n * 4, s);
     }
+    // broad-phase query order buffers (filled at the mesh's first call)
+    if (e == cudaSuccess) e = m->vperm.ensure((size_t)std::max(1, nv) * 4);
+    if (e == cudaSuccess) e = m->eperm.ensure((size_t)std::max(1, m->ne) * 4);
+    if (e == cudaSuccess) e = m->qspread.ensure(64);
     // device-mode edge-row precoloring (Jones-Plassmann rounds)
     if (e == cudaSuccess) e = m->d_edge_color.ensure((size_t)std::max(1, m->ne) * 4);
     if (e == cudaSuccess && m->ne > 0) {
@@ -744,7 +773,8 @@ void tw_mesh_destroy(tw_mesh* m) {
     if (!m) return;
     cudaSetDevice(m->device);
     cudaDeviceSynchronize();
-    DevMem* all[] = {&m->d_inv_mass, &m->d_edges, &m->d_tris, &m->d_iso, &m->d_vedge_off, &m->d_vedge, &m->d_edge_color};
+    DevMem* all[] = {&m->d_inv_mass, &m->d_edges, &m->d_tris, &m->d_iso, &m->d_vedge_off, &m->d_vedge, &m->d_edge_color,
+                     &m->vperm, &m->eperm, &m->qspread};
     for (DevMem* d : all) d->release();
     for (auto& B : m->bvh) {
         B.prim.release(), B.child.release(), B.parent.release(), B.node.release(), B.flag.release();

@@ -126,6 +126,9 @@ struct Params {
     const int* edge_color;  // device-mode precoloring (-1 both static)
     int edge_ncolors;
     Bvh bvh[3];             // 0 triangles, 1 edges, 2 isolated vertices
+    const int* vperm;       // vertices in Morton order (vertex-query order of the broad phase)
+    const double* qspread;  // packet spreads {vertex: mesh, Morton; edge: mesh, Morton} (k_packet_spread)
+    const int* eperm;       // edges in Morton order (fixed per mesh)
     // ---- vertex state
     double4* x;
     const double4* yk1;

@@ -26,6 +26,11 @@ void launch_bvh_build(cudaStream_t s, int cls, const Bvh& B, const int4* tris, c
                       unsigned long long* box /* 6, device */);
 
 int launch_count_last();  // kernels launched by the last launcher call
+void launch_vertex_order(cudaStream_t s, int nv, const double4* x, void* tmp, size_t tmp_bytes,
+                         unsigned long long* box, int* vperm);
+// packet compactness of a query class in mesh order vs Morton order (spread[0..1], summed)
+void launch_packet_spread(cudaStream_t s, int n, int cls, const int2* edges, const double4* x, const int* perm,
+                          double* spread);
 void launch_bounds(cudaStream_t s, int nv, const double4* x, unsigned long long* box);
 
 // cooperative kernels

@@ -114,8 +114,10 @@ __global__ void k_morton(int n, int cls, const int4* tris, const int2* edges, co
         } else if (cls == 1) {
             const int2 e = edges[i];
             ids[0] = e.x, ids[1] = e.y, k = 2;
-        } else {
+        } else if (cls == 2) {
             ids[0] = iso[i], k = 1;
+        } else {  // 3: the vertices themselves (query order of the broad phase)
+            ids[0] = (int)i, k = 1;
         }
         for (int j = 0; j < k; ++j) {
             const double4 p = x[ids[j]];
@@ -806,6 +808,57 @@ void launch_bvh_build(cudaStream_t s, int cls, const Bvh& B, const int4* tris, c
     k_karras<<<grid_for(n), 256, 0, s>>>(n, codes2, idx2, B.prim, B.child, B.parent, B.flag);
     g_last_launches = 3;
     (void)nv;
+}
+
+// Spread of the 32-query packets of a query class in two orders: the mesh
+// numbering (identity) and Morton order (perm). spread[0] / spread[1] receive
+// the sums over packets of the union-box extents (x + y + z); the broad phase
+// hands out packets in the more compact order (query_at).
+__global__ void k_packet_spread(int n, int cls, const int2* edges, const double4* x, const int* perm,
+                                double* spread) {
+    const int npk = (n + 31) / 32;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 2 * npk; t += gridDim.x * blockDim.x) {
+        const int pk = t >> 1, ord = t & 1;
+        float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+        for (int j = pk * 32; j < min(n, pk * 32 + 32); ++j) {
+            const int q = ord ? perm[j] : j;
+            double c[3];
+            if (cls == 1) {
+                const int2 e = edges[q];
+                const double4 a = x[e.x], b = x[e.y];
+                c[0] = 0.5 * (a.x + b.x), c[1] = 0.5 * (a.y + b.y), c[2] = 0.5 * (a.z + b.z);
+            } else {
+                const double4 a = x[q];
+                c[0] = a.x, c[1] = a.y, c[2] = a.z;
+            }
+            for (int k = 0; k < 3; ++k) lo[k] = fminf(lo[k], (float)c[k]), hi[k] = fmaxf(hi[k], (float)c[k]);
+        }
+        atomicAdd(&spread[ord], (double)((hi[0] - lo[0]) + (hi[1] - lo[1]) + (hi[2] - lo[2])));
+    }
+}
+
+void launch_packet_spread(cudaStream_t s, int n, int cls, const int2* edges, const double4* x, const int* perm,
+                          double* spread) {
+    if (n == 0) return;
+    k_packet_spread<<<grid_for((n + 31) / 16), 256, 0, s>>>(n, cls, edges, x, perm, spread);
+}
+
+// vertices in Morton order: the order the broad phase hands vertex queries to
+// warps (32 spatially compact queries per packet whatever the mesh numbering)
+void launch_vertex_order(cudaStream_t s, int nv, const double4* x, void* tmp, size_t tmp_bytes,
+                         unsigned long long* box, int* vperm) {
+    g_last_launches = 0;
+    if (nv == 0) return;
+    const size_t arr = ((size_t)nv * 4 + 255) & ~(size_t)255;
+    char* base = (char*)tmp;
+    unsigned* codes = (unsigned*)base;
+    unsigned* codes2 = (unsigned*)(base + arr);
+    int* idx = (int*)(base + 2 * arr);
+    void* cub_tmp = base + 4 * arr;
+    size_t cub_bytes = tmp_bytes - 4 * arr - 256;
+    k_morton<<<grid_for(nv), 256, 0, s>>>(nv, 3, nullptr, nullptr, nullptr, x, box, codes, idx);
+    cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, codes, codes2, idx, vperm, nv, 0, 30, s);
+    g_last_launches = 2;
 }
 
 void launch_bounds(cudaStream_t s, int nv, const double4* x, unsigned long long* box) {

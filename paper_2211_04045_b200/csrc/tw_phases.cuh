@@ -248,6 +248,26 @@ __device__ __forceinline__ long long num_queries(const Params& P) {
     return 2 * pad32(P.niso) + pad32(P.nv) + pad32(P.ne);
 }
 
+// The query handed out at packet position pos. Isolated vertices go in Morton
+// order (the leaf order of their hierarchy). Vertices and edges go in mesh
+// order or Morton order (P.vperm / P.eperm), whichever makes the 32 queries
+// of a warp packet more compact (k_packet_spread, at the mesh's first call):
+// strip meshes numbered row by row are compact as they are, arbitrary
+// numberings are not. Padding positions map to themselves.
+__device__ __forceinline__ long long query_at(const Params& P, long long pos) {
+    const long long niso = P.niso, s1 = pad32(niso), s2 = 2 * s1, s3 = s2 + pad32(P.nv);
+    if (pos < s1) return pos < niso ? P.bvh[2].prim[pos] : pos;
+    if (pos < s2) return s1 + (pos - s1 < niso ? P.bvh[2].prim[pos - s1] : pos - s1);
+    if (pos < s3) {
+        const long long j = pos - s2;
+        const bool morton = P.qspread[1] < 0.9 * P.qspread[0];
+        return s2 + (j < P.nv && morton ? P.vperm[j] : j);
+    }
+    const long long j = pos - s3;
+    const bool morton = P.qspread[3] < 0.9 * P.qspread[2];
+    return s3 + (j < P.ne && morton ? P.eperm[j] : j);
+}
+
 __device__ __forceinline__ void simplex_ids(const Params& P, int k, int idx, int* v) {
     v[0] = v[1] = v[2] = -1;
     if (k == KV) {
@@ -350,7 +370,7 @@ __device__ void ph_traverse(const Params& P) {
         if (lane == 0) base = (long long)atomicAdd(&P.g->work_q, 32ull);
         base = __shfl_sync(0xffffffffu, base, 0);
         if (base >= nq) break;
-        const long long q = base + lane;  // nq is a multiple of 32
+        const long long q = query_at(P, base + lane);  // nq is a multiple of 32
         int ka, ia, kb, cls;
         query_of(P, q, &ka, &ia, &kb, &cls);  // ka, kb, cls are warp-uniform
         const Bvh& B = P.bvh[cls];
@@ -393,7 +413,7 @@ __device__ void ph_traverse(const Params& P) {
                 gb = __shfl_sync(0xffffffffu, gb, 0);
                 if (lane < take && (long long)(gb + lane) < P.ccap) {
                     const int2 e = cq[warp][qn - take + lane];
-                    P.cand[gb + lane] = make_int2((int)(base + e.x), e.y);
+                    P.cand[gb + lane] = e;
                 }
                 if (lane == 0 && (long long)(gb + take) > P.ccap) atomicOr(&P.g->error, ERR_CAP_CAND);
                 qn -= take;
@@ -403,7 +423,7 @@ __device__ void ph_traverse(const Params& P) {
         auto leaf = [&](bool hit, int ib) {
             const bool take = hit && !(ordered && ib <= ia);
             const unsigned m = __ballot_sync(0xffffffffu, take);
-            if (take) cq[warp][qn + __popc(m & lt)] = make_int2(lane, ib);
+            if (take) cq[warp][qn + __popc(m & lt)] = make_int2((int)q, ib);
             qn += __popc(m);
             __syncwarp();
             if (qn >= 32) flush(false);
