@@ -197,14 +197,15 @@ class Mesh:
             pass
 
 
-def resolve(ctx: Context, mesh: Mesh, x, y, trace=False, **kw):
-    """resolve(x_start, y_target, mesh, cfg) on the device. Returns (x_out, stats dict)."""
+def resolve(ctx: Context, mesh: Mesh, x, y, trace=False, out=None, **kw):
+    """resolve(x_start, y_target, mesh, cfg) on the device. Returns (x_out, stats dict).
+    out: optional (nv, 3) float64 result buffer (e.g. pinned host memory)."""
     cfg = make_config(**kw)
     x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
     y = np.ascontiguousarray(y, np.float64).reshape(-1, 3)
     if len(x) != mesh.nv or len(y) != mesh.nv:
         raise ValueError("resolve: position arrays do not match mesh")
-    xo = np.zeros_like(x)
+    xo = np.zeros_like(x) if out is None else out
     st = Stats()
     smd = np.zeros(max(1, cfg.step_limit))
     path = np.zeros((cfg.step_limit + 1, mesh.nv, 3)) if cfg.record_path else None

@@ -427,8 +427,11 @@ int build_bvhs(tw_ctx* ctx, tw_mesh* m) {
 }
 
 // Runs one resolve on inputs already in ctx->xs / ctx->ys (device, N x 3).
+// host_out (nullable): the result is also copied to this host buffer, enqueued
+// behind the kernel so that one stream synchronization covers the call
 int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys, const tw_resolve_config& cfg,
-                double* d_out, tw_resolve_stats* st, double* smd_host, double* path_host, tw_step_trace* trace_host) {
+                double* d_out, tw_resolve_stats* st, double* smd_host, double* path_host, tw_step_trace* trace_host,
+                double* host_out = nullptr) {
     Globals G;
     int retries = 0;
     float dev_ms = 0.f, kern_ms = 0.f;
@@ -456,6 +459,18 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
         CK(coop_resolve(ctx->stream, P, ctx->nblocks, ctx->minb));
         ctx->launches += 1;
         CK(cudaEventRecord(ctx->ev1, ctx->stream));
+        // the result (re-enqueued by a capacity retry) ahead of the globals read-back
+        launch_pack(ctx->stream, m->nv, ctx->x.as<double4>(), d_out);
+        ctx->launches += launch_count_last();
+        if (host_out && m->nv)
+            CK(cudaMemcpyAsync(host_out, d_out, (size_t)m->nv * 24, cudaMemcpyDeviceToHost, ctx->stream));
+        if (smd_host)
+            CK(cudaMemcpyAsync(smd_host, ctx->smd.p, (size_t)cfg.step_limit * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (trace_host) {
+            static_assert(sizeof(Trace) == sizeof(tw_step_trace), "trace layout");
+            CK(cudaMemcpyAsync(trace_host, ctx->trace.p, (size_t)cfg.step_limit * sizeof(Trace),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+        }
         CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof(Globals), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         CK(cudaEventElapsedTime(&dev_ms, ctx->ev0, ctx->ev1));
@@ -479,8 +494,6 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
         if (G.error & ERR_CAP_REFPOOL) ctx->refpool_cap *= 4;
     }
     ctx->last = G;
-    launch_pack(ctx->stream, m->nv, ctx->x.as<double4>(), d_out);
-    ctx->launches += launch_count_last();
     std::memset(st, 0, sizeof *st);
     st->steps = G.steps;
     st->searches = G.searches;
@@ -498,13 +511,6 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
     st->setup_ms = dev_ms - kern_ms;
     st->retries = retries;
     st->kernel_launches = (int32_t)(ctx->launches - launches0);
-    if (smd_host && G.steps > 0)
-        CK(cudaMemcpyAsync(smd_host, ctx->smd.p, (size_t)G.steps * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    if (trace_host && G.steps > 0) {
-        static_assert(sizeof(Trace) == sizeof(tw_step_trace), "trace layout");
-        CK(cudaMemcpyAsync(trace_host, ctx->trace.p, (size_t)G.steps * sizeof(Trace), cudaMemcpyDeviceToHost,
-                           ctx->stream));
-    }
     if (path_host && cfg.record_path)
         CK(cudaMemcpyAsync(path_host, ctx->path.p, ((size_t)G.steps + 1) * m->nv * 24, cudaMemcpyDeviceToHost,
                            ctx->stream));
@@ -798,10 +804,9 @@ int tw_resolve(tw_ctx* ctx, tw_mesh* m, const double* x_start, const double* y_t
     }
     tw_resolve_stats st;
     rc = run_resolve(ctx, m, ctx->xs.as<double>(), ctx->ys.as<double>(), *cfg, ctx->xo.as<double>(), &st,
-                     step_max_disp, cfg->record_path ? path : nullptr, trace);
+                     step_max_disp, cfg->record_path ? path : nullptr, trace, x_out);
     if (rc) return rc;
-    if (bytes) CK(cudaMemcpyAsync(x_out, ctx->xo.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    if (cfg->record_path && path) CK(cudaStreamSynchronize(ctx->stream));
     st.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (stats) *stats = st;
     return TW_OK;
