@@ -155,6 +155,35 @@ def bytes_per_resolve(trace, sc, sweeps=1):
     return total
 
 
+def peaks_gbs():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(p)).get("hbm_gbs", 6650.0) if os.path.exists(p) else 6650.0
+
+
+def phase_roofline(trace, sc, phases, peak):
+    """Achieved algorithmic GB/s of the main phases of one resolve (same
+    per-unit bytes as bytes_per_resolve, phase times from the kernel's own
+    phase profile), and their fraction of the HBM peak."""
+    nv = sc.nv
+    rows = [(t["num_contact_rows"], t["num_edge_rows"]) for t in trace]
+    refreshed = sum(t["num_pairs"] for i, t in enumerate(trace) if i + 1 < len(trace) and not trace[i + 1]["searched"])
+    searched = sum(t["num_pairs"] for t in trace if t["searched"])
+    units = {
+        "ph_refresh": 98 * refreshed,
+        "ph_emit_records": 98 * searched,
+        "ph_pgs_color+ph_pgs_tail": sum(336 * c + 184 * e for c, e in rows),
+        "ph_rows+ph_rows_build": sum(210 * c + 88 * e for c, e in rows),
+        "ph_advance": 128 * nv * len(trace),
+    }
+    out = {}
+    for name, b in units.items():
+        ms = sum(phases.get(k, [0.0])[0] for k in name.split("+"))
+        if ms > 0:
+            gbs = b / (ms / 1e3) / 1e9
+            out[name] = {"bytes": b, "ms": round(ms, 4), "gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    return out
+
+
 def max_over_ranks(vals, dist, device):
     """Elementwise max over ranks of per-rank timings (ms); identity at N = 1."""
     import torch
@@ -214,6 +243,7 @@ def run_ours(args):
     algo_bytes = bytes_per_resolve(st_tr["trace"], sc)
     capi.resolve_device_ptr(ctx, mesh, d_x.data_ptr(), d_y.data_ptr(), d_out.data_ptr(), **kw)
     phases = {k: [round(v[0], 3), v[1]] for k, v in capi.phase_profile(ctx).items()}  # untraced call
+    phase_roof = phase_roofline(st_tr["trace"], sc, phases, peaks_gbs())
 
     # ---- device-resident throughput (inputs already in HBM)
     barrier()
@@ -290,6 +320,7 @@ def run_ours(args):
                         "final_pairs": st["num_pairs"], "pairs_evaluated_per_call": pairs_eval / args.steps,
                         "kernel_ms": round(kern_avg_ms, 4), "setup_ms": round(st["setup_ms"], 4),
                         "phase_ms_count": phases,
+                        "phase_roofline": phase_roof,
                         "two_way_steps_per_s": round(world * steps_sum / (dev_ms_max / 1e3), 1),
                         "ccd_pairs_per_s": round(world * pairs_eval / (dev_ms_max / 1e3), 1)},
             "e2e": {"value": round(e2e_value, 3), "unit": "steps/s", "h2d_bytes_per_step": 2 * sc.nv * 24,
