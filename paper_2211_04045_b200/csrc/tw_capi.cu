@@ -581,6 +581,10 @@ int tw_ctx_create(int device, void* stream, tw_ctx** out) {
     if (const char* s = std::getenv("TW_BLOCKS_PER_SM")) want = std::min(4, std::max(2, std::atoi(s)));
     ctx->minb = want;
     if (const char* s = std::getenv("TW_PGS_TAIL")) ctx->pgs_tail_rows = std::max(0LL, std::atoll(s));
+    if (std::getenv("TW_TINY_CAPS")) {  // start every capacity tiny: exercises the grow-and-rerun paths
+        ctx->pcap = 256, ctx->ccap = 256, ctx->K = 4, ctx->arch_cap = 16, ctx->refpool_cap = 1024;
+        ctx->colcap = 8;
+    }
     const int per_sm = std::max(1, std::min(resolve_blocks_per_sm(want), want));
     ctx->nblocks = std::min(ctx->sm_count * per_sm, tw::MAX_BLOCKS);
     if (stream) {

@@ -1,0 +1,56 @@
+"""Capacity growth: a context whose pair, candidate, partner-slot, archive,
+color and reference-coloring capacities all start tiny (TW_TINY_CAPS) must
+grow them by device-flagged overflow + rerun and return exactly what a
+normally sized context returns."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2211_04045_b200 import capi, scenes as S
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def normal():
+    c = capi.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.fixture
+def ctxs(normal):
+    os.environ["TW_TINY_CAPS"] = "1"  # read at context creation: a fresh tiny context per test
+    try:
+        tiny = capi.Context(0)
+    finally:
+        del os.environ["TW_TINY_CAPS"]
+    yield normal, tiny
+    tiny.close()
+
+
+CASES = [(sc, {}) for sc in S.scene_fixtures(0)[:6]] + [(S.reef_knot(), dict(delta=5e-4))]
+
+
+@pytest.mark.parametrize("mode", ["device", "reference"])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: c[0].name)
+def test_tiny_capacities_grow_to_identical_results(ctxs, case, mode):
+    sc, kw = case
+    if mode == "reference" and sc.nv > 10000:
+        pytest.skip("reference coloring replays on one thread: fixture sizes only")
+    normal, tiny = ctxs
+    mn, mt = capi.Mesh.from_scene(normal, sc), capi.Mesh.from_scene(tiny, sc)
+    xn, sn = capi.resolve(normal, mn, sc.x, sc.y, coloring_mode=mode, **kw)
+    xt, stt = capi.resolve(tiny, mt, sc.x, sc.y, coloring_mode=mode, **kw)
+    assert np.array_equal(_bits(xn), _bits(xt))
+    assert (sn["steps"], sn["searches"], sn["num_pairs"]) == (stt["steps"], stt["searches"], stt["num_pairs"])
+    if sn["num_pairs"] > 256:
+        assert stt["retries"] > 0  # the growth path did run
+    # the stage search grows its own way
+    pn, pt = capi.search(normal, mn, sc.y, 4e-3), capi.search(tiny, mt, sc.y, 4e-3)
+    assert np.array_equal(pn.keys, pt.keys) and np.array_equal(_bits(pn.dist), _bits(pt.dist))
