@@ -64,6 +64,7 @@ struct tw_ctx {
     int nblocks = 0;
     int minb = 4;  // resolve-kernel instance (CTAs per SM)
     long long pgs_tail_rows = 256;  // TW_PGS_TAIL
+    int bvh_rebuild = 16;           // TW_BVH_REBUILD: rebuild the LBVH topology every n calls on a mesh
     long long launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk = nullptr;
     // capacities
@@ -107,6 +108,7 @@ struct tw_mesh {
     // at the first call on this mesh: it only steers performance
     DevMem vperm, qspread, eperm;
     bool qorder_ready = false;
+    int bvh_age = -1;  // calls since the hierarchies' topology was built (-1: never)
 };
 
 namespace {
@@ -392,7 +394,20 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     return P;
 }
 
+// The hierarchies' topology (Morton sort + Karras build) is rebuilt from the
+// call's start positions every ctx->bvh_rebuild calls on a mesh; in between
+// the topology of the last build is reused and only refitted (the refit runs
+// at every search in the kernel). Any topology gives the same, exact pair
+// set: the choice only affects how tight the boxes are. The refit arrival
+// counters are cleared every call (an aborted attempt may leave them set).
 int build_bvhs(tw_ctx* ctx, tw_mesh* m) {
+    if (m->bvh_age >= 0 && m->bvh_age + 1 < ctx->bvh_rebuild) {
+        ++m->bvh_age;
+        for (int c = 0; c < 3; ++c)
+            if (m->bvh[c].n > 1) CK(cudaMemsetAsync(m->bvh[c].flag.p, 0, (size_t)(m->bvh[c].n - 1) * 4, ctx->stream));
+        return TW_OK;
+    }
+    m->bvh_age = 0;
     CK(cudaMemsetAsync(ctx->box.p, 0, 64, ctx->stream));
     // lo = ~0 (max), hi = 0
     std::vector<unsigned long long> init = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
@@ -581,6 +596,7 @@ int tw_ctx_create(int device, void* stream, tw_ctx** out) {
     if (const char* s = std::getenv("TW_BLOCKS_PER_SM")) want = std::min(4, std::max(2, std::atoi(s)));
     ctx->minb = want;
     if (const char* s = std::getenv("TW_PGS_TAIL")) ctx->pgs_tail_rows = std::max(0LL, std::atoll(s));
+    if (const char* s = std::getenv("TW_BVH_REBUILD")) ctx->bvh_rebuild = std::max(1, std::atoi(s));
     if (std::getenv("TW_TINY_CAPS")) {  // start every capacity tiny: exercises the grow-and-rerun paths
         ctx->pcap = 256, ctx->ccap = 256, ctx->K = 4, ctx->arch_cap = 16, ctx->refpool_cap = 1024;
         ctx->colcap = 8;
