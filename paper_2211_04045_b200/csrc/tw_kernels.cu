@@ -375,6 +375,9 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
             const int ctail = first_tail_color(P, ncol, ncol_c, ncol_e, P.pgs_tail_rows);
             for (int sw = 0; sw < C.sweeps; ++sw) {
                 for (int c = 0; c < ctail; ++c) {
+                    long long c0, nci, e0, nrow;
+                    pgs_color_range(P, c, ncol_c, ncol_e, &c0, &nci, &e0, &nrow);
+                    if (nrow == 0) continue;  // an unused color: no phase, no barrier
                     ph_pgs_color(P, c, ncol_c, ncol_e);
                     SYNC();
                 }
