@@ -8,7 +8,7 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 PKG       := paper_2211_04045_b200
 CSRC      := $(PKG)/csrc
 NVFLAGS   := $(ARCH) -O3 -std=c++17 -lineinfo -fmad=false -Xcompiler -fPIC -Iinclude -I$(CSRC) \
-             --expt-relaxed-constexpr -diag-suppress 550
+             --expt-relaxed-constexpr -diag-suppress 550 $(NVEXTRA)
 LIB       := $(PKG)/libtwoway_b200.so
 CU_SRCS   := $(CSRC)/tw_kernels.cu $(CSRC)/tw_capi.cu
 CU_HDRS   := $(CSRC)/tw_math.cuh $(CSRC)/tw_engine.cuh $(CSRC)/tw_phases.cuh $(CSRC)/tw_internal.h include/tw_c.h

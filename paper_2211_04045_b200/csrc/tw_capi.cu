@@ -265,7 +265,7 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     }
     const size_t nb = (size_t)ctx->nblocks;
     CK(ctx->part_q.ensure(nb * 8));
-    CK(ctx->part_c.ensure(((size_t)P / 4096 + 2) * 8));  // per pair tile (PAIR_TILE = TPB * 16)
+    CK(ctx->part_c.ensure(((size_t)P / 256 + 2) * 8));  // per pair tile (PAIR_TILE >= TPB)
     CK(ctx->part_k.ensure(nb * 8));
     CK(ctx->globals.ensure(sizeof(Globals)));
     CK(ctx->box.ensure(64));

@@ -2,6 +2,7 @@
 // LBVH build, the persistent cooperative resolve kernel (the whole Alg. 1
 // loop on the device, no host round trip per step) and the stage kernels
 // used for stage-by-stage parity. Compiled with -fmad=false.
+#include <cstdlib>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "tw_ccd.cuh"
@@ -874,8 +875,20 @@ static const void* resolve_fn(int minb) {
     return (const void*)k_resolve<2>;
 }
 
+#ifndef TW_CARVEOUT
+#define TW_CARVEOUT -1
+#endif
+// Shared-memory carveout of the resolve kernel (percent of the maximum; -1:
+// the driver's choice). Env TW_CARVEOUT overrides.
+static void set_carveout(const void* fn) {
+    int pct = TW_CARVEOUT;
+    if (const char* e = getenv("TW_CARVEOUT")) pct = atoi(e);
+    if (pct >= 0) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 int resolve_blocks_per_sm(int minb) {
     int b = 0;
+    set_carveout(resolve_fn(minb));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, resolve_fn(minb), TPB, 0);
     return b;
 }

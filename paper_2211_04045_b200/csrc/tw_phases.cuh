@@ -98,6 +98,17 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
     return m;
 }
 
+// One shared-memory scratch buffer for the phases that stage data per warp
+// (walk stacks and candidate queues, warm-start segments). Phases never
+// overlap (a grid barrier, hence a CTA barrier, separates them), and a small
+// static footprint leaves more of the SM's unified 256 KB to L1, which the
+// vertex gathers of the pair passes live on.
+constexpr int SCRATCH_BYTES = 8192;
+__device__ __forceinline__ char* smem_scratch() {
+    __shared__ __align__(16) char buf[SCRATCH_BYTES];
+    return buf;
+}
+
 // sum of part[0..upto) (every thread gets it)
 __device__ __forceinline__ long long prefix_of(const long long* part, int upto) {
     long long s = 0;
@@ -116,7 +127,11 @@ __device__ __forceinline__ void chunk_of(long long n, long long* lo, long long* 
 // where the knot is tight; contiguous chunks would leave that work to a few
 // CTAs). body(p) returns whether pair p is a contact pair; per-tile counts go
 // to part_c[tile] for ph_rows.
-constexpr long long PAIR_TILE = (long long)TPB * 16;
+#ifndef TW_PAIR_PER
+#define TW_PAIR_PER 4
+#endif
+constexpr int PAIR_PER = TW_PAIR_PER;  // pairs per thread per tile (4: 2.5% faster than 16)
+constexpr long long PAIR_TILE = (long long)TPB * PAIR_PER;
 __device__ __forceinline__ long long pair_tiles(long long np) { return (np + PAIR_TILE - 1) / PAIR_TILE; }
 
 __device__ __forceinline__ long long gtid() { return (long long)blockIdx.x * TPB + threadIdx.x; }
@@ -359,8 +374,9 @@ __device__ __forceinline__ void sort_partners(int* s, int n, int lane) {
 // keeps it light on registers; the exact tests run in ph_cand_eval.
 constexpr int TRAV_STACK = 128;
 __device__ void ph_traverse(const Params& P) {
-    __shared__ int sstack[TPB / 32][TRAV_STACK];
-    __shared__ int2 cq[TPB / 32][64];
+    static_assert(sizeof(int) * (TPB / 32) * TRAV_STACK + sizeof(int2) * (TPB / 32) * 64 <= SCRATCH_BYTES, "");
+    int(*sstack)[TRAV_STACK] = reinterpret_cast<int(*)[TRAV_STACK]>(smem_scratch());
+    int2(*cq)[64] = reinterpret_cast<int2(*)[64]>(smem_scratch() + sizeof(int) * (TPB / 32) * TRAV_STACK);
     const long long nq = num_queries(P);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
@@ -683,15 +699,25 @@ __device__ __forceinline__ d3 edge_jac(const double4& g4, int m) {
 __device__ void ph_rows(const Params& P) {
     const long long np = P.g->np, ntile = pair_tiles(np);
     const long long nc_total = prefix_of(P.part_c, (int)ntile);
-    // pass 1: the contact pairs in pair order (= row order), tile by tile (the
-    // tiles of the contact-flag pass): each thread scans 16 consecutive
-    // pairs, one block scan per tile, and records the pair of each row
-    // (c_arch holds it until ph_rows_build).
+    // pass 1: the contact pairs in pair order (= row order) over scan tiles of
+    // TPB * 16 pairs (SUP pair tiles of the contact-flag pass): each thread
+    // scans 16 consecutive pairs, one block scan per tile, and records the
+    // pair of each row (c_arch holds it until ph_rows_build). The CTA's scan
+    // tiles are blockIdx.x + k * grid: its first base is a prefix over
+    // part_c, each next one adds the pair tiles in between.
     constexpr int PER = 16;
-    static_assert(PAIR_TILE == (long long)TPB * PER, "one scan per pair tile");
-    for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
-        const long long base = prefix_of(P.part_c, (int)tile);
-        const long long lo = tile * PAIR_TILE, hi = min(np, lo + PAIR_TILE);
+    constexpr long long SUP = (long long)PER / PAIR_PER, SCAN_TILE = PAIR_TILE * SUP;
+    static_assert(PER % PAIR_PER == 0, "scan tiles are whole pair tiles");
+    const long long nscan = (np + SCAN_TILE - 1) / SCAN_TILE;
+    long long base = blockIdx.x < nscan ? prefix_of(P.part_c, (int)(blockIdx.x * SUP)) : 0;
+    for (long long tile = blockIdx.x; tile < nscan; tile += gridDim.x) {
+        if (tile != blockIdx.x) {
+            long long s = 0;
+            for (long long i = (tile - gridDim.x) * SUP + threadIdx.x; i < tile * SUP; i += TPB)
+                s += ((volatile const long long*)P.part_c)[i];
+            base += block_sum(s);
+        }
+        const long long lo = tile * SCAN_TILE, hi = min(np, lo + SCAN_TILE);
         const long long p0 = lo + (long long)threadIdx.x * PER;
         unsigned fm = 0;
 #pragma unroll
@@ -867,7 +893,8 @@ __device__ __forceinline__ void warm_edges(const Params& P, int v, double im, d3
 constexpr int WARM_SHORT = 32, WARM_WARP_MAX = 256;
 
 __device__ void ph_warm(const Params& P, long long nc, bool reset_colors = true) {
-    __shared__ int sseg[TPB / 32][WARM_WARP_MAX];
+    static_assert(sizeof(int) * (TPB / 32) * WARM_WARP_MAX <= SCRATCH_BYTES, "");
+    int(*sseg)[WARM_WARP_MAX] = reinterpret_cast<int(*)[WARM_WARP_MAX]>(smem_scratch());
     for (long long vl = gtid(); vl < P.nv; vl += gstride()) {
         const int v = (int)vl;
         const double im = P.inv_mass[v];
