@@ -373,6 +373,9 @@ __device__ __forceinline__ void sort_partners(int* s, int n, int lane) {
 // per warp and written out 32 at a time. The walk holds no FP64 state, which
 // keeps it light on registers; the exact tests run in ph_cand_eval.
 constexpr int TRAV_STACK = 128;
+#ifndef TW_WALK_PAIRS
+#define TW_WALK_PAIRS 1  // two nodes per walk step (four: slower, register pressure)
+#endif
 __device__ void ph_traverse(const Params& P) {
     static_assert(sizeof(int) * (TPB / 32) * TRAV_STACK + sizeof(int2) * (TPB / 32) * 64 <= SCRATCH_BYTES, "");
     int(*sstack)[TRAV_STACK] = reinterpret_cast<int(*)[TRAV_STACK]>(smem_scratch());
@@ -457,14 +460,10 @@ __device__ void ph_traverse(const Params& P) {
                     atomicOr(&P.g->error, ERR_CAP_STACK);
                 }
             };
-            while (sp > 0) {
-                const int node = stack[--sp];
-                __syncwarp();
-                const float4* nd = B.node + 4LL * node;  // both child boxes: one 64 B line
-                const float4 l0 = nd[0], h0 = nd[1], l1 = nd[2], h1 = nd[3];
-                // ordered classes (EE, VV) only need partners above the query's own index:
-                // subtrees whose largest index is <= ia are skipped
-                const int need = ordered ? ia : -0x7fffffff - 1;
+            // ordered classes (EE, VV) only need partners above the query's own index:
+            // subtrees whose largest index is <= ia are skipped
+            const int need = ordered ? ia : -0x7fffffff - 1;
+            auto visit = [&](float4 l0, float4 h0, float4 l1, float4 h1) {
                 const bool hit0 = box_hit(qlo, qhi, l0, h0) && __float_as_int(h0.w) > need;
                 const bool hit1 = box_hit(qlo, qhi, l1, h1) && __float_as_int(h1.w) > need;
                 const bool any0 = __any_sync(0xffffffffu, hit0), any1 = __any_sync(0xffffffffu, hit1);
@@ -476,6 +475,29 @@ __device__ void ph_traverse(const Params& P) {
                     if (ref < 0) leaf(k ? hit1 : hit0, ~ref);
                     else push(ref);
                 }
+            };
+            while (sp > 0) {
+#if TW_WALK_PAIRS
+                // two nodes per step when the stack holds two: their child boxes
+                // load together, halving the dependent load chain of the walk
+                if (sp >= 2) {
+                    const int na = stack[sp - 1], nb = stack[sp - 2];
+                    sp -= 2;
+                    __syncwarp();
+                    const float4* da = B.node + 4LL * na;
+                    const float4* db = B.node + 4LL * nb;
+                    const float4 a0 = da[0], a1 = da[1], a2 = da[2], a3 = da[3];
+                    const float4 b0 = db[0], b1 = db[1], b2 = db[2], b3 = db[3];
+                    visit(a0, a1, a2, a3);
+                    visit(b0, b1, b2, b3);
+                    __syncwarp();
+                    continue;
+                }
+#endif
+                const int node = stack[--sp];
+                __syncwarp();
+                const float4* nd = B.node + 4LL * node;  // both child boxes: one 64 B line
+                visit(nd[0], nd[1], nd[2], nd[3]);
                 __syncwarp();
             }
             flush(true);
