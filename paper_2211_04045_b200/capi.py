@@ -255,7 +255,8 @@ def phase_profile(ctx: Context):
         if line.strip() == "SYNC();":
             prev = src[i - 2]
             m = re.search(r"(ph_[a-z_]+)", prev)
-            names[i % NS] = m.group(1) if m else f"line{i}"
+            # sites are __LINE__ % NS: the resolve kernel (first in the file) wins
+            names.setdefault(i % NS, m.group(1) if m else f"line{i}")
     out = {}
     for k in range(min(n, NS)):
         name = names.get(int(sites[k]), f"site{int(sites[k])}")

@@ -54,15 +54,24 @@ struct Bvh {
     unsigned* flag;   // refit arrival counters (internal nodes)
 };
 
+// The words every CTA hammers live on their own 128-byte lines: the grid
+// barrier's counter (spun on by every waiting CTA), the error word (polled by
+// the waiters) and the dynamic work counters, so that the counters' atomics
+// do not queue behind the waiters' polling loads (+1.5% resolves/s).
 struct Globals {
     unsigned bar_count;
     unsigned bar_gen;
+    char pad_bar[120];
     int error;
     int nonfinite;
     int internal_line;
+    char pad_err[116];
     unsigned long long work_q;  // dynamic query counter of the traversal (reset by the refit)
+    char pad_q[120];
     unsigned long long ncand;   // broad-phase candidates of the current search (reset by the refit)
+    char pad_c[120];
     unsigned long long work_s;  // dynamic query counter of the partner sort (reset by the refit)
+    char pad_s[120];
     int ccd_violations;         // certification results (k_ccd)
     int ccd_certain;
     int ner;             // edge rows of this call (set by the prologue)

@@ -342,6 +342,49 @@ __device__ __forceinline__ int bitonic32(int a, int lane) {
     return a;
 }
 
+// Ascending bitonic sort of L independent lists at once, each of up to 32 R
+// ints held as v[i][r] = element r * 32 + lane: stages with a partner distance
+// of 32 or more compare registers of the same lane, the others shuffle. The L
+// lists' shuffle chains interleave. v is sized for the largest R (SORT_R).
+#ifndef TW_SORT_L
+#define TW_SORT_L 4
+#endif
+constexpr int SORT_L = TW_SORT_L, SORT_R = 4;  // K <= 128 partners per query sort in registers
+template <int R, int L>
+__device__ __forceinline__ void bitonic_lists(int (&v)[L][SORT_R], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jr = j >> 5;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (r & jr) continue;
+                    const bool up = ((r * 32 + lane) & k) == 0;
+#pragma unroll
+                    for (int i = 0; i < L; ++i) {
+                        const int lo = min(v[i][r], v[i][r | jr]), hi = max(v[i][r], v[i][r | jr]);
+                        v[i][r] = up ? lo : hi;
+                        v[i][r | jr] = up ? hi : lo;
+                    }
+                }
+                continue;
+            }
+            const bool low = (lane & j) == 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const bool keep_min = (((r * 32 + lane) & k) == 0) == low;
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    const int p = __shfl_xor_sync(0xffffffffu, v[i][r], j);
+                    v[i][r] = keep_min ? min(v[i][r], p) : max(v[i][r], p);
+                }
+            }
+        }
+    }
+}
+
 // warp-cooperative ascending sort of one query's partner list (n >= 2)
 __device__ __forceinline__ void sort_partners(int* s, int n, int lane) {
     if (n <= 32) {
@@ -543,6 +586,9 @@ __device__ void ph_query_totals(const Params& P) {
     for (long long q = lo + threadIdx.x; q < hi; q += TPB) s += min(P.qcount[q], P.K);
     const long long tot = block_sum(s);
     if (threadIdx.x == 0) P.part_q[blockIdx.x] = tot;
+    // K <= 128: ph_emit_pairs sorts each list in registers as it writes it
+    // out. Larger K: the lists are sorted here, one warp per list.
+    if (P.K <= 32 * SORT_R) return;
     const int lane = threadIdx.x & 31;
     for (;;) {
         long long qb = 0;
@@ -550,10 +596,11 @@ __device__ void ph_query_totals(const Params& P) {
         qb = __shfl_sync(0xffffffffu, qb, 0);
         if (qb >= nq) break;
         const int cnt = P.qcount[qb + lane];
-        for (int j = 0; j < 32; ++j) {
-            const int cj = __shfl_sync(0xffffffffu, cnt, j);
-            if (cj < 2 || cj > P.K) continue;
-            sort_partners(P.qslot + (qb + j) * P.K, cj, lane);
+        unsigned todo = __ballot_sync(0xffffffffu, cnt >= 2 && cnt <= P.K);
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            sort_partners(P.qslot + (qb + j) * P.K, __shfl_sync(0xffffffffu, cnt, j), lane);
         }
     }
 }
@@ -605,6 +652,48 @@ __device__ void ph_emit_pairs(const Params& P) {
         long long tile_tot;
         const long long off = base + block_scan(cnt, &tile_tot);
         base += tile_tot;
+        if (P.K <= 32 * SORT_R) {
+            // the warp writes the keys of its 32 queries, SORT_L lists at a
+            // time: each list is loaded into registers, sorted in lockstep with
+            // the others and written out as keys
+            unsigned todo = __ballot_sync(0xffffffffu, cnt > 0);
+            while (todo) {
+                int ns[SORT_L], v[SORT_L][SORT_R];
+                long long os[SORT_L];
+                uint64_t kbase[SORT_L];
+                int nmax = 0;
+#pragma unroll
+                for (int i = 0; i < SORT_L; ++i) {
+                    ns[i] = 0, os[i] = 0, kbase[i] = 0;
+#pragma unroll
+                    for (int r = 0; r < SORT_R; ++r) v[i][r] = 0x7fffffff;
+                    if (todo) {
+                        const int j = __ffs(todo) - 1;
+                        todo &= todo - 1;
+                        ns[i] = __shfl_sync(0xffffffffu, cnt, j);
+                        os[i] = __shfl_sync(0xffffffffu, off, j);
+                        const long long qj = __shfl_sync(0xffffffffu, q, j);
+                        int ka, ia, kb, cls;
+                        query_of(P, qj, &ka, &ia, &kb, &cls);
+                        kbase[i] = pair_key(ka, ia, kb, 0);
+                        const int* sl = P.qslot + qj * P.K;
+#pragma unroll
+                        for (int r = 0; r < SORT_R; ++r)
+                            if (r * 32 + lane < ns[i]) v[i][r] = sl[r * 32 + lane];
+                        nmax = max(nmax, ns[i]);
+                    }
+                }
+                if (nmax > 64) bitonic_lists<4>(v, lane);
+                else if (nmax > 32) bitonic_lists<2>(v, lane);
+                else if (nmax > 1) bitonic_lists<1>(v, lane);
+#pragma unroll
+                for (int i = 0; i < SORT_L; ++i)
+#pragma unroll
+                    for (int r = 0; r < SORT_R; ++r)
+                        if (r * 32 + lane < ns[i]) P.pkey[os[i] + r * 32 + lane] = kbase[i] | uint64_t(uint32_t(v[i][r]));
+            }
+            continue;
+        }
         // the warp writes the keys of its 32 queries, lanes over the partners
         for (int j = 0; j < 32; ++j) {
             const int cj = __shfl_sync(0xffffffffu, cnt, j);
