@@ -597,6 +597,9 @@ int tw_ctx_create(int device, void* stream, tw_ctx** out) {
     ctx->minb = want;
     if (const char* s = std::getenv("TW_PGS_TAIL")) ctx->pgs_tail_rows = std::max(0LL, std::atoll(s));
     if (const char* s = std::getenv("TW_BVH_REBUILD")) ctx->bvh_rebuild = std::max(1, std::atoi(s));
+    // initial partner slots per query (<= 128: lists sorted in registers in the
+    // key emission; more: sorted in memory by ph_query_totals)
+    if (const char* s = std::getenv("TW_QUERY_SLOTS")) ctx->K = std::max(4, std::atoi(s));
     if (std::getenv("TW_TINY_CAPS")) {  // start every capacity tiny: exercises the grow-and-rerun paths
         ctx->pcap = 256, ctx->ccap = 256, ctx->K = 4, ctx->arch_cap = 16, ctx->refpool_cap = 1024;
         ctx->colcap = 8;

@@ -54,3 +54,30 @@ def test_tiny_capacities_grow_to_identical_results(ctxs, case, mode):
     # the stage search grows its own way
     pn, pt = capi.search(normal, mn, sc.y, 4e-3), capi.search(tiny, mt, sc.y, 4e-3)
     assert np.array_equal(pn.keys, pt.keys) and np.array_equal(_bits(pn.dist), _bits(pt.dist))
+
+
+@pytest.fixture
+def wide_slots(normal):
+    os.environ["TW_QUERY_SLOTS"] = "256"  # > 128 partner slots: the in-memory partner sort
+    try:
+        wide = capi.Context(0)
+    finally:
+        del os.environ["TW_QUERY_SLOTS"]
+    yield normal, wide
+    wide.close()
+
+
+@pytest.mark.parametrize("sc", [S.reef_knot(), S.bow_knot()], ids=lambda s: s.name)
+def test_partner_sort_paths_agree(wide_slots, sc):
+    """Partner lists are sorted in registers inside the key emission when the
+    slot capacity is <= 128 and by ph_query_totals in memory above that: both
+    orders must be the reference's key order."""
+    normal, wide = wide_slots
+    mn, mw = capi.Mesh.from_scene(normal, sc), capi.Mesh.from_scene(wide, sc)
+    pn, pw = capi.search(normal, mn, sc.x, 4e-3), capi.search(wide, mw, sc.x, 4e-3)
+    k = pn.keys.astype(np.uint64)
+    assert len(k) > 0 and np.all(k[1:] > k[:-1])  # strictly ascending keys
+    assert np.array_equal(pn.keys, pw.keys) and np.array_equal(_bits(pn.dist), _bits(pw.dist))
+    xn, sn = capi.resolve(normal, mn, sc.x, sc.y, delta=5e-4, step_limit=3)
+    xw, sw = capi.resolve(wide, mw, sc.x, sc.y, delta=5e-4, step_limit=3)
+    assert np.array_equal(_bits(xn), _bits(xw)) and sn["num_pairs"] == sw["num_pairs"]
