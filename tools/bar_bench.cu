@@ -78,6 +78,37 @@ __device__ __forceinline__ void bar(Bar* b) {
     __syncthreads();
 }
 
+__device__ __forceinline__ void cluster_bar() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// V5: flip-bit barrier of the persistent kernel (one atomic per CTA).
+// V6: cluster-hierarchical flip-bit: hardware cluster barrier, then one
+// flip-bit atomic per cluster, then the cluster barrier again.
+template <int V>
+__device__ __forceinline__ void flipbar(Bar* b) {
+    unsigned rank = 0, nunits = gridDim.x, unit = blockIdx.x;
+    if (V == 6) {
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(nunits));
+        asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(unit));
+        cluster_bar();
+    } else {
+        __syncthreads();
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+        const unsigned inc = unit == 0 ? 0x80000000u - (nunits - 1u) : 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(&b->count, inc);
+        volatile unsigned* cnt = &b->count;
+        while (((old ^ *cnt) & 0x80000000u) == 0u) {
+        }
+        __threadfence();
+    }
+    if (V == 6) cluster_bar();
+    else __syncthreads();
+}
+
 template <int V>
 __global__ void k(Bar* b, int n, unsigned long long* ns, float* sink) {
     float acc = threadIdx.x;
@@ -86,6 +117,7 @@ __global__ void k(Bar* b, int n, unsigned long long* ns, float* sink) {
     for (int i = 0; i < n; ++i) {
         acc = acc * 1.0001f + 1.f;
         if (V == 4) cg::this_grid().sync();
+        else if (V >= 5) flipbar<V>(b);
         else bar<V>(b);
     }
     unsigned long long t1;
@@ -108,6 +140,35 @@ void run(int nblocks, Bar* b, unsigned long long* ns, float* sink) {
     printf("variant %d blocks %4d: %s %.3f us/barrier\n", V, nblocks, cudaGetErrorString(e), h / 1e3 / n);
 }
 
+template <int V>
+void runc(int nblocks, int cl, Bar* b, unsigned long long* ns, float* sink) {
+    int n = 2000;
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3(nblocks);
+    c.blockDim = dim3(256);
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = cl;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    c.attrs = at;
+    c.numAttrs = 2;
+    cudaError_t e = cudaSuccess;
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaMemset(b, 0, sizeof(Bar));
+        e = cudaLaunchKernelEx(&c, k<V>, b, n, ns, sink);
+        if (e != cudaSuccess) break;
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    unsigned long long h = 0;
+    cudaMemcpy(&h, ns, 8, cudaMemcpyDeviceToHost);
+    printf("variant %d cluster %d blocks %4d: %s %.3f us/barrier\n", V, cl, nblocks, cudaGetErrorString(e),
+           h / 1e3 / n);
+    cudaGetLastError();
+}
+
 int main() {
     Bar* b;
     unsigned long long* ns;
@@ -121,6 +182,9 @@ int main() {
         run<2>(nb, b, ns, sink);
         run<3>(nb, b, ns, sink);
         run<4>(nb, b, ns, sink);
+        run<5>(nb, b, ns, sink);
+        for (int cl : {1, 2, 4, 8}) runc<5>(nb, cl, b, ns, sink);
+        for (int cl : {2, 4, 8}) runc<6>(nb, cl, b, ns, sink);
     }
     return 0;
 }
