@@ -216,8 +216,8 @@ struct Params {
     // reference coloring scratch
     long long refpool_cap;
     int* refpool;
-    // PGS colors with at most this many rows at the end of the color order run
-    // on one CTA (ph_pgs_tail); 0 disables
+    // runs of consecutive PGS colors with at most this many rows each run on
+    // one CTA (ph_pgs_tail); 0 disables
     long long pgs_tail_rows;
     int pw_all;      // store pair weights for every pair (stage entries) or contact pairs only (resolve)
     const double4* ccd_x1;  // certification (k_ccd): end positions of the segment, else null

@@ -373,18 +373,25 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
             SYNC();
         }
         if (C.solver == 0) {
-            const int ctail = first_tail_color(P, ncol, ncol_c, ncol_e, P.pgs_tail_rows);
             for (int sw = 0; sw < C.sweeps; ++sw) {
-                for (int c = 0; c < ctail; ++c) {
+                for (int c = 0; c < ncol;) {
                     long long c0, nci, e0, nrow;
                     pgs_color_range(P, c, ncol_c, ncol_e, &c0, &nci, &e0, &nrow);
-                    if (nrow == 0) continue;  // an unused color: no phase, no barrier
+                    if (nrow == 0) {  // an unused color: no phase, no barrier
+                        ++c;
+                        continue;
+                    }
+                    if (nrow <= P.pgs_tail_rows) {
+                        // a run of small colors: CTA 0 alone, CTA barriers between them
+                        const int cend = small_color_run(P, c, ncol, ncol_c, ncol_e, P.pgs_tail_rows);
+                        ph_pgs_tail(P, c, cend, ncol_c, ncol_e);
+                        SYNC();
+                        c = cend;
+                        continue;
+                    }
                     ph_pgs_color(P, c, ncol_c, ncol_e);
                     SYNC();
-                }
-                if (ctail < ncol) {
-                    ph_pgs_tail(P, ctail, ncol, ncol_c, ncol_e);
-                    SYNC();
+                    ++c;
                 }
             }
         } else {

@@ -1697,17 +1697,18 @@ __device__ void ph_pgs_color(const Params& P, int c, int ncol_contact, int ncol_
 
 // The trailing colors of a coloring are small (greedy coloring: the last
 // colors pick up the few rows of the densest cliques): a grid-wide phase per
-// color would cost a grid barrier for a handful of rows. first_tail_color
-// returns the first color of the longest suffix of colors with at most
-// `tail_rows` rows each; ph_pgs_tail runs those colors in order on CTA 0
-// alone, with CTA barriers between colors.
-__device__ int first_tail_color(const Params& P, int ncol, int ncol_contact, int ncol_edge, long long tail_rows) {
-    int c = ncol;
-    while (c > 0) {
+// color would cost a grid barrier for a handful of rows. small_color_run
+// returns the end of the run of consecutive colors with at most `tail_rows`
+// rows each that starts at cfirst; ph_pgs_tail runs such a run in order on
+// CTA 0 alone, with CTA barriers between colors (one grid barrier per run).
+__device__ int small_color_run(const Params& P, int cfirst, int ncol, int ncol_contact, int ncol_edge,
+                               long long tail_rows) {
+    int c = cfirst;
+    while (c < ncol) {
         long long c0, nci, e0, n;
-        pgs_color_range(P, c - 1, ncol_contact, ncol_edge, &c0, &nci, &e0, &n);
+        pgs_color_range(P, c, ncol_contact, ncol_edge, &c0, &nci, &e0, &n);
         if (n > tail_rows) break;
-        --c;
+        ++c;
     }
     return c;
 }
