@@ -252,7 +252,7 @@ def phase_profile(ctx: Context):
     src = open(os.path.join(_HERE, "csrc", "tw_kernels.cu")).read().splitlines()
     names = {}
     for i, line in enumerate(src, start=1):
-        if line.strip() == "SYNC();":
+        if line.strip() in ("SYNC();", "SUBSYNC(nsub);"):
             prev = src[i - 2]
             m = re.search(r"(ph_[a-z_]+)", prev)
             # sites are __LINE__ % NS: the resolve kernel (first in the file) wins

@@ -64,6 +64,7 @@ struct tw_ctx {
     int nblocks = 0;
     int minb = 4;  // resolve-kernel instance (CTAs per SM)
     long long pgs_tail_rows = 256;  // TW_PGS_TAIL
+    int pgs_per_sm = 2;             // TW_PGS_CTAS_PER_SM (measured: 1: 152, 2: 154.7, 4: 148.4 resolves/s)
     int bvh_rebuild = 16;           // TW_BVH_REBUILD: rebuild the LBVH topology every n calls on a mesh
     long long launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk = nullptr;
@@ -382,6 +383,7 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.refpool = ctx->refpool.as<int>();
     P.nblocks = ctx->nblocks;
     P.pgs_tail_rows = ctx->pgs_tail_rows;
+    P.pgs_ctas = std::max(1, std::min(ctx->nblocks, ctx->sm_count * ctx->pgs_per_sm));
     P.pw_all = 1;
     P.part_q = ctx->part_q.as<long long>();
     P.part_c = ctx->part_c.as<long long>();
@@ -595,6 +597,7 @@ int tw_ctx_create(int device, void* stream, tw_ctx** out) {
     int want = 4;  // measured best on B200 (bow knot): 64 regs, 32 warps/SM
     if (const char* s = std::getenv("TW_BLOCKS_PER_SM")) want = std::min(4, std::max(2, std::atoi(s)));
     ctx->minb = want;
+    if (const char* s = std::getenv("TW_PGS_CTAS_PER_SM")) ctx->pgs_per_sm = std::max(1, std::atoi(s));
     if (const char* s = std::getenv("TW_PGS_TAIL")) ctx->pgs_tail_rows = std::max(0LL, std::atoll(s));
     if (const char* s = std::getenv("TW_BVH_REBUILD")) ctx->bvh_rebuild = std::max(1, std::atoi(s));
     // initial partner slots per query (<= 128: lists sorted in registers in the

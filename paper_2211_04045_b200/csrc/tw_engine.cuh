@@ -62,6 +62,8 @@ struct Globals {
     unsigned bar_count;
     unsigned bar_gen;
     char pad_bar[120];
+    unsigned sub_count;  // barrier of the CTAs that run the PGS color phases
+    char pad_sub[124];
     int error;
     int nonfinite;
     int internal_line;
@@ -219,6 +221,9 @@ struct Params {
     // runs of consecutive PGS colors with at most this many rows each run on
     // one CTA (ph_pgs_tail); 0 disables
     long long pgs_tail_rows;
+    // CTAs that run the PGS color phases (the first pgs_ctas of the grid, one
+    // or two per SM): their barrier is cheaper than the whole grid's
+    int pgs_ctas;
     int pw_all;      // store pair weights for every pair (stage entries) or contact pairs only (resolve)
     const double4* ccd_x1;  // certification (k_ccd): end positions of the segment, else null
     // per block scratch

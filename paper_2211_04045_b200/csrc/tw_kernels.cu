@@ -277,6 +277,18 @@ __device__ bool prologue(const Params& P) {
         }                                                                         \
     } while (0)
 
+// the same over the first n CTAs only (sub_sync)
+#define SUBSYNC(n)                                                                \
+    do {                                                                          \
+        if (!sub_sync(g, (n))) return;                                            \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                \
+            const unsigned long long now_ = global_ns();                          \
+            g->phase_ns[__LINE__ % kPhaseSites] += now_ - g->phase_t0;            \
+            g->phase_cnt[__LINE__ % kPhaseSites] += 1;                            \
+            g->phase_t0 = now_;                                                   \
+        }                                                                         \
+    } while (0)
+
 // MINB = resident CTAs per SM the register allocation targets (2: 128 regs,
 // 3: 80, 4: 64); the context picks the instance (TW_BLOCKS_PER_SM).
 template <int MINB>
@@ -373,27 +385,34 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
             SYNC();
         }
         if (C.solver == 0) {
-            for (int sw = 0; sw < C.sweeps; ++sw) {
-                for (int c = 0; c < ncol;) {
-                    long long c0, nci, e0, nrow;
-                    pgs_color_range(P, c, ncol_c, ncol_e, &c0, &nci, &e0, &nrow);
-                    if (nrow == 0) {  // an unused color: no phase, no barrier
+            // the color phases run on the first pgs_ctas CTAs (one per SM) with
+            // their own barrier; the rest of the grid waits at the join
+            const int nsub = P.pgs_ctas;
+            if ((int)blockIdx.x < nsub) {
+                for (int sw = 0; sw < C.sweeps; ++sw) {
+                    for (int c = 0; c < ncol;) {
+                        long long c0, nci, e0, nrow;
+                        pgs_color_range(P, c, ncol_c, ncol_e, &c0, &nci, &e0, &nrow);
+                        if (nrow == 0) {  // an unused color: no phase, no barrier
+                            ++c;
+                            continue;
+                        }
+                        if (nrow <= P.pgs_tail_rows) {
+                            // a run of small colors: CTA 0 alone, CTA barriers between them
+                            const int cend = small_color_run(P, c, ncol, ncol_c, ncol_e, P.pgs_tail_rows);
+                            ph_pgs_tail(P, c, cend, ncol_c, ncol_e);
+                            SUBSYNC(nsub);
+                            c = cend;
+                            continue;
+                        }
+                        ph_pgs_color(P, c, ncol_c, ncol_e, nsub);
+                        SUBSYNC(nsub);
                         ++c;
-                        continue;
                     }
-                    if (nrow <= P.pgs_tail_rows) {
-                        // a run of small colors: CTA 0 alone, CTA barriers between them
-                        const int cend = small_color_run(P, c, ncol, ncol_c, ncol_e, P.pgs_tail_rows);
-                        ph_pgs_tail(P, c, cend, ncol_c, ncol_e);
-                        SYNC();
-                        c = cend;
-                        continue;
-                    }
-                    ph_pgs_color(P, c, ncol_c, ncol_e);
-                    SYNC();
-                    ++c;
                 }
             }
+            // ph_pgs_join
+            SYNC();
         } else {
             for (int sw = 0; sw < C.sweeps; ++sw) {
                 ph_jacobi_next(P, nc);
@@ -679,7 +698,7 @@ __global__ void __launch_bounds__(TPB, 4) k_stage_backward(Params P, long long n
         STAGE_SYNC();
         for (int sw = 0; sw < P.cfg.sweeps; ++sw)
             for (int c = 0; c < ncol; ++c) {
-                ph_pgs_color(P, c, ncol, 0);
+                ph_pgs_color(P, c, ncol, 0, gridDim.x);
                 STAGE_SYNC();
             }
     } else {

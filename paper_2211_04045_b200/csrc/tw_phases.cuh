@@ -48,6 +48,34 @@ __device__ __forceinline__ bool grid_sync(Globals* g) {
     return *((volatile int*)&g->error) == 0;
 }
 
+// Barrier of the first n CTAs of the grid only (the same flip-bit scheme on
+// its own counter); the other CTAs wait at the next grid barrier.
+__device__ __forceinline__ bool sub_sync(Globals* g, unsigned n) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (n - 1u) : 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(&g->sub_count, inc);
+        volatile unsigned* cnt = &g->sub_count;
+        volatile int* err = &g->error;
+        unsigned long long t0 = 0;
+        for (unsigned it = 0; ((old ^ *cnt) & 0x80000000u) == 0u; ++it) {
+            if ((it & 63u) == 63u) {
+                if (*err) break;
+                const unsigned long long t = global_ns();
+                if (t0 == 0) t0 = t;
+                else if (t - t0 > 20000000000ull) {
+                    atomicOr(&g->error, ERR_TIMEOUT);
+                    break;
+                }
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    return *((volatile int*)&g->error) == 0;
+}
+
 // ============================================================ block scans
 // exclusive scan of v over the CTA; *total receives the CTA sum
 __device__ __forceinline__ long long block_scan(long long v, long long* total) {
@@ -1684,12 +1712,13 @@ __device__ __forceinline__ void pgs_color_range(const Params& P, int c, int ncol
     *n = *nci + (e1 - *e0);
 }
 
-__device__ void ph_pgs_color(const Params& P, int c, int ncol_contact, int ncol_edge) {
+__device__ void ph_pgs_color(const Params& P, int c, int ncol_contact, int ncol_edge, int nctas) {
     long long c0, nci, e0, n;
     pgs_color_range(P, c, ncol_contact, ncol_edge, &c0, &nci, &e0, &n);
-    // rows dealt round-robin over the CTAs (row k -> CTA k mod grid): a small
-    // color spreads over all SMs instead of filling the first few
-    for (long long k = blockIdx.x + (long long)threadIdx.x * gridDim.x; k < n; k += gstride()) {
+    // rows dealt round-robin over the nctas CTAs (row k -> CTA k mod nctas): a
+    // small color spreads over all SMs instead of filling the first few
+    const long long stride = (long long)nctas * TPB;
+    for (long long k = blockIdx.x + (long long)threadIdx.x * nctas; k < n; k += stride) {
         if (k < nci) pgs_contact_packed(P, c0 + k);
         else pgs_edge_row(P, P.er_by_color[e0 + (k - nci)]);
     }
