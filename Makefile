@@ -42,8 +42,11 @@ $(PYMOD): $(CSRC)/tw_pymodule.cpp $(LIB) include/twoway/*.hpp
 	$(CXX) -O2 -std=c++20 -fPIC -shared -Iinclude -I$(PY_INC) -I$(PYBIND_INC) $< -o $@ \
 	    -L$(PKG) -l:libtwoway_b200.so -Wl,-rpath,'$$ORIGIN'
 
+# The real reference (oracle/_ref, test infrastructure) is built only where its
+# sources exist (this container); the GPU box uses the prebuilt files.
 oracle:
 	$(MAKE) -s -C oracle
+	@if [ -d /root/reference/proj/src ]; then $(MAKE) -s -C oracle -f Makefile.ref -j8 all; fi
 
 clean:
 	rm -rf $(BUILD) $(LIB) $(PYMOD)

@@ -140,6 +140,20 @@ def append_mesh(m: Mesh, o: Mesh) -> int:
     return off
 
 
+def _sqnorm3(v) -> float:
+    """Eigen squaredNorm of a Vector3d: (x*x + y*y) + z*z."""
+    return (float(v[0]) * float(v[0]) + float(v[1]) * float(v[1])) + float(v[2]) * float(v[2])
+
+
+def _norm3(v) -> float:
+    return math.sqrt(_sqnorm3(v))
+
+
+def _matvec3(R, v):
+    """Matrix3d * Vector3d, each row ((r0*v0 + r1*v1) + r2*v2)."""
+    return np.array([(R[i, 0] * v[0] + R[i, 1] * v[1]) + R[i, 2] * v[2] for i in range(3)])
+
+
 def compute_lumped_masses(m: Mesh, area_density: float, line_density: float) -> None:
     """compute_lumped_masses (mesh.cpp:57-77); pinned vertices stay pinned."""
     n = len(m.positions)
@@ -147,11 +161,11 @@ def compute_lumped_masses(m: Mesh, area_density: float, line_density: float) -> 
     P = m.positions
     for t in m.triangles:
         e1, e2 = P[t[1]] - P[t[0]], P[t[2]] - P[t[0]]
-        a = area_density * 0.5 * np.linalg.norm(np.cross(e1, e2))
+        a = area_density * 0.5 * _norm3(np.cross(e1, e2))
         for k in range(3):
             mass[t[k]] += a / 3.0
     for e in m.strand_edges:
-        a = line_density * np.linalg.norm(P[e[1]] - P[e[0]])
+        a = line_density * _norm3(P[e[1]] - P[e[0]])
         mass[e[0]] += 0.5 * a
         mass[e[1]] += 0.5 * a
     pinned = m.inv_mass == 0.0
@@ -213,7 +227,7 @@ def make_icosphere(subdivisions, radius, center) -> Mesh:
     t = (1.0 + math.sqrt(5.0)) / 2.0
     verts = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t), (0, -1, -t),
              (0, 1, -t), (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
-    verts = [np.asarray(v, dtype=np.float64) / np.linalg.norm(v) for v in verts]
+    verts = [np.asarray(v, dtype=np.float64) / _norm3(np.asarray(v, dtype=np.float64)) for v in verts]
     faces = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4),
              (11, 10, 2), (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8),
              (3, 8, 9), (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)]
@@ -225,7 +239,7 @@ def make_icosphere(subdivisions, radius, center) -> Mesh:
             if key in mid:
                 return mid[key]
             v = verts[a] + verts[b]
-            verts.append(v / np.linalg.norm(v))
+            verts.append(v / _norm3(v))
             mid[key] = len(verts) - 1
             return mid[key]
 
@@ -282,7 +296,7 @@ def make_strand(n, a, b) -> Mesh:
 def rotation_matrix(axis, angle):
     """Eigen::AngleAxisd::toRotationMatrix."""
     ax = np.asarray(axis, dtype=np.float64)
-    ax = ax / np.linalg.norm(ax)
+    ax = ax / _norm3(ax)
     s, c = math.sin(angle), math.cos(angle)
     sa, ca = s * ax, (1.0 - c) * ax
     R = np.empty((3, 3))
@@ -299,7 +313,7 @@ def rotation_matrix(axis, angle):
 def rotate_about(x, center, axis, angle):
     R = rotation_matrix(axis, angle)
     c = np.asarray(center, dtype=np.float64)
-    return c + (np.asarray(x) - c) @ R.T
+    return np.array([c + _matvec3(R, p - c) for p in np.asarray(x, dtype=np.float64)]).reshape(-1, 3)
 
 
 def _scene(name, m: Mesh, y, benign=True, penetrating=False) -> Scene:
@@ -344,7 +358,7 @@ def fixture_tube_twist() -> Scene:
         t = (y[v, 2] + 0.03) / 0.06
         ang = (t - 0.5) * (2.0 * PI / 1.5)
         c = np.array([0, 0, y[v, 2]])
-        p = c + rotation_matrix((0, 0, 1), ang) @ (y[v] - c)
+        p = c + _matvec3(rotation_matrix((0, 0, 1), ang), y[v] - c)
         p[2] *= 0.7
         y[v] = p
     return _scene("tube_twist", m, y, True, False)
@@ -378,9 +392,15 @@ def fixture_random(seed: int, index: int) -> Scene:
     compute_lumped_masses(top, 0.1, 0.0)
     append_mesh(m, top)
     x = m.positions
-    axis = (uni(), uni(), 1.5 + 0.5 * uni())
+    # Vec3(a, b, c) constructor arguments: g++ evaluates them right to left,
+    # so the reference draws z, then y, then x (fixtures.cpp:290,292).
+    az = 1.5 + 0.5 * uni()
+    ay = uni()
+    axis = (uni(), ay, az)
     ang = (30.0 + 25.0 * uni()) * PI / 180.0
-    shift = np.array([0.004 * uni(), 0.004 * uni(), -0.008 + 0.004 * uni()])
+    sz = -0.008 + 0.004 * uni()
+    sy = 0.004 * uni()
+    shift = np.array([0.004 * uni(), sy, sz])
     y = x.copy()
     y[36:] = rotate_about(y[36:], (0, 0, 0.004), axis, ang) + shift
     for v in range(36):
