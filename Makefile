@@ -10,8 +10,8 @@ CSRC      := $(PKG)/csrc
 NVFLAGS   := $(ARCH) -O3 -std=c++17 -lineinfo -fmad=false -Xcompiler -fPIC -Iinclude -I$(CSRC) \
              --expt-relaxed-constexpr -diag-suppress 550 $(NVEXTRA)
 LIB       := $(PKG)/libtwoway_b200.so
-CU_SRCS   := $(CSRC)/tw_kernels.cu $(CSRC)/tw_capi.cu
-CU_HDRS   := $(CSRC)/tw_math.cuh $(CSRC)/tw_engine.cuh $(CSRC)/tw_phases.cuh $(CSRC)/tw_internal.h include/tw_c.h
+CU_SRCS   := $(CSRC)/tw_kernels.cu $(CSRC)/tw_capi.cu $(CSRC)/tw_dynamics.cu
+CU_HDRS   := $(CSRC)/tw_ctx.h $(CSRC)/tw_math.cuh $(CSRC)/tw_engine.cuh $(CSRC)/tw_phases.cuh $(CSRC)/tw_internal.h include/tw_c.h
 CPP_SRCS  := $(CSRC)/tw_api.cpp
 PY_EXT    := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_config_var('EXT_SUFFIX'))" 2>/dev/null)
 PYMOD     := $(PKG)/_twoway$(PY_EXT)
@@ -19,7 +19,7 @@ PY_INC    := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_paths()[
 PYBIND_INC:= $(shell $(PYTHON) -c "import pybind11;print(pybind11.get_include())" 2>/dev/null)
 
 BUILD     := build
-OBJS      := $(BUILD)/tw_kernels.o $(BUILD)/tw_capi.o $(BUILD)/tw_api.o
+OBJS      := $(BUILD)/tw_kernels.o $(BUILD)/tw_capi.o $(BUILD)/tw_dynamics.o $(BUILD)/tw_api.o
 
 all: $(LIB) $(PYMOD) oracle
 
@@ -31,6 +31,9 @@ $(BUILD)/tw_kernels.o: $(CSRC)/tw_kernels.cu $(CU_HDRS) | $(BUILD)
 
 $(BUILD)/tw_capi.o: $(CSRC)/tw_capi.cu $(CU_HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(BUILD)/tw_dynamics.o: $(CSRC)/tw_dynamics.cu $(CU_HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_dynamics.log || (cat $(BUILD)/ptxas_dynamics.log; false)
 
 $(BUILD)/tw_api.o: $(CSRC)/tw_api.cpp include/twoway/*.hpp include/tw_c.h | $(BUILD)
 	$(CXX) -O2 -std=c++20 -fPIC -ffp-contract=off -Iinclude -c $< -o $@

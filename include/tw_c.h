@@ -201,6 +201,62 @@ int tw_stage_advance(tw_ctx* ctx, int32_t nv, const double* inv_mass, const doub
 int tw_ccd_certify(tw_ctx* ctx, tw_mesh* mesh, const double* x0, const double* x1, int32_t* violations,
                    int32_t* certain, int64_t* candidates);
 
+
+/* ---- dynamics: the step-and-project simulator around resolve -------------
+ * proj/include/twoway/dynamics.hpp / proj/src/dynamics.cpp on the device: the
+ * implicit-Euler incremental potential (inertia, springs, flat-rest bending,
+ * gravity), the quadratic repulsion on the proximity set, the block-Jacobi
+ * PCG Newton target and step() = target + resolve + velocity update. */
+
+/* EnergyModel scalars (dynamics.hpp:12-24) */
+typedef struct {
+    double spring_stiffness;    /* 50 N/m */
+    double bending_stiffness;   /* 0 */
+    double gravity[3];          /* (0, 0, -9.81) */
+    double repulsion_stiffness; /* 1e3 N/m */
+    double repulsion_radius;    /* 1e-3 m */
+    double dt;                  /* 0.01 s */
+    int32_t newton_iters;       /* 1 */
+    double mu;                  /* 0: friction_filter (mu > 0) returns TW_EUNSUPPORTED */
+    double pcg_tol;             /* 1e-6 relative */
+    int32_t pcg_max_iters;      /* 400 */
+} tw_energy_model;
+
+/* StepStats (dynamics.hpp:78-90) plus device diagnostics */
+typedef struct {
+    int32_t resolve_steps;   /* total_resolve_steps() */
+    int32_t searches;        /* total_searches() of the resolves */
+    int32_t resolve_converged;
+    int32_t pcg_iterations;  /* summed over Newton iterations */
+    int32_t pcg_converged;
+    int32_t num_pairs;       /* |P| of the last target search */
+    int32_t repulsive_pairs; /* pairs closer than repulsion_radius */
+    double device_ms;        /* CUDA-event time of the whole step on the device */
+    double resolve_ms;       /* of which resolve */
+    double wall_ms;
+} tw_step_stats;
+
+typedef struct tw_dyn tw_dyn;
+
+void tw_default_energy_model(tw_energy_model* model);
+/* EnergyModel::prepare (dynamics.cpp:17-69): rest lengths and flat-rest
+ * hinges from rest_x (nv * 3). The model is validated (EnergyModel::validate,
+ * dynamics.cpp:10-15 -> TW_EINVAL). */
+int tw_dyn_create(tw_ctx* ctx, tw_mesh* mesh, const tw_energy_model* model, const double* rest_x, tw_dyn** out);
+void tw_dyn_destroy(tw_dyn* dyn);
+int32_t tw_dyn_num_hinges(const tw_dyn* dyn);
+/* proximity_search(x, d_max) + gradient_and_hessian + add_repulsion +
+ * newton_target (dynamics.cpp:334-337) with the inertia target built from
+ * (x0, v0): writes the Newton target y_out and (nullable) the gradient. */
+int tw_newton_target(tw_ctx* ctx, tw_mesh* mesh, tw_dyn* dyn, double d_max, const double* x0, const double* v0,
+                     const double* x, double* y_out, double* grad_out, tw_step_stats* stats);
+/* step() (dynamics.cpp:326-349): x, v (nv * 3) in/out, host buffers. */
+int tw_step(tw_ctx* ctx, tw_mesh* mesh, tw_dyn* dyn, const tw_resolve_config* cfg, double* x, double* v,
+            tw_step_stats* stats);
+/* Same on device-resident state (HBM pointers, nv * 3 doubles each). */
+int tw_step_device(tw_ctx* ctx, tw_mesh* mesh, tw_dyn* dyn, const tw_resolve_config* cfg, double* d_x, double* d_v,
+                   tw_step_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,8 +65,29 @@ EXPORTS = [
     "tw_ctx_kernel_launches", "tw_ctx_phase_profile", "tw_mesh_create", "tw_mesh_num_edges", "tw_mesh_edges",
     "tw_mesh_destroy", "tw_resolve", "tw_resolve_device", "tw_stage_closest", "tw_stage_search",
     "tw_stage_refresh", "tw_stage_linearize", "tw_stage_color", "tw_stage_backward",
-    "tw_stage_advance", "tw_ccd_certify",
+    "tw_stage_advance", "tw_ccd_certify", "tw_default_energy_model", "tw_dyn_create", "tw_dyn_destroy",
+    "tw_dyn_num_hinges", "tw_newton_target", "tw_step", "tw_step_device",
 ]
+
+
+class EnergyModel(C.Structure):
+    """tw_energy_model = EnergyModel scalars (dynamics.hpp:12-24)."""
+
+    _fields_ = [
+        ("spring_stiffness", C.c_double), ("bending_stiffness", C.c_double),
+        ("gravity", C.c_double * 3), ("repulsion_stiffness", C.c_double),
+        ("repulsion_radius", C.c_double), ("dt", C.c_double), ("newton_iters", C.c_int32),
+        ("mu", C.c_double), ("pcg_tol", C.c_double), ("pcg_max_iters", C.c_int32),
+    ]
+
+
+class StepStats(C.Structure):
+    _fields_ = [
+        ("resolve_steps", C.c_int32), ("searches", C.c_int32), ("resolve_converged", C.c_int32),
+        ("pcg_iterations", C.c_int32), ("pcg_converged", C.c_int32), ("num_pairs", C.c_int32),
+        ("repulsive_pairs", C.c_int32), ("device_ms", C.c_double), ("resolve_ms", C.c_double),
+        ("wall_ms", C.c_double),
+    ]
 
 _LIB = None
 
@@ -103,6 +124,14 @@ def lib():
         L.tw_stage_color.argtypes = [P, P, C.c_int64, P, P, P, P, C.c_uint64, C.c_int32, C.c_int32, P, P]
         L.tw_stage_backward.argtypes = [P, C.c_int32, P, C.c_int64, P, P, P, P, P, C.c_int32, P, P, C.c_int32,
                                         C.c_int32, C.c_double, P, P, P]
+        L.tw_default_energy_model.argtypes = [C.POINTER(EnergyModel)]
+        L.tw_dyn_create.argtypes = [P, P, C.POINTER(EnergyModel), P, C.POINTER(P)]
+        L.tw_dyn_destroy.argtypes = [P]
+        L.tw_dyn_num_hinges.restype = C.c_int32
+        L.tw_dyn_num_hinges.argtypes = [P]
+        L.tw_newton_target.argtypes = [P, P, P, C.c_double, P, P, P, P, P, C.POINTER(StepStats)]
+        L.tw_step.argtypes = [P, P, P, C.POINTER(Config), P, P, C.POINTER(StepStats)]
+        L.tw_step_device.argtypes = [P, P, P, C.POINTER(Config), P, P, C.POINTER(StepStats)]
         _LIB = L
     return _LIB
 
@@ -424,3 +453,91 @@ def ccd_certify_path(ctx: Context, mesh: Mesh, path):
         tot += v
         cert += c
     return tot, cert
+
+
+# ---------------------------------------------------------------- dynamics
+def make_energy_model(**kw) -> EnergyModel:
+    m = EnergyModel()
+    lib().tw_default_energy_model(C.byref(m))
+    for k, v in kw.items():
+        if k == "gravity":
+            for i in range(3):
+                m.gravity[i] = float(v[i])
+        elif any(k == f[0] for f in EnergyModel._fields_):
+            setattr(m, k, v)
+        else:
+            raise ValueError(f"unknown energy model key '{k}'")
+    return m
+
+
+class Dynamics:
+    """tw_dyn: EnergyModel prepared on a mesh (rest lengths, hinges) plus the
+    device state of step() (dynamics.cpp:326-349)."""
+
+    def __init__(self, ctx: Context, mesh: Mesh, rest_x, **model):
+        self.ctx, self.mesh = ctx, mesh
+        self.model = make_energy_model(**model)
+        rx = np.ascontiguousarray(rest_x, np.float64).reshape(-1, 3)
+        self.h = C.c_void_p()
+        rc = lib().tw_dyn_create(ctx.h, mesh.h, C.byref(self.model), _p(rx), C.byref(self.h))
+        if rc == TW_EINVAL:
+            raise ValueError(lib().tw_last_error(ctx.h).decode())
+        ctx.check(rc)
+
+    @property
+    def num_hinges(self):
+        return int(lib().tw_dyn_num_hinges(self.h))
+
+    def close(self):
+        if self.h:
+            lib().tw_dyn_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _step_stats(st):
+    return {k: getattr(st, k) for k, _ in StepStats._fields_}
+
+
+def newton_target(ctx: Context, mesh: Mesh, dyn: Dynamics, x0, v0, x=None, d_max=4e-3):
+    """search + gradient_and_hessian + add_repulsion + newton_target: (y, grad, stats)."""
+    x0 = np.ascontiguousarray(x0, np.float64).reshape(-1, 3)
+    v0 = np.ascontiguousarray(v0, np.float64).reshape(-1, 3)
+    x = x0 if x is None else np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    y = np.zeros_like(x0)
+    g = np.zeros(3 * mesh.nv)
+    st = StepStats()
+    rc = lib().tw_newton_target(ctx.h, mesh.h, dyn.h, d_max, _p(x0), _p(v0), _p(x), _p(y), _p(g), C.byref(st))
+    if rc == TW_EUNSUPPORTED:
+        raise NotImplementedError(lib().tw_last_error(ctx.h).decode())
+    ctx.check(rc)
+    return y, g, _step_stats(st)
+
+
+def step(ctx: Context, mesh: Mesh, dyn: Dynamics, x, v, **kw):
+    """One simulation step on the device: returns (x_next, v_next, stats)."""
+    cfg = make_config(**kw)
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3).copy()
+    v = np.ascontiguousarray(v, np.float64).reshape(-1, 3).copy()
+    st = StepStats()
+    rc = lib().tw_step(ctx.h, mesh.h, dyn.h, C.byref(cfg), _p(x), _p(v), C.byref(st))
+    if rc == TW_EINVAL:
+        raise ValueError(lib().tw_last_error(ctx.h).decode())
+    if rc == TW_EUNSUPPORTED:
+        raise NotImplementedError(lib().tw_last_error(ctx.h).decode())
+    ctx.check(rc)
+    return x, v, _step_stats(st)
+
+
+def step_device_ptr(ctx: Context, mesh: Mesh, dyn: Dynamics, d_x: int, d_v: int, **kw):
+    """step() on device-resident state (HBM pointers, nv*3 float64 each)."""
+    cfg = make_config(**kw)
+    st = StepStats()
+    ctx.check(lib().tw_step_device(ctx.h, mesh.h, dyn.h, C.byref(cfg), C.c_void_p(d_x), C.c_void_p(d_v),
+                                   C.byref(st)))
+    return _step_stats(st)

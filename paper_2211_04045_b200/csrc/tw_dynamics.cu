@@ -1,0 +1,996 @@
+// Device dynamics: the caller of the resolve path that defines a simulation
+// step (proj/src/dynamics.cpp). One step (dynamics.cpp:326-349) runs, per
+// Newton iteration,
+//   proximity search at x (the device broad phase of the resolve path),
+//   gradient_and_hessian (dynamics.cpp:111-168) + add_repulsion (170-202),
+//   newton_target: block-Jacobi preconditioned CG (204-270),
+//   resolve(x, y) (the device-resident Alg. 1),
+// then the velocity update v = (x - x0)/dt (345-347); everything stays in HBM.
+//
+// The Hessian is never assembled. Its blocks are the reference's triplets:
+//   vertex  dynamic: m/dt^2 I ; static: I                    (dynamics.cpp:118-127)
+//   edge    K = k (u u^T + max(0, 1 - L0/l)(I - u u^T)) = a I + b u u^T on
+//           (i,i) / (j,j) for dynamic rows, -K on (i,j) / (j,i) when both are
+//           dynamic                                           (dynamics.cpp:130-150)
+//   hinge   kb k_i k_j I for dynamic rows and columns         (dynamics.cpp:153-166)
+//   pair    sw_a sw_b k dir dir^T on every vertex of a repulsive pair, static
+//           ones included, as add_repulsion does              (dynamics.cpp:170-202)
+// and H z is a per-vertex gather over the vertex's edges (mesh CSR, edge
+// order), hinges (hinge order) and repulsive pair slots (a CSR rebuilt per
+// Newton iteration, pair order): deterministic, no atomics. The gradient is
+// gathered in the same orders, i.e. in the reference's accumulation order.
+//
+// The CG runs in one cooperative kernel with two grid barriers per iteration:
+// phase A updates d, r, z = P r and the partial sums of r.r and r.z; phase B
+// copies d to the best iterate when the residual improved, forms
+// p = z + beta p and q = H p = H z + beta q (the recurrence saves the third
+// barrier a fresh H p would need) and the partial sum of p.q. Block partials
+// are summed by every CTA in the same fixed order, so all CTAs agree on
+// alpha / beta / the exit test without another barrier.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "tw_ctx.h"
+#include "tw_math.cuh"
+
+namespace tw {
+namespace dyn {
+
+constexpr int DTPB = 256;
+
+struct Model {
+    double k_spring, k_bend, grav[3], k_rep, r_rep, dt;
+    double mu, pcg_tol;
+    int pcg_max_iters;
+};
+
+struct DynGlobals {
+    unsigned bar;
+    char pad0[124];
+    int error;
+    int iters;
+    int converged;
+    int nrep;  // repulsive pairs of this Newton iteration
+    double bnorm;
+    double best_res;
+    char pad1[88];
+};
+
+struct DynParams {
+    int nv, ne, nh, nblocks;
+    Model m;
+    const double* inv_mass;
+    const int2* edges;
+    const int* vedge_off;
+    const int* vedge;
+    const double* rest;      // rest length per edge
+    const int4* hv;          // hinge vertices
+    const double4* hk;       // hinge coefficients
+    const int* vh_off;       // vertex -> (hinge << 2 | slot), hinge order
+    const int* vh;
+    const double* x0;        // N x 3: positions at t (inertia target)
+    const double* v0;        // N x 3: velocities at t
+    const double* x;         // N x 3: current Newton point
+    // per edge (this Newton iteration)
+    double4* e_u;            // (u, k * strain); u = 0 for an inactive edge
+    double2* e_ab;           // (a, b): K = a I + b u u^T (0, 0 inactive)
+    // repulsive pairs: compacted records and the vertex -> slot CSR
+    const uint64_t* pkey;
+    const int4* pids;
+    const double4* pdd;
+    const double4* pw;
+    const uint8_t* pflag;
+    long long np;
+    int* rp_ids;             // 4 per repulsive pair (-1 padded)
+    double* rp_sw;           // 4 signed weights per repulsive pair
+    double4* rp_dir;         // (dir, depth)
+    int* rp_count;           // [0]: repulsive pairs
+    unsigned long long* rs_key;  // (vertex << 32 | pair << 2 | slot) per nonzero slot
+    int* vr_off;             // vertex -> range in the sorted rs_key
+    // per vertex
+    double* sdiag;           // m/dt^2 (dynamic) or 1 (static)
+    double4* grad;
+    double* pre;             // 9 per vertex: inverse of the diagonal block (row-major)
+    double4 *b, *d, *r, *z, *p, *q, *best;
+    double* part;            // 2 per block
+    DynGlobals* g;
+};
+
+__device__ __forceinline__ d3 ld3(const double* a, int v) { return mk(a[3 * v], a[3 * v + 1], a[3 * v + 2]); }
+__device__ __forceinline__ d3 l4(const double4& a) { return mk(a.x, a.y, a.z); }
+__device__ __forceinline__ double4 s4(d3 a, double w = 0.0) { return make_double4(a.x, a.y, a.z, w); }
+
+// inertia target x^t + dt v^t + dt^2 g (dynamics.cpp:73-76)
+__device__ __forceinline__ d3 inertia_target(const DynParams& P, int v) {
+    const d3 g = mk(P.m.grav[0], P.m.grav[1], P.m.grav[2]);
+    return add(add(ld3(P.x0, v), scl(P.m.dt, ld3(P.v0, v))), scl(P.m.dt * P.m.dt, g));
+}
+
+// ------------------------------------------------------------------ edges
+// k * strain * u and the PSD-projected block of every edge at x
+// (dynamics.cpp:130-150); both-static and zero-length edges are inactive.
+__global__ void k_edges(DynParams P) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= P.ne) return;
+    const int2 ij = P.edges[e];
+    const bool si = P.inv_mass[ij.x] == 0.0, sj = P.inv_mass[ij.y] == 0.0;
+    double4 u4 = make_double4(0, 0, 0, 0);
+    double2 ab = make_double2(0, 0);
+    if (!(si && sj)) {
+        const d3 dd = sub(ld3(P.x, ij.x), ld3(P.x, ij.y));
+        const double l = nrm(dd);
+        if (!(l < 1e-12)) {
+            const d3 u = dvd(dd, l);
+            const double k = P.m.k_spring;
+            const double strain = l - P.rest[e];
+            const double c = maxd(0.0, 1.0 - P.rest[e] / l);
+            u4 = s4(u, k * strain);
+            ab = make_double2(k * c, k * (1.0 - c));  // K = k (c I + (1 - c) u u^T)
+        }
+    }
+    P.e_u[e] = u4;
+    P.e_ab[e] = ab;
+}
+
+// ------------------------------------------------------- repulsive pairs
+// add_repulsion's pair filter (dynamics.cpp:176-181): active, not all-static,
+// depth = r_rep - d > 0, nonzero direction. One record per pair, slots with a
+// nonzero signed weight become CSR entries keyed (vertex, pair, slot).
+__global__ void k_rep_pairs(DynParams P) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.np) return;
+    const uint8_t fl = P.pflag[i];
+    if (!(fl & 1) || (fl & 2)) return;
+    const double4 dd = P.pdd[i];
+    const double depth = P.m.r_rep - dd.w;
+    if (!(depth > 0.0)) return;
+    const d3 dir = l4(dd);
+    if (is_zero(dir)) return;
+    const uint64_t key = P.pkey[i];
+    const int ka = key_ka(key), kb = key_kb(key);
+    const int4 ids = P.pids[i];
+    const double4 w = P.pw[i];
+    int vid[4] = {-1, -1, -1, -1};
+    double sw[4] = {0, 0, 0, 0};
+    if (ka == KE) {  // EE: (a0, a1, b0, b1), weights (wa0, wa1, wb0, wb1)
+        vid[0] = ids.x, vid[1] = ids.y, vid[2] = ids.z, vid[3] = ids.w;
+        sw[0] = w.x, sw[1] = w.y, sw[2] = -w.z, sw[3] = -w.w;
+    } else {  // vertex a (weight 1) against b = V / E / T
+        vid[0] = ids.x, sw[0] = 1.0;
+        const int nb = kb + 1;
+        const int bid[3] = {ids.y, ids.z, ids.w};
+        const double bw[3] = {w.x, w.y, w.z};
+        for (int k = 0; k < nb; ++k) vid[1 + k] = bid[k], sw[1 + k] = -(kb == KV ? 1.0 : bw[k]);
+    }
+    const int slot = atomicAdd(P.rp_count, 1);
+    (void)slot;
+    // records are indexed by pair index (sparse, only repulsive ones written);
+    // the CSR keys carry the pair index so the gather runs in pair order
+    for (int k = 0; k < 4; ++k) {
+        P.rp_ids[4 * i + k] = vid[k];
+        P.rp_sw[4 * i + k] = sw[k];
+    }
+    P.rp_dir[i] = s4(dir, depth);
+    for (int k = 0; k < 4; ++k)
+        if (vid[k] >= 0 && sw[k] != 0.0) {
+            const unsigned long long e = ((unsigned long long)(unsigned)vid[k] << 32) | ((unsigned long long)i << 2) | k;
+            P.rs_key[atomicAdd(P.rp_count + 1, 1)] = e;
+        }
+}
+
+// vr_off[v] = first sorted entry of vertex v (lower bound), v in [0, nv]
+__global__ void k_rep_offsets(const unsigned long long* keys, int n, int nv, int* off) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v > nv) return;
+    int lo = 0, hi = n;
+    const unsigned long long t = (unsigned long long)(unsigned)v << 32;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (keys[mid] < t) lo = mid + 1;
+        else hi = mid;
+    }
+    off[v] = lo;
+}
+
+// ------------------------------------------------- gradient + diag block
+// Gradient and the diagonal Hessian block of vertex v, gathered in the
+// reference's accumulation order: inertia, edges (edge order), hinges (hinge
+// order), repulsive pairs (pair order). The block is inverted for the 3x3
+// block-Jacobi preconditioner (dynamics.cpp:218-235; a singular block keeps
+// the identity, as a failed LDLT does).
+__global__ void k_grad_diag(DynParams P) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= P.nv) return;
+    const double im = P.inv_mass[v];
+    const bool dyn = im != 0.0;
+    const double inv_dt2 = 1.0 / (P.m.dt * P.m.dt);
+    d3 g = mk(0, 0, 0);
+    double B[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    double s = 1.0;
+    if (dyn) {
+        const double mass = 1.0 / im;
+        s = mass * inv_dt2;
+        g = scl(mass * inv_dt2, sub(ld3(P.x, v), inertia_target(P, v)));
+    }
+    B[0] = B[4] = B[8] = s;
+    P.sdiag[v] = s;
+    if (dyn) {
+        for (int k = P.vedge_off[v]; k < P.vedge_off[v + 1]; ++k) {
+            const int e = P.vedge[k];
+            const double4 u4 = P.e_u[e];
+            const double2 ab = P.e_ab[e];
+            if (ab.x == 0.0 && ab.y == 0.0 && u4.x == 0.0 && u4.y == 0.0 && u4.z == 0.0) continue;
+            const d3 u = l4(u4);
+            const d3 f = scl(u4.w, u);
+            g = P.edges[e].x == v ? add(g, f) : sub(g, f);
+            const double ul[3] = {u.x, u.y, u.z};
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) B[3 * r + c] += (r == c ? ab.x : 0.0) + ab.y * ul[r] * ul[c];
+        }
+        for (int k = P.vh_off[v]; k < P.vh_off[v + 1]; ++k) {
+            const int h = P.vh[k] >> 2, i = P.vh[k] & 3;
+            const int4 hv = P.hv[h];
+            const double4 hk = P.hk[h];
+            const int hvv[4] = {hv.x, hv.y, hv.z, hv.w};
+            const double hkk[4] = {hk.x, hk.y, hk.z, hk.w};
+            d3 c = mk(0, 0, 0);
+            for (int j = 0; j < 4; ++j) c = add(c, scl(hkk[j], ld3(P.x, hvv[j])));
+            g = add(g, scl(P.m.k_bend * hkk[i], c));
+            const double w = P.m.k_bend * hkk[i] * hkk[i];
+            B[0] += w, B[4] += w, B[8] += w;
+        }
+    }
+    for (int k = P.vr_off[v]; k < P.vr_off[v + 1]; ++k) {
+        const unsigned long long e = P.rs_key[k];
+        const long long pi = (long long)((e & 0xffffffffull) >> 2);
+        const int a = (int)(e & 3);
+        const double4 dd = P.rp_dir[pi];
+        const d3 dir = l4(dd);
+        const double swa = P.rp_sw[4 * pi + a];
+        const double kr = P.m.k_rep;
+        g = add(g, scl(-kr * dd.w * swa, dir));
+        const d3 gn = scl(kr, dir);
+        const double dl[3] = {dir.x, dir.y, dir.z}, gl[3] = {gn.x, gn.y, gn.z};
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) B[3 * r + c] += swa * swa * (gl[r] * dl[c]);
+    }
+    P.grad[v] = s4(g);
+    // inverse of the symmetric block (adjugate / determinant)
+    const double c00 = B[4] * B[8] - B[5] * B[7], c01 = B[5] * B[6] - B[3] * B[8], c02 = B[3] * B[7] - B[4] * B[6];
+    const double det = B[0] * c00 + B[1] * c01 + B[2] * c02;
+    double* Pi = P.pre + 9 * (size_t)v;
+    if (det > 0.0 && isfinite(det)) {
+        const double id = 1.0 / det;
+        Pi[0] = c00 * id;
+        Pi[1] = (B[2] * B[7] - B[1] * B[8]) * id;
+        Pi[2] = (B[1] * B[5] - B[2] * B[4]) * id;
+        Pi[3] = c01 * id;
+        Pi[4] = (B[0] * B[8] - B[2] * B[6]) * id;
+        Pi[5] = (B[2] * B[3] - B[0] * B[5]) * id;
+        Pi[6] = c02 * id;
+        Pi[7] = (B[1] * B[6] - B[0] * B[7]) * id;
+        Pi[8] = (B[0] * B[4] - B[1] * B[3]) * id;
+    } else {
+        for (int k = 0; k < 9; ++k) Pi[k] = (k % 4 == 0) ? 1.0 : 0.0;
+    }
+}
+
+// ------------------------------------------------------------- operator
+// (H z)_v: the row of vertex v of the implicit Hessian
+__device__ __forceinline__ d3 hess_row(const DynParams& P, int v, const double4* z) {
+    const bool dyn = P.inv_mass[v] != 0.0;
+    const d3 zv = l4(z[v]);
+    d3 out = scl(P.sdiag[v], zv);
+    if (dyn) {
+        for (int k = P.vedge_off[v]; k < P.vedge_off[v + 1]; ++k) {
+            const int e = P.vedge[k];
+            const double2 ab = P.e_ab[e];
+            if (ab.x == 0.0 && ab.y == 0.0) continue;
+            const int2 ij = P.edges[e];
+            const int o = ij.x == v ? ij.y : ij.x;
+            const d3 u = l4(P.e_u[e]);
+            // K z_v - K z_o (the second only when the other end is dynamic)
+            d3 t = zv;
+            if (P.inv_mass[o] != 0.0) t = sub(zv, l4(z[o]));
+            out = add(out, add(scl(ab.x, t), scl(ab.y * dot(u, t), u)));
+        }
+        for (int k = P.vh_off[v]; k < P.vh_off[v + 1]; ++k) {
+            const int h = P.vh[k] >> 2, i = P.vh[k] & 3;
+            const int4 hv = P.hv[h];
+            const double4 hk = P.hk[h];
+            const int hvv[4] = {hv.x, hv.y, hv.z, hv.w};
+            const double hkk[4] = {hk.x, hk.y, hk.z, hk.w};
+            for (int j = 0; j < 4; ++j)
+                if (P.inv_mass[hvv[j]] != 0.0) out = add(out, scl(P.m.k_bend * hkk[i] * hkk[j], l4(z[hvv[j]])));
+        }
+    }
+    for (int k = P.vr_off[v]; k < P.vr_off[v + 1]; ++k) {
+        const unsigned long long e = P.rs_key[k];
+        const long long pi = (long long)((e & 0xffffffffull) >> 2);
+        const int a = (int)(e & 3);
+        const d3 dir = l4(P.rp_dir[pi]);
+        double s = 0.0;
+        for (int b = 0; b < 4; ++b) {
+            const int vb = P.rp_ids[4 * pi + b];
+            const double swb = P.rp_sw[4 * pi + b];
+            if (vb >= 0 && swb != 0.0) s += swb * dot(dir, l4(z[vb]));
+        }
+        out = add(out, scl(P.rp_sw[4 * pi + a] * P.m.k_rep * s, dir));
+    }
+    return out;
+}
+
+__device__ __forceinline__ d3 precond(const DynParams& P, int v, d3 r) {
+    const double* Pi = P.pre + 9 * (size_t)v;
+    return mk((Pi[0] * r.x + Pi[1] * r.y) + Pi[2] * r.z, (Pi[3] * r.x + Pi[4] * r.y) + Pi[5] * r.z,
+              (Pi[6] * r.x + Pi[7] * r.y) + Pi[8] * r.z);
+}
+
+// ---------------------------------------------------- grid-wide helpers
+__device__ __forceinline__ void dyn_sync(DynGlobals* g) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(&g->bar, inc);
+        volatile unsigned* cnt = &g->bar;
+        while (((old ^ *cnt) & 0x80000000u) == 0u) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// block sums of two values -> part[2 * block + {0, 1}]
+__device__ __forceinline__ void block_partial2(double a, double b, double* part) {
+    __shared__ double sa[DTPB / 32], sb[DTPB / 32];
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, o);
+        b += __shfl_down_sync(0xffffffffu, b, o);
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) sa[w] = a, sb[w] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ta = 0.0, tb = 0.0;
+        for (int i = 0; i < DTPB / 32; ++i) ta += sa[i], tb += sb[i];
+        part[2 * blockIdx.x] = ta;
+        part[2 * blockIdx.x + 1] = tb;
+    }
+    __syncthreads();
+}
+
+// every CTA sums the partials in the same order -> identical totals
+__device__ __forceinline__ void grid_total2(const double* part, int nb, double* ta, double* tb) {
+    __shared__ double ra, rb;
+    if (threadIdx.x < 32) {
+        double a = 0.0, b = 0.0;
+        for (int i = threadIdx.x; i < nb; i += 32) a += ((volatile const double*)part)[2 * i], b += ((volatile const double*)part)[2 * i + 1];
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_down_sync(0xffffffffu, a, o);
+            b += __shfl_down_sync(0xffffffffu, b, o);
+        }
+        if (threadIdx.x == 0) ra = a, rb = b;
+    }
+    __syncthreads();
+    *ta = ra;
+    *tb = rb;
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ PCG
+// newton_target's CG (dynamics.cpp:239-262) on b = -grad (static rows 0).
+__global__ void __launch_bounds__(DTPB) k_pcg(DynParams P) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    // partial sums alternate between two buffers, so a CTA may write the next
+    // phase's partials while a slower one still reads the previous ones: one
+    // barrier per phase
+    double* part[2] = {P.part, P.part + 2 * gridDim.x};
+    int cur = 0;
+    // init: b, r = b, z = P r, p = z, d = best = 0; sums r.z and b.b
+    double rz_l = 0.0, bb_l = 0.0;
+    for (int v = tid; v < P.nv; v += nth) {
+        d3 bv = neg(l4(P.grad[v]));
+        if (P.inv_mass[v] == 0.0) bv = mk(0, 0, 0);
+        const d3 zv = precond(P, v, bv);
+        P.b[v] = s4(bv);
+        P.r[v] = s4(bv);
+        P.z[v] = s4(zv);
+        P.p[v] = s4(zv);
+        P.d[v] = make_double4(0, 0, 0, 0);
+        P.best[v] = make_double4(0, 0, 0, 0);
+        rz_l += dot(bv, zv);
+        bb_l += sqn(bv);
+    }
+    block_partial2(rz_l, bb_l, part[cur]);
+    dyn_sync(P.g);
+    double rz, bb;
+    grid_total2(part[cur], gridDim.x, &rz, &bb);
+    cur ^= 1;
+    const double bnorm = sqrt(bb);
+    double best_res = bnorm;
+    // q = H p, p.q
+    double pq_l = 0.0;
+    for (int v = tid; v < P.nv; v += nth) {
+        const d3 q = hess_row(P, v, P.p);
+        P.q[v] = s4(q);
+        pq_l += dot(l4(P.p[v]), q);
+    }
+    block_partial2(pq_l, 0.0, part[cur]);
+    dyn_sync(P.g);
+    int it = 0;
+    const int maxit = P.m.pcg_max_iters;
+    const double tol = P.m.pcg_tol;
+    for (; it < maxit && best_res > tol * bnorm; ++it) {
+        double pq, unused;
+        grid_total2(part[cur], gridDim.x, &pq, &unused);
+        cur ^= 1;
+        if (pq <= 0.0) break;
+        const double alpha = rz / pq;
+        // phase A: d += alpha p; r -= alpha q; z = P r; sums r.r, r.z
+        double rr_l = 0.0, rz_l2 = 0.0;
+        for (int v = tid; v < P.nv; v += nth) {
+            const d3 pv = l4(P.p[v]);
+            const d3 dv = add(l4(P.d[v]), scl(alpha, pv));
+            const d3 rv = sub(l4(P.r[v]), scl(alpha, l4(P.q[v])));
+            const d3 zv = precond(P, v, rv);
+            P.d[v] = s4(dv);
+            P.r[v] = s4(rv);
+            P.z[v] = s4(zv);
+            rr_l += sqn(rv);
+            rz_l2 += dot(rv, zv);
+        }
+        block_partial2(rr_l, rz_l2, part[cur]);
+        dyn_sync(P.g);
+        double rr, rzn;
+        grid_total2(part[cur], gridDim.x, &rr, &rzn);
+        cur ^= 1;
+        const double res = sqrt(rr);
+        const bool improved = res < best_res;
+        if (improved) best_res = res;
+        const double beta = rzn / rz;
+        rz = rzn;
+        // phase B: best = d (if improved); p = z + beta p; q = H z + beta q; sum p.q
+        double pq_l2 = 0.0;
+        for (int v = tid; v < P.nv; v += nth) {
+            if (improved) P.best[v] = P.d[v];
+            const d3 pv = add(l4(P.z[v]), scl(beta, l4(P.p[v])));
+            const d3 qv = add(hess_row(P, v, P.z), scl(beta, l4(P.q[v])));
+            P.p[v] = s4(pv);
+            P.q[v] = s4(qv);
+            pq_l2 += dot(pv, qv);
+        }
+        block_partial2(pq_l2, 0.0, part[cur]);
+        dyn_sync(P.g);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        P.g->iters = it;
+        P.g->converged = best_res <= tol * bnorm ? 1 : 0;
+        P.g->bnorm = bnorm;
+        P.g->best_res = best_res;
+    }
+}
+
+// y = x + best for dynamic vertices (dynamics.cpp:266-268)
+__global__ void k_target(int nv, const double* inv_mass, const double* x, const double4* best, int converged_zero,
+                         double* y) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    double3 o = make_double3(x[3 * v], x[3 * v + 1], x[3 * v + 2]);
+    if (inv_mass[v] != 0.0 && !converged_zero) {
+        const double4 b = best[v];
+        o.x += b.x, o.y += b.y, o.z += b.z;
+    }
+    y[3 * v] = o.x, y[3 * v + 1] = o.y, y[3 * v + 2] = o.z;
+}
+
+// positions (N x 3) -> the resolve path's double4 (x, inv_mass) for the search
+__global__ void k_pack_x4(int nv, const double* x, const double* inv_mass, double4* x4) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < nv) x4[v] = make_double4(x[3 * v], x[3 * v + 1], x[3 * v + 2], inv_mass[v]);
+}
+
+// v = (x - x0) / dt for dynamic vertices, 0 for static (dynamics.cpp:345-347)
+__global__ void k_velocity(int nv, const double* inv_mass, const double* x, const double* x0, double dt, double* vel) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * nv) return;
+    vel[i] = inv_mass[i / 3] == 0.0 ? 0.0 : (x[i] - x0[i]) / dt;
+}
+
+}  // namespace dyn
+}  // namespace tw
+
+using namespace tw;
+using namespace tw::dyn;
+using namespace tw::host;
+
+// --------------------------------------------------------------- C-ABI
+struct tw_dyn {
+    tw_ctx* ctx = nullptr;
+    tw_mesh* mesh = nullptr;
+    tw_energy_model model{};
+    int nh = 0;
+    DevMem rest, hv, hk, vh_off, vh;
+    DevMem hx, hvel, x0, v0, xk, y, e_u, e_ab, rp_ids, rp_sw, rp_dir, rp_count, rs_key, rs_key2, vr_off, sort_tmp;
+    DevMem sdiag, grad, pre, b, d, r, z, p, q, best, part, glob;
+    long long rp_cap = 0;
+};
+
+namespace {
+
+bool model_valid(const tw_energy_model& m) {  // EnergyModel::validate, dynamics.cpp:10-15
+    if (m.spring_stiffness < 0.0 || m.bending_stiffness < 0.0 || m.repulsion_stiffness < 0.0) return false;
+    if (!(m.dt > 0.0)) return false;
+    if (m.newton_iters < 1) return false;
+    if (m.mu < 0.0) return false;
+    return true;
+}
+
+// Flat-rest hinge coefficients (dynamics.cpp:26-68): for every interior edge
+// with exactly two incident triangles, the unit null vector of
+// [1 1 1 1; in-plane rest coordinates of the 4 stencil vertices]. The null
+// vector of a rank-3 3x4 matrix is its generalized cross product (signed 3x3
+// minors); its sign is irrelevant (the energy is quadratic in it).
+void build_hinges(const tw_mesh* m, const std::vector<int32_t>& tris, const double* X, std::vector<int>& hv,
+                  std::vector<double>& hk) {
+    std::vector<std::pair<uint64_t, int>> et;  // (edge key, triangle)
+    const int nt = (int)tris.size() / 3;
+    et.reserve(3 * (size_t)nt);
+    for (int t = 0; t < nt; ++t)
+        for (int k = 0; k < 3; ++k) {
+            const int a = tris[3 * t + k], b = tris[3 * t + (k + 1) % 3];
+            et.push_back({((uint64_t)(uint32_t)std::min(a, b) << 32) | (uint32_t)std::max(a, b), t});
+        }
+    std::stable_sort(et.begin(), et.end(), [](auto& p, auto& q) { return p.first < q.first; });
+    auto P = [&](int v) { return mk(X[3 * v], X[3 * v + 1], X[3 * v + 2]); };
+    for (size_t i = 0; i < et.size();) {
+        size_t j = i;
+        while (j < et.size() && et[j].first == et[i].first) ++j;
+        if (j - i == 2) {
+            const int e0 = (int)(et[i].first >> 32), e1 = (int)(et[i].first & 0xffffffffu);
+            auto opposite = [&](int t) {
+                for (int k = 0; k < 3; ++k) {
+                    const int v = tris[3 * t + k];
+                    if (v != e0 && v != e1) return v;
+                }
+                return -1;
+            };
+            const int v[4] = {e0, e1, opposite(et[i].second), opposite(et[i + 1].second)};
+            const d3 x0 = P(v[0]), e1v = sub(P(v[1]), x0);
+            d3 n = crs(e1v, sub(P(v[2]), x0));
+            if (!(sqn(n) < 1e-24 || sqn(e1v) < 1e-24)) {
+                n = normalized(n);
+                const d3 bu = normalized(e1v), bv = crs(n, bu);
+                double M[3][4];
+                for (int c = 0; c < 4; ++c) {
+                    const d3 d = sub(P(v[c]), x0);
+                    M[0][c] = 1.0, M[1][c] = dot(d, bu), M[2][c] = dot(d, bv);
+                }
+                auto minor = [&](int skip) {
+                    int cols[3], q = 0;
+                    for (int c = 0; c < 4; ++c)
+                        if (c != skip) cols[q++] = c;
+                    const double(*A)[4] = M;
+                    return A[0][cols[0]] * (A[1][cols[1]] * A[2][cols[2]] - A[1][cols[2]] * A[2][cols[1]]) -
+                           A[0][cols[1]] * (A[1][cols[0]] * A[2][cols[2]] - A[1][cols[2]] * A[2][cols[0]]) +
+                           A[0][cols[2]] * (A[1][cols[0]] * A[2][cols[1]] - A[1][cols[1]] * A[2][cols[0]]);
+                };
+                double k[4] = {minor(0), -minor(1), minor(2), -minor(3)};
+                double scale = 0.0, kn = 0.0;
+                for (int r = 0; r < 3; ++r)
+                    for (int c = 0; c < 4; ++c) scale = std::max(scale, std::fabs(M[r][c]));
+                for (int c = 0; c < 4; ++c) kn += k[c] * k[c];
+                kn = std::sqrt(kn);
+                // rank 3 at the reference's 1e-9 relative LU threshold
+                if (kn > 1e-9 * scale * scale * scale) {
+                    for (int c = 0; c < 4; ++c) hv.push_back(v[c]), hk.push_back(k[c] / kn);
+                }
+            }
+        }
+        i = j;
+    }
+}
+
+template <typename T>
+cudaError_t upload(DevMem& d, const std::vector<T>& h) {
+    cudaError_t e = d.ensure(std::max<size_t>(16, h.size() * sizeof(T)));
+    if (e == cudaSuccess && !h.empty()) e = cudaMemcpy(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+DynParams make_dparams(tw_dyn* D, const double* d_x) {
+    tw_ctx* ctx = D->ctx;
+    tw_mesh* m = D->mesh;
+    DynParams P;
+    std::memset(&P, 0, sizeof P);
+    P.nv = m->nv, P.ne = m->ne, P.nh = D->nh;
+    P.nblocks = 0;
+    const tw_energy_model& em = D->model;
+    P.m.k_spring = em.spring_stiffness, P.m.k_bend = em.bending_stiffness;
+    for (int k = 0; k < 3; ++k) P.m.grav[k] = em.gravity[k];
+    P.m.k_rep = em.repulsion_stiffness, P.m.r_rep = em.repulsion_radius, P.m.dt = em.dt;
+    P.m.mu = em.mu, P.m.pcg_tol = em.pcg_tol, P.m.pcg_max_iters = em.pcg_max_iters;
+    P.inv_mass = m->d_inv_mass.as<double>();
+    P.edges = m->d_edges.as<int2>();
+    P.vedge_off = m->d_vedge_off.as<int>();
+    P.vedge = m->d_vedge.as<int>();
+    P.rest = D->rest.as<double>();
+    P.hv = D->hv.as<int4>();
+    P.hk = D->hk.as<double4>();
+    P.vh_off = D->vh_off.as<int>();
+    P.vh = D->vh.as<int>();
+    P.x0 = D->x0.as<double>();
+    P.v0 = D->v0.as<double>();
+    P.x = d_x;
+    P.e_u = D->e_u.as<double4>();
+    P.e_ab = D->e_ab.as<double2>();
+    P.pkey = ctx->pkey.as<uint64_t>();
+    P.pids = ctx->pids.as<int4>();
+    P.pdd = ctx->pdd.as<double4>();
+    P.pw = ctx->pw.as<double4>();
+    P.pflag = ctx->pflag.as<uint8_t>();
+    P.rp_ids = D->rp_ids.as<int>();
+    P.rp_sw = D->rp_sw.as<double>();
+    P.rp_dir = D->rp_dir.as<double4>();
+    P.rp_count = D->rp_count.as<int>();
+    P.rs_key = D->rs_key.as<unsigned long long>();
+    P.vr_off = D->vr_off.as<int>();
+    P.sdiag = D->sdiag.as<double>();
+    P.grad = D->grad.as<double4>();
+    P.pre = D->pre.as<double>();
+    P.b = D->b.as<double4>(), P.d = D->d.as<double4>(), P.r = D->r.as<double4>(), P.z = D->z.as<double4>();
+    P.p = D->p.as<double4>(), P.q = D->q.as<double4>(), P.best = D->best.as<double4>();
+    P.part = D->part.as<double>();
+    P.g = D->glob.as<DynGlobals>();
+    return P;
+}
+
+int pcg_blocks(tw_ctx* ctx, int nv) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg, DTPB, 0);
+    per_sm = std::max(1, std::min(per_sm, 4));
+    const int want = (nv + DTPB - 1) / DTPB;
+    return std::max(1, std::min(ctx->sm_count * per_sm, want));
+}
+
+// Runs the proximity search of the resolve path at ctx->x (double4) with
+// capacity regrowth; leaves the pair set in the context's pair buffers.
+int search_at_x(tw_ctx* ctx, tw_mesh* m, double d_max, long long* np) {
+    tw_resolve_config cfg;
+    tw_default_config(&cfg);
+    cfg.d_max = d_max;
+    cfg.step_limit = 1;
+    Globals G;
+    for (int attempt = 0;; ++attempt) {
+        int rc = ensure_buffers(ctx, m, cfg);
+        if (rc) return rc;
+        Params P = make_params(ctx, m, cfg);
+        CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), ctx->stream));
+        CK(cudaMemsetAsync(ctx->dmin.p, 0x7f, (size_t)m->nv * 8, ctx->stream));
+        rc = build_bvhs(ctx, m);
+        if (rc) return rc;
+        CK(coop_search(ctx->stream, P, ctx->nblocks));
+        ++ctx->launches;
+        CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof G, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (G.error & ERR_TIMEOUT) return fail(ctx, TW_ETIMEOUT, "search: watchdog");
+        if (!(G.error & (ERR_CAP_SLOTS | ERR_CAP_PAIRS | ERR_CAP_CAND))) break;
+        if (attempt > 10) return fail(ctx, TW_ECAPACITY, "search: capacity");
+        if (G.error & ERR_CAP_SLOTS) ctx->K = std::max(ctx->K * 2, ((G.needed_k + 31) / 32) * 32);
+        if (G.error & ERR_CAP_PAIRS) grow_ll(ctx->pcap, G.needed_pairs + G.needed_pairs / 4);
+        if (G.error & ERR_CAP_CAND) grow_ll(ctx->ccap, (long long)G.ncand + (long long)G.ncand / 4);
+    }
+    *np = G.np;
+    return TW_OK;
+}
+
+// search + gradient/Hessian + repulsion + PCG at d_xk (N x 3, device) with
+// inertia data D->x0 / D->v0; the target goes to d_y. stats: pcg iterations /
+// convergence / pairs.
+int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_y, tw_step_stats* st,
+                         double* grad_host) {
+    tw_ctx* ctx = D->ctx;
+    tw_mesh* m = D->mesh;
+    cudaStream_t s = ctx->stream;
+    const int nv = m->nv;
+    const int nb = (nv + DTPB - 1) / DTPB;
+    CK(ctx->x.ensure((size_t)std::max(1, nv) * 32));
+    k_pack_x4<<<std::max(1, nb), DTPB, 0, s>>>(nv, d_xk, m->d_inv_mass.as<double>(), ctx->x.as<double4>());
+    ++ctx->launches;
+    long long np = 0;
+    int rc = search_at_x(ctx, m, d_max, &np);
+    if (rc) return rc;
+    if (D->rp_cap < np + 1) {
+        D->rp_cap = np + 1024;
+        CK(D->rp_ids.ensure((size_t)D->rp_cap * 16));
+        CK(D->rp_sw.ensure((size_t)D->rp_cap * 32));
+        CK(D->rp_dir.ensure((size_t)D->rp_cap * 32));
+        CK(D->rs_key.ensure((size_t)D->rp_cap * 4 * 8));
+        CK(D->rs_key2.ensure((size_t)D->rp_cap * 4 * 8));
+    }
+    DynParams P = make_dparams(D, d_xk);
+    P.np = np;
+    CK(cudaMemsetAsync(D->rp_count.p, 0, 16, s));
+    if (m->ne) {
+        k_edges<<<(m->ne + DTPB - 1) / DTPB, DTPB, 0, s>>>(P);
+        ++ctx->launches;
+    }
+    if (np && D->model.repulsion_stiffness > 0.0) {
+        k_rep_pairs<<<(unsigned)((np + DTPB - 1) / DTPB), DTPB, 0, s>>>(P);
+        ++ctx->launches;
+    }
+    int counts[2] = {0, 0};
+    CK(cudaMemcpyAsync(counts, D->rp_count.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int nent = counts[1];
+    if (nent > 1) {
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, tb, D->rs_key.as<unsigned long long>(),
+                                       D->rs_key2.as<unsigned long long>(), nent, 0, 64, s);
+        CK(D->sort_tmp.ensure(tb));
+        cub::DeviceRadixSort::SortKeys(D->sort_tmp.p, tb, D->rs_key.as<unsigned long long>(),
+                                       D->rs_key2.as<unsigned long long>(), nent, 0, 64, s);
+        ctx->launches += 4;
+        P.rs_key = D->rs_key2.as<unsigned long long>();
+    }
+    k_rep_offsets<<<(nv + 1 + DTPB - 1) / DTPB, DTPB, 0, s>>>(P.rs_key, nent, nv, P.vr_off);
+    k_grad_diag<<<std::max(1, nb), DTPB, 0, s>>>(P);
+    ctx->launches += 2;
+    if (grad_host) {
+        std::vector<double4> g(nv);
+        CK(cudaMemcpyAsync(g.data(), D->grad.p, (size_t)nv * 32, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (int v = 0; v < nv; ++v) grad_host[3 * v] = g[v].x, grad_host[3 * v + 1] = g[v].y, grad_host[3 * v + 2] = g[v].z;
+    }
+    const int pb = pcg_blocks(ctx, nv);
+    P.nblocks = pb;
+    CK(D->part.ensure((size_t)pb * 32));
+    CK(cudaMemsetAsync(D->glob.p, 0, sizeof(DynGlobals), s));
+    void* args[] = {&P};
+    CK(cudaLaunchCooperativeKernel((void*)k_pcg, dim3(pb), dim3(DTPB), args, 0, s));
+    ++ctx->launches;
+    DynGlobals G;
+    CK(cudaMemcpyAsync(&G, D->glob.p, sizeof G, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    k_target<<<std::max(1, nb), DTPB, 0, s>>>(nv, m->d_inv_mass.as<double>(), d_xk, P.best, G.bnorm == 0.0, d_y);
+    ++ctx->launches;
+    if (st) {
+        st->pcg_iterations += G.iters;
+        st->pcg_converged = st->pcg_converged && G.converged;
+        st->num_pairs = (int32_t)np;
+        st->repulsive_pairs = counts[0];
+    }
+    CK(cudaGetLastError());
+    return TW_OK;
+}
+
+int dyn_check(tw_ctx* ctx, tw_mesh* m, tw_dyn* D) {
+    if (!ctx || !m || !D) return fail(ctx, TW_EINVAL, "dynamics: null argument");
+    if (D->mesh != m) return fail(ctx, TW_EINVAL, "dynamics: model prepared on another mesh");
+    if (D->model.mu > 0.0) return fail(ctx, TW_EUNSUPPORTED, "dynamics: friction_filter (mu > 0) is not provided");
+    return TW_OK;
+}
+
+// one step (dynamics.cpp:326-349) on device state d_x / d_v (N x 3)
+int step_device(tw_ctx* ctx, tw_mesh* m, tw_dyn* D, const tw_resolve_config* cfg, double* d_x, double* d_v,
+                tw_step_stats* st) {
+    cudaStream_t s = ctx->stream;
+    const size_t bytes = (size_t)m->nv * 24;
+    CK(cudaEventRecord(ctx->ev0, s));
+    CK(cudaMemcpyAsync(D->x0.p, d_x, bytes, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(D->v0.p, d_v, bytes, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(D->xk.p, d_x, bytes, cudaMemcpyDeviceToDevice, s));
+    st->pcg_converged = 1;
+    for (int k = 0; k < D->model.newton_iters; ++k) {
+        int rc = newton_target_device(D, cfg->d_max, D->xk.as<double>(), D->y.as<double>(), st, nullptr);
+        if (rc) return rc;
+        tw_resolve_stats rs;
+        rc = run_resolve(ctx, m, D->xk.as<double>(), D->y.as<double>(), *cfg, d_x, &rs, nullptr, nullptr, nullptr);
+        if (rc) return rc;
+        st->resolve_steps += rs.steps;
+        st->searches += rs.searches;
+        st->resolve_converged = rs.converged;
+        st->resolve_ms += rs.device_ms;
+        if (k + 1 < D->model.newton_iters) CK(cudaMemcpyAsync(D->xk.p, d_x, bytes, cudaMemcpyDeviceToDevice, s));
+    }
+    const int n3 = 3 * m->nv;
+    k_velocity<<<std::max(1, (n3 + DTPB - 1) / DTPB), DTPB, 0, s>>>(m->nv, m->d_inv_mass.as<double>(), d_x,
+                                                                   D->x0.as<double>(), D->model.dt, d_v);
+    ++ctx->launches;
+    CK(cudaEventRecord(ctx->ev1, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    st->device_ms = ms;
+    CK(cudaGetLastError());
+    return TW_OK;
+}
+
+int ensure_state(tw_dyn* D) {
+    tw_ctx* ctx = D->ctx;
+    const size_t nv = (size_t)std::max(1, D->mesh->nv), ne = (size_t)std::max(1, D->mesh->ne);
+    DevMem* v24[] = {&D->hx, &D->hvel, &D->x0, &D->v0, &D->xk, &D->y};
+    for (DevMem* d : v24) CK(d->ensure(nv * 24));
+    DevMem* v32[] = {&D->grad, &D->b, &D->d, &D->r, &D->z, &D->p, &D->q, &D->best};
+    for (DevMem* d : v32) CK(d->ensure(nv * 32));
+    CK(D->sdiag.ensure(nv * 8));
+    CK(D->pre.ensure(nv * 72));
+    CK(D->vr_off.ensure((nv + 1) * 4));
+    CK(D->e_u.ensure(ne * 32));
+    CK(D->e_ab.ensure(ne * 16));
+    CK(D->rp_count.ensure(16));
+    CK(D->glob.ensure(sizeof(DynGlobals)));
+    if (D->rp_cap == 0) {
+        D->rp_cap = 1024;
+        CK(D->rp_ids.ensure((size_t)D->rp_cap * 16));
+        CK(D->rp_sw.ensure((size_t)D->rp_cap * 32));
+        CK(D->rp_dir.ensure((size_t)D->rp_cap * 32));
+        CK(D->rs_key.ensure((size_t)D->rp_cap * 32));
+        CK(D->rs_key2.ensure((size_t)D->rp_cap * 32));
+    }
+    return TW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void tw_default_energy_model(tw_energy_model* m) {  // EnergyModel defaults, dynamics.hpp:12-24
+    m->spring_stiffness = 50.0;
+    m->bending_stiffness = 0.0;
+    m->gravity[0] = 0.0, m->gravity[1] = 0.0, m->gravity[2] = -9.81;
+    m->repulsion_stiffness = 1e3;
+    m->repulsion_radius = 1e-3;
+    m->dt = 0.01;
+    m->newton_iters = 1;
+    m->mu = 0.0;
+    m->pcg_tol = 1e-6;
+    m->pcg_max_iters = 400;
+}
+
+int tw_dyn_create(tw_ctx* ctx, tw_mesh* m, const tw_energy_model* model, const double* rest_x, tw_dyn** out) {
+    if (!ctx || !m || !model || !rest_x || !out) return fail(ctx, TW_EINVAL, "dynamics: null argument");
+    if (!model_valid(*model)) return fail(ctx, TW_EINVAL, "dynamics: invalid energy model");
+    CK(cudaSetDevice(ctx->device));
+    auto* D = new tw_dyn();
+    D->ctx = ctx;
+    D->mesh = m;
+    D->model = *model;
+    // EnergyModel::prepare (dynamics.cpp:17-69): rest lengths and hinges
+    std::vector<double> rest(std::max(1, m->ne));
+    for (int e = 0; e < m->ne; ++e) {
+        const int i = m->edges[2 * e], j = m->edges[2 * e + 1];
+        const d3 d = sub(mk(rest_x[3 * i], rest_x[3 * i + 1], rest_x[3 * i + 2]),
+                         mk(rest_x[3 * j], rest_x[3 * j + 1], rest_x[3 * j + 2]));
+        rest[e] = nrm(d);
+    }
+    std::vector<int> hv;
+    std::vector<double> hk;
+    if (model->bending_stiffness > 0.0 && m->nt) {
+        std::vector<int32_t> tris((size_t)m->nt * 3);
+        std::vector<int4> t4(m->nt);
+        cudaMemcpy(t4.data(), m->d_tris.p, (size_t)m->nt * 16, cudaMemcpyDeviceToHost);
+        for (int t = 0; t < m->nt; ++t) tris[3 * t] = t4[t].x, tris[3 * t + 1] = t4[t].y, tris[3 * t + 2] = t4[t].z;
+        build_hinges(m, tris, rest_x, hv, hk);
+    }
+    D->nh = (int)hv.size() / 4;
+    // vertex -> (hinge, slot) in hinge order
+    std::vector<int> off(m->nv + 1, 0), lst(hv.size());
+    for (int v : hv) ++off[v + 1];
+    for (int v = 0; v < m->nv; ++v) off[v + 1] += off[v];
+    std::vector<int> fill(off.begin(), off.end() - 1);
+    for (int h = 0; h < D->nh; ++h)
+        for (int i = 0; i < 4; ++i) lst[fill[hv[4 * h + i]]++] = (h << 2) | i;
+    cudaError_t e = upload(D->rest, rest);
+    if (e == cudaSuccess) e = upload(D->hv, hv);
+    if (e == cudaSuccess) e = upload(D->hk, hk);
+    if (e == cudaSuccess) e = upload(D->vh_off, off);
+    if (e == cudaSuccess) e = upload(D->vh, lst);
+    if (e != cudaSuccess) {
+        delete D;
+        return cuda_fail(ctx, e, "tw_dyn_create");
+    }
+    const int rc = ensure_state(D);
+    if (rc) {
+        delete D;
+        return rc;
+    }
+    *out = D;
+    return TW_OK;
+}
+
+void tw_dyn_destroy(tw_dyn* D) {
+    if (!D) return;
+    cudaSetDevice(D->ctx ? D->ctx->device : 0);
+    DevMem* all[] = {&D->hx, &D->hvel, &D->rest, &D->hv, &D->hk, &D->vh_off, &D->vh, &D->x0, &D->v0, &D->xk, &D->y, &D->e_u,
+                     &D->e_ab, &D->rp_ids, &D->rp_sw, &D->rp_dir, &D->rp_count, &D->rs_key, &D->rs_key2,
+                     &D->vr_off, &D->sort_tmp, &D->sdiag, &D->grad, &D->pre, &D->b, &D->d, &D->r, &D->z,
+                     &D->p, &D->q, &D->best, &D->part, &D->glob};
+    for (DevMem* d : all) d->release();
+    delete D;
+}
+
+int32_t tw_dyn_num_hinges(const tw_dyn* D) { return D ? D->nh : 0; }
+
+int tw_newton_target(tw_ctx* ctx, tw_mesh* m, tw_dyn* D, double d_max, const double* x0, const double* v0,
+                     const double* x, double* y_out, double* grad_out, tw_step_stats* st) {
+    int rc = dyn_check(ctx, m, D);
+    if (rc) return rc;
+    if (!x0 || !v0 || !x || !y_out) return fail(ctx, TW_EINVAL, "newton_target: null argument");
+    if (!(d_max > 0.0)) return fail(ctx, TW_EINVAL, "newton_target: d_max must be > 0");
+    CK(cudaSetDevice(ctx->device));
+    const size_t bytes = (size_t)m->nv * 24;
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemcpyAsync(D->x0.p, x0, bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(D->v0.p, v0, bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(D->xk.p, x, bytes, cudaMemcpyHostToDevice, s));
+    tw_step_stats local;
+    std::memset(&local, 0, sizeof local);
+    local.pcg_converged = 1;
+    rc = newton_target_device(D, d_max, D->xk.as<double>(), D->y.as<double>(), &local, grad_out);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(y_out, D->y.p, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (st) *st = local;
+    return TW_OK;
+}
+
+int tw_step(tw_ctx* ctx, tw_mesh* m, tw_dyn* D, const tw_resolve_config* cfg, double* x, double* v,
+            tw_step_stats* st) {
+    int rc = dyn_check(ctx, m, D);
+    if (rc) return rc;
+    if (!x || !v) return fail(ctx, TW_EINVAL, "step: null argument");
+    rc = check_cfg(ctx, cfg);
+    if (rc) return rc;
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaSetDevice(ctx->device));
+    rc = ensure_buffers(ctx, m, *cfg);
+    if (rc) return rc;
+    const size_t bytes = (size_t)m->nv * 24;
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemcpyAsync(D->hx.p, x, bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(D->hvel.p, v, bytes, cudaMemcpyHostToDevice, s));
+    tw_step_stats local;
+    std::memset(&local, 0, sizeof local);
+    tw_resolve_config c = *cfg;
+    c.record_path = 0;
+    rc = step_device(ctx, m, D, &c, D->hx.as<double>(), D->hvel.as<double>(), &local);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(x, D->hx.p, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(v, D->hvel.p, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    local.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (st) *st = local;
+    return TW_OK;
+}
+
+int tw_step_device(tw_ctx* ctx, tw_mesh* m, tw_dyn* D, const tw_resolve_config* cfg, double* d_x, double* d_v,
+                   tw_step_stats* st) {
+    int rc = dyn_check(ctx, m, D);
+    if (rc) return rc;
+    if (!d_x || !d_v) return fail(ctx, TW_EINVAL, "step: null argument");
+    rc = check_cfg(ctx, cfg);
+    if (rc) return rc;
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaSetDevice(ctx->device));
+    rc = ensure_buffers(ctx, m, *cfg);
+    if (rc) return rc;
+    tw_step_stats local;
+    std::memset(&local, 0, sizeof local);
+    tw_resolve_config c = *cfg;
+    c.record_path = 0;
+    rc = step_device(ctx, m, D, &c, d_x, d_v, &local);
+    if (rc) return rc;
+    local.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (st) *st = local;
+    return TW_OK;
+}
+
+}  // extern "C"
