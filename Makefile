@@ -12,14 +12,13 @@ NVFLAGS   := $(ARCH) -O3 -std=c++17 -lineinfo -fmad=false -Xcompiler -fPIC -Iinc
 LIB       := $(PKG)/libtwoway_b200.so
 CU_SRCS   := $(CSRC)/tw_kernels.cu $(CSRC)/tw_capi.cu $(CSRC)/tw_dynamics.cu
 CU_HDRS   := $(CSRC)/tw_ctx.h $(CSRC)/tw_math.cuh $(CSRC)/tw_engine.cuh $(CSRC)/tw_phases.cuh $(CSRC)/tw_internal.h include/tw_c.h
-CPP_SRCS  := $(CSRC)/tw_api.cpp
 PY_EXT    := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_config_var('EXT_SUFFIX'))" 2>/dev/null)
 PYMOD     := $(PKG)/_twoway$(PY_EXT)
 PY_INC    := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_paths()['include'])" 2>/dev/null)
 PYBIND_INC:= $(shell $(PYTHON) -c "import pybind11;print(pybind11.get_include())" 2>/dev/null)
 
 BUILD     := build
-OBJS      := $(BUILD)/tw_kernels.o $(BUILD)/tw_capi.o $(BUILD)/tw_dynamics.o $(BUILD)/tw_api.o
+OBJS      := $(BUILD)/tw_kernels.o $(BUILD)/tw_capi.o $(BUILD)/tw_dynamics.o
 
 all: $(LIB) $(PYMOD) oracle
 
@@ -35,19 +34,16 @@ $(BUILD)/tw_capi.o: $(CSRC)/tw_capi.cu $(CU_HDRS) | $(BUILD)
 $(BUILD)/tw_dynamics.o: $(CSRC)/tw_dynamics.cu $(CU_HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_dynamics.log || (cat $(BUILD)/ptxas_dynamics.log; false)
 
-$(BUILD)/tw_api.o: $(CSRC)/tw_api.cpp include/twoway/*.hpp include/tw_c.h | $(BUILD)
-	$(CXX) -O2 -std=c++20 -fPIC -ffp-contract=off -Iinclude -c $< -o $@
-
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(OBJS) -lcudart_static -lrt -ldl -lpthread
 
-$(PYMOD): $(CSRC)/tw_pymodule.cpp $(LIB) include/twoway/*.hpp
-	$(CXX) -O2 -std=c++20 -fPIC -shared -Iinclude -I$(PY_INC) -I$(PYBIND_INC) $< -o $@ \
+$(PYMOD): $(CSRC)/tw_pymodule.cpp $(LIB) include/twoway/*.hpp include/twoway/detail/*.hpp include/tw_c.h
+	$(CXX) -O2 -std=c++20 -fPIC -shared -ffp-contract=off -Iinclude -I$(PY_INC) -I$(PYBIND_INC) $< -o $@ \
 	    -L$(PKG) -l:libtwoway_b200.so -Wl,-rpath,'$$ORIGIN'
 
 # The real reference (oracle/_ref, test infrastructure) is built only where its
 # sources exist (this container); the GPU box uses the prebuilt files.
-oracle:
+oracle: $(LIB)
 	$(MAKE) -s -C oracle
 	@if [ -d /root/reference/proj/src ]; then $(MAKE) -s -C oracle -f Makefile.ref -j8 all; fi
 

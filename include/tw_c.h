@@ -188,6 +188,53 @@ int tw_stage_backward(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t n
                       const double* x, const double* y_target, int32_t solver, int32_t sweeps,
                       double under_relax, double* lambda, double* q_out, double* y_out);
 
+/* The backward step split as the reference's lcp.hpp:36-53 splits it.
+ * mode: TW_LCP_ASSEMBLE = assemble_lcp (q = value + J (y - x), lcp.cpp:8-25;
+ * the warm-start impulse M^-1 J^T lambda accumulated in row order), TW_LCP_SOLVE
+ * = pgs_sweeps / projected_jacobi_sweeps (lcp.cpp:27-59) from the given q,
+ * lambda and impulse, TW_LCP_RECOVER = recover_target (lcp.cpp:131-136) into
+ * y_out. Without ASSEMBLE, q (nrows) and impulse (nv * 3) are inputs; lambda
+ * and impulse are written back after the sweeps; q is written by ASSEMBLE. */
+enum { TW_LCP_ASSEMBLE = 1, TW_LCP_SOLVE = 2, TW_LCP_RECOVER = 4 };
+int tw_stage_lcp(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t nrows, const int32_t* verts,
+                 const double* value, const double* jac, const double* diag, const int32_t* color, int32_t ncolors,
+                 const double* x, const double* y_target, int32_t solver, int32_t sweeps, double under_relax,
+                 int32_t mode, double* lambda, double* q, double* impulse, double* y_out);
+
+/* Row flavors (Constraint::Flavor, constraints.hpp:31) */
+enum { TW_FLAVOR_VOLUME = 0, TW_FLAVOR_GAP = 1, TW_FLAVOR_LENGTH = 2 };
+
+/* linearize_all plus each row's re-evaluation data (Constraint::flavor,
+ * ref_volume, gap_weights[4], denom; constraints.hpp:26-33) for
+ * constraint_value_at. Same arguments as tw_stage_linearize plus the four
+ * outputs (R entries; gap_weights 4 per row). */
+int tw_stage_linearize_ex(tw_ctx* ctx, tw_mesh* mesh, const double* x, int64_t np, const uint64_t* keys,
+                          const double* dist, const double* wa, const double* wb, const double* dir,
+                          const uint8_t* flags, const double* edge_targets, double delta, double sigma,
+                          int32_t family, int32_t edge_constraints, int64_t cap, uint8_t* kind, int32_t* verts,
+                          double* value, double* jac, double* diag, uint64_t* pair_key, int32_t* edge_index,
+                          uint8_t* flavor, double* ref_volume, double* gap_weights, double* denom, int64_t* nrows);
+
+/* build_vt / build_ee / build_vv / build_ve_constraint (constraints.cpp:78-142;
+ * gap = 0: by the pair kinds with the reference's gap fallbacks) or
+ * build_gap_constraint (constraints.cpp:56-76; gap = 1) for n pairs given as
+ * kinds (2n: ka, kb), simplex vertex ids (6n, -1 padded) and cached closest
+ * results (11n, the tw_stage_closest layout). Rows carry no diag (fill it
+ * with tw_stage_fill_diag). */
+int tw_stage_build_rows(tw_ctx* ctx, int32_t nv, const double* x, int64_t n, const int32_t* kinds,
+                        const int32_t* verts, const double* closest, double delta, int32_t gap, uint8_t* kind,
+                        int32_t* nverts, int32_t* row_verts, double* value, double* jac, uint8_t* flavor,
+                        double* ref_volume, double* gap_weights, double* denom);
+
+/* constraint_value_at (constraints.cpp:39-54) of n rows at x. */
+int tw_stage_constraint_value(tw_ctx* ctx, int32_t nv, const double* x, int64_t n, const uint8_t* flavor,
+                              const int32_t* nverts, const int32_t* row_verts, const double* ref_volume,
+                              const double* gap_weights, const double* denom, const double* sigma, double* out);
+
+/* fill_diag (constraints.cpp:175-179) of n rows. */
+int tw_stage_fill_diag(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t n, const int32_t* nverts,
+                       const int32_t* row_verts, const double* jac, double* diag);
+
 /* advance (advance.cpp:8-39): x and r in/out, D = per-vertex bound. */
 int tw_stage_advance(tw_ctx* ctx, int32_t nv, const double* inv_mass, const double* y,
                      const double* D, double gamma, double* x, double* r, double* max_disp);
@@ -256,6 +303,14 @@ int tw_step(tw_ctx* ctx, tw_mesh* mesh, tw_dyn* dyn, const tw_resolve_config* cf
 /* Same on device-resident state (HBM pointers, nv * 3 doubles each). */
 int tw_step_device(tw_ctx* ctx, tw_mesh* mesh, tw_dyn* dyn, const tw_resolve_config* cfg, double* d_x, double* d_v,
                    tw_step_stats* stats);
+
+
+/* normal_flow_target (normal_flow.cpp:38-81; the validation of
+ * require_closed_manifold, normal_flow.cpp:24-36, -> TW_EINVAL): area-weighted
+ * unit normals, the offset y = x + beta n, cotangent edge weights and three
+ * Jacobi smoothing passes scaled by alpha_smooth, on the device. */
+int tw_normal_flow_target(tw_ctx* ctx, int32_t nv, const double* x, int32_t nt, const int32_t* triangles,
+                          double beta, double alpha_smooth, double* y_out);
 
 #ifdef __cplusplus
 }

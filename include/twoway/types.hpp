@@ -18,6 +18,7 @@ namespace twoway {
 
 #ifdef TWOWAY_USE_EIGEN
 using Vec3 = Eigen::Vector3d;
+using Mat3 = Eigen::Matrix3d;
 #else
 class Vec3 {
 public:
@@ -90,6 +91,79 @@ private:
 
 inline Vec3 operator*(double s, const Vec3& v) { return {s * v.x(), s * v.y(), s * v.z()}; }
 static_assert(sizeof(Vec3) == 24, "Vec3 must have the byte layout of Eigen::Vector3d");
+
+/// 3x3 FP64 matrix (the reference's Mat3 = Eigen::Matrix3d, types.hpp:11),
+/// column-major like Eigen, with the members the reference's dynamics code
+/// uses: Zero/Identity, (r, c), + - and scalar products, transpose, M * v
+/// (row sums (m0 v0 + m1 v1) + m2 v2) and the outer product outer(u, v).
+class Mat3 {
+public:
+    constexpr Mat3() : m_{0, 0, 0, 0, 0, 0, 0, 0, 0} {}
+    static constexpr Mat3 Zero() { return Mat3(); }
+    static constexpr Mat3 Identity() {
+        Mat3 m;
+        m.m_[0] = m.m_[4] = m.m_[8] = 1.0;
+        return m;
+    }
+    static Mat3 outer(const Vec3& u, const Vec3& v) {
+        Mat3 m;
+        for (int c = 0; c < 3; ++c)
+            for (int r = 0; r < 3; ++r) m(r, c) = u[r] * v[c];
+        return m;
+    }
+    double& operator()(int r, int c) { return m_[r + 3 * c]; }
+    double operator()(int r, int c) const { return m_[r + 3 * c]; }
+    double* data() { return m_; }
+    const double* data() const { return m_; }
+
+    Mat3 operator+(const Mat3& o) const { return zip(o, [](double a, double b) { return a + b; }); }
+    Mat3 operator-(const Mat3& o) const { return zip(o, [](double a, double b) { return a - b; }); }
+    Mat3 operator-() const { return zip(*this, [](double a, double) { return -a; }); }
+    Mat3 operator*(double s) const { return zip(*this, [s](double a, double) { return a * s; }); }
+    Mat3 operator/(double s) const { return zip(*this, [s](double a, double) { return a / s; }); }
+    Mat3& operator+=(const Mat3& o) { return *this = *this + o; }
+    Mat3& operator-=(const Mat3& o) { return *this = *this - o; }
+    Mat3& operator*=(double s) { return *this = *this * s; }
+    bool operator==(const Mat3& o) const {
+        for (int i = 0; i < 9; ++i)
+            if (m_[i] != o.m_[i]) return false;
+        return true;
+    }
+    Vec3 operator*(const Vec3& v) const {
+        Vec3 out;
+        for (int r = 0; r < 3; ++r) out[r] = ((*this)(r, 0) * v[0] + (*this)(r, 1) * v[1]) + (*this)(r, 2) * v[2];
+        return out;
+    }
+    Mat3 operator*(const Mat3& o) const {
+        Mat3 out;
+        for (int c = 0; c < 3; ++c) {
+            Vec3 col = *this * Vec3(o(0, c), o(1, c), o(2, c));
+            for (int r = 0; r < 3; ++r) out(r, c) = col[r];
+        }
+        return out;
+    }
+    Mat3 transpose() const {
+        Mat3 t;
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) t(c, r) = (*this)(r, c);
+        return t;
+    }
+    Vec3 col(int c) const { return {(*this)(0, c), (*this)(1, c), (*this)(2, c)}; }
+    Vec3 row(int r) const { return {(*this)(r, 0), (*this)(r, 1), (*this)(r, 2)}; }
+    double trace() const { return ((*this)(0, 0) + (*this)(1, 1)) + (*this)(2, 2); }
+
+private:
+    template <typename F>
+    Mat3 zip(const Mat3& o, F f) const {
+        Mat3 out;
+        for (int i = 0; i < 9; ++i) out.m_[i] = f(m_[i], o.m_[i]);
+        return out;
+    }
+    double m_[9];
+};
+
+inline Mat3 operator*(double s, const Mat3& m) { return m * s; }
+static_assert(sizeof(Mat3) == 72, "Mat3 must have the byte layout of Eigen::Matrix3d");
 #endif
 
 using Positions = std::vector<Vec3>;

@@ -458,6 +458,39 @@ int check_cfg(tw_ctx* ctx, const tw_resolve_config* cfg) {
 
 using namespace tw::host;
 
+namespace {
+struct Scratch {  // per-call device buffers of the row stage entries
+    std::vector<void*> ptrs;
+    cudaError_t err = cudaSuccess;
+    template <typename T>
+    T* up(const T* host, size_t n) {
+        void* p = nullptr;
+        if (err == cudaSuccess) err = cudaMalloc(&p, std::max<size_t>(16, n * sizeof(T)));
+        if (err == cudaSuccess && host && n) err = cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice);
+        if (p) ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    template <typename T>
+    T* out(size_t n) {
+        return up<T>(nullptr, n);
+    }
+    template <typename T>
+    void down(T* host, const T* dev, size_t n) {
+        if (err == cudaSuccess && host && n) err = cudaMemcpy(host, dev, n * sizeof(T), cudaMemcpyDeviceToHost);
+    }
+    ~Scratch() {
+        for (void* p : ptrs) cudaFree(p);
+    }
+};
+
+double4* upload_x4(Scratch& S, int32_t nv, const double* x, const double* inv_mass) {
+    std::vector<double4> x4(std::max(1, nv));
+    for (int v = 0; v < nv; ++v)
+        x4[v] = make_double4(x[3 * v], x[3 * v + 1], x[3 * v + 2], inv_mass ? inv_mass[v] : 1.0);
+    return S.up(x4.data(), x4.size());
+}
+}  // namespace
+
 // ================================================================= C-ABI
 extern "C" {
 
@@ -1244,9 +1277,22 @@ int tw_stage_backward(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t n
                       const double* value, const double* jac, const double* diag, const int32_t* color,
                       int32_t ncolors, const double* x, const double* y_target, int32_t solver, int32_t sweeps,
                       double under_relax, double* lambda, double* q_out, double* y_out) {
-    if (!ctx || nv < 0 || !inv_mass || nrows < 0 ||
-        (nrows && (!verts || !value || !jac || !diag || !lambda)) || !x || !y_target || !y_out || sweeps < 1 ||
-        (solver == TW_SOLVER_PGS && nrows && (!color || ncolors < 1)))
+    if (!y_out) return fail(ctx, TW_EINVAL, "backward: bad argument");
+    return tw_stage_lcp(ctx, nv, inv_mass, nrows, verts, value, jac, diag, color, ncolors, x, y_target, solver,
+                        sweeps, under_relax, TW_LCP_ASSEMBLE | TW_LCP_SOLVE | TW_LCP_RECOVER, lambda, q_out,
+                        nullptr, y_out);
+}
+
+int tw_stage_lcp(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t nrows, const int32_t* verts,
+                 const double* value, const double* jac, const double* diag, const int32_t* color, int32_t ncolors,
+                 const double* x, const double* y_target, int32_t solver, int32_t sweeps, double under_relax,
+                 int32_t mode, double* lambda, double* q, double* impulse, double* y_out) {
+    const bool assemble = mode & TW_LCP_ASSEMBLE, solve = mode & TW_LCP_SOLVE, recover = mode & TW_LCP_RECOVER;
+    if (!ctx || nv < 0 || !inv_mass || nrows < 0 || (mode & ~7) || !mode ||
+        (nrows && (!verts || !jac || !lambda)) || (nrows && assemble && !value) || (nrows && solve && !diag) ||
+        ((assemble || recover) && !y_target) || (assemble && !x) || (recover && !y_out) ||
+        (!assemble && (solve || recover) && !impulse) || (!assemble && solve && nrows && !q) || sweeps < 1 ||
+        (solve && solver == TW_SOLVER_PGS && nrows && (!color || ncolors < 1)))
         return fail(ctx, TW_EINVAL, "backward: bad argument");
     if (solver != TW_SOLVER_PGS && solver != TW_SOLVER_JACOBI)
         return fail(ctx, TW_EUNSUPPORTED, "backward: only pgs and jacobi run on the device");
@@ -1279,10 +1325,11 @@ int tw_stage_backward(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t n
     if (rc) return rc;
     cudaStream_t s = ctx->stream;
     const size_t n = (size_t)std::max(1, nv);
-    std::vector<double4> x4(n), y4(n);
+    std::vector<double4> x4(n), y4(n), imp4(n);
     for (int v = 0; v < nv; ++v) {
-        x4[v] = make_double4(x[3 * v], x[3 * v + 1], x[3 * v + 2], inv_mass[v]);
-        y4[v] = make_double4(y_target[3 * v], y_target[3 * v + 1], y_target[3 * v + 2], inv_mass[v]);
+        if (x) x4[v] = make_double4(x[3 * v], x[3 * v + 1], x[3 * v + 2], inv_mass[v]);
+        if (y_target) y4[v] = make_double4(y_target[3 * v], y_target[3 * v + 1], y_target[3 * v + 2], inv_mass[v]);
+        if (impulse) imp4[v] = make_double4(impulse[3 * v], impulse[3 * v + 1], impulse[3 * v + 2], inv_mass[v]);
     }
     std::vector<int4> ids(std::max<int64_t>(1, nrows));
     for (int64_t i = 0; i < nrows; ++i)
@@ -1292,27 +1339,211 @@ int tw_stage_backward(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t n
     if (nrows) {
         CK(cudaMemcpyAsync(ctx->c_ids.p, ids.data(), nrows * 16, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(ctx->c_jac.p, jac, nrows * 96, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(ctx->c_value.p, value, nrows * 8, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(ctx->c_diag.p, diag, nrows * 8, cudaMemcpyHostToDevice, s));
+        if (value) CK(cudaMemcpyAsync(ctx->c_value.p, value, nrows * 8, cudaMemcpyHostToDevice, s));
+        if (diag) CK(cudaMemcpyAsync(ctx->c_diag.p, diag, nrows * 8, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(ctx->c_lambda.p, lambda, nrows * 8, cudaMemcpyHostToDevice, s));
-        if (solver == TW_SOLVER_PGS) CK(cudaMemcpyAsync(ctx->c_color.p, color, nrows * 4, cudaMemcpyHostToDevice, s));
+        if (!assemble && q) CK(cudaMemcpyAsync(ctx->c_q.p, q, nrows * 8, cudaMemcpyHostToDevice, s));
+        if (solve && solver == TW_SOLVER_PGS)
+            CK(cudaMemcpyAsync(ctx->c_color.p, color, nrows * 4, cudaMemcpyHostToDevice, s));
     }
+    if (!assemble) CK(cudaMemcpyAsync(ctx->imp.p, imp4.data(), n * 32, cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(ctx->vcnt.p, 0, n * 4, s));
     CK(cudaMemsetAsync(ctx->ccount.p, 0, (size_t)ctx->colcap * 4, s));
     CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), s));
     Params P = make_params(ctx, m, cfg);
-    CK(coop_stage_backward(s, P, ctx->nblocks, nrows, solver == TW_SOLVER_PGS ? ncolors : 0));
+    CK(coop_stage_backward(s, P, ctx->nblocks, nrows, solver == TW_SOLVER_PGS ? ncolors : 0, mode));
     ++ctx->launches;
     Globals G;
     CK(cudaMemcpyAsync(&G, ctx->globals.p, sizeof G, cudaMemcpyDeviceToHost, s));
     if (nrows) {
         CK(cudaMemcpyAsync(lambda, ctx->c_lambda.p, nrows * 8, cudaMemcpyDeviceToHost, s));
-        if (q_out) CK(cudaMemcpyAsync(q_out, ctx->c_q.p, nrows * 8, cudaMemcpyDeviceToHost, s));
+        if (assemble && q) CK(cudaMemcpyAsync(q, ctx->c_q.p, nrows * 8, cudaMemcpyDeviceToHost, s));
     }
-    CK(cudaMemcpyAsync(x4.data(), ctx->x.p, n * 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(imp4.data(), ctx->imp.p, n * 32, cudaMemcpyDeviceToHost, s));
+    if (recover) CK(cudaMemcpyAsync(x4.data(), ctx->x.p, n * 32, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (G.error) return fail(ctx, TW_ETIMEOUT, "backward: device error");
-    for (int v = 0; v < nv; ++v) y_out[3 * v] = x4[v].x, y_out[3 * v + 1] = x4[v].y, y_out[3 * v + 2] = x4[v].z;
+    if (recover)
+        for (int v = 0; v < nv; ++v) y_out[3 * v] = x4[v].x, y_out[3 * v + 1] = x4[v].y, y_out[3 * v + 2] = x4[v].z;
+    if (impulse)
+        for (int v = 0; v < nv; ++v)
+            impulse[3 * v] = imp4[v].x, impulse[3 * v + 1] = imp4[v].y, impulse[3 * v + 2] = imp4[v].z;
+    return TW_OK;
+}
+
+
+int tw_stage_build_rows(tw_ctx* ctx, int32_t nv, const double* x, int64_t n, const int32_t* kinds,
+                        const int32_t* verts, const double* closest, double delta, int32_t gap, uint8_t* kind,
+                        int32_t* nverts, int32_t* row_verts, double* value, double* jac, uint8_t* flavor,
+                        double* ref_volume, double* gap_weights, double* denom) {
+    if (!ctx || nv < 0 || n < 0 || !x || (n && (!kinds || !verts || !closest || !kind || !nverts || !row_verts ||
+                                                 !value || !jac || !flavor || !ref_volume || !gap_weights || !denom)) ||
+        !(delta > 0.0))
+        return fail(ctx, TW_EINVAL, "build_rows: bad argument");
+    for (int64_t i = 0; i < n; ++i) {
+        const int ka = kinds[2 * i], kb = kinds[2 * i + 1];
+        const bool ok = (ka == 0 && (kb == 0 || kb == 1 || kb == 2)) || (ka == 1 && kb == 1);
+        if (!ok) return fail(ctx, TW_EINVAL, "build_rows: unsupported pair kinds");
+        for (int k = 0; k < 6; ++k)
+            if (verts[6 * i + k] >= nv) return fail(ctx, TW_EINVAL, "build_rows: vertex id out of range");
+    }
+    CK(cudaSetDevice(ctx->device));
+    if (!n) return TW_OK;
+    Scratch S;
+    const double4* dx = upload_x4(S, nv, x, nullptr);
+    const int* dk = S.up(kinds, 2 * (size_t)n);
+    const int* dv = S.up(verts, 6 * (size_t)n);
+    const double* dc = S.up(closest, 11 * (size_t)n);
+    int *okind = S.out<int>(n), *onv = S.out<int>(n), *orv = S.out<int>(4 * n), *ofl = S.out<int>(n);
+    double *oval = S.out<double>(n), *ojac = S.out<double>(12 * n), *orefv = S.out<double>(n),
+           *ogw = S.out<double>(4 * n), *oden = S.out<double>(n);
+    if (S.err) return cuda_fail(ctx, S.err, "build_rows: upload");
+    launch_build_rows(nullptr, dx, n, dk, dv, dc, delta, gap ? 1 : 0, okind, onv, orv, oval, ojac, ofl, orefv, ogw,
+                      oden);
+    ++ctx->launches;
+    CK(cudaDeviceSynchronize());
+    std::vector<int> hk(n), hf(n);
+    S.down(hk.data(), okind, n);
+    S.down(nverts, onv, n);
+    S.down(row_verts, orv, 4 * n);
+    S.down(value, oval, n);
+    S.down(jac, ojac, 12 * n);
+    S.down(hf.data(), ofl, n);
+    S.down(ref_volume, orefv, n);
+    S.down(gap_weights, ogw, 4 * n);
+    S.down(denom, oden, n);
+    if (S.err) return cuda_fail(ctx, S.err, "build_rows: download");
+    for (int64_t i = 0; i < n; ++i) kind[i] = (uint8_t)hk[i], flavor[i] = (uint8_t)hf[i];
+    return TW_OK;
+}
+
+int tw_stage_constraint_value(tw_ctx* ctx, int32_t nv, const double* x, int64_t n, const uint8_t* flavor,
+                              const int32_t* nverts, const int32_t* row_verts, const double* ref_volume,
+                              const double* gap_weights, const double* denom, const double* sigma, double* out) {
+    if (!ctx || nv < 0 || n < 0 || !x ||
+        (n && (!flavor || !nverts || !row_verts || !ref_volume || !gap_weights || !denom || !sigma || !out)))
+        return fail(ctx, TW_EINVAL, "constraint_value: bad argument");
+    for (int64_t i = 0; i < n; ++i) {
+        if (flavor[i] > 2 || nverts[i] < 1 || nverts[i] > 4) return fail(ctx, TW_EINVAL, "constraint_value: bad row");
+        for (int k = 0; k < nverts[i]; ++k)
+            if (row_verts[4 * i + k] < 0 || row_verts[4 * i + k] >= nv)
+                return fail(ctx, TW_EINVAL, "constraint_value: vertex id out of range");
+    }
+    CK(cudaSetDevice(ctx->device));
+    if (!n) return TW_OK;
+    Scratch S;
+    std::vector<int> fl(flavor, flavor + n);
+    const double4* dx = upload_x4(S, nv, x, nullptr);
+    const int* df = S.up(fl.data(), n);
+    const int* dn = S.up(nverts, n);
+    const int* dv = S.up(row_verts, 4 * (size_t)n);
+    const double* drv = S.up(ref_volume, n);
+    const double* dg = S.up(gap_weights, 4 * (size_t)n);
+    const double* dd = S.up(denom, n);
+    const double* ds = S.up(sigma, n);
+    double* dout = S.out<double>(n);
+    if (S.err) return cuda_fail(ctx, S.err, "constraint_value: upload");
+    launch_value_at(nullptr, dx, n, df, dn, dv, drv, dg, dd, ds, dout);
+    ++ctx->launches;
+    CK(cudaDeviceSynchronize());
+    S.down(out, dout, n);
+    if (S.err) return cuda_fail(ctx, S.err, "constraint_value: download");
+    return TW_OK;
+}
+
+int tw_stage_fill_diag(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t n, const int32_t* nverts,
+                       const int32_t* row_verts, const double* jac, double* diag) {
+    if (!ctx || nv < 0 || n < 0 || !inv_mass || (n && (!nverts || !row_verts || !jac || !diag)))
+        return fail(ctx, TW_EINVAL, "fill_diag: bad argument");
+    for (int64_t i = 0; i < n; ++i) {
+        if (nverts[i] < 0 || nverts[i] > 4) return fail(ctx, TW_EINVAL, "fill_diag: bad row");
+        for (int k = 0; k < nverts[i]; ++k)
+            if (row_verts[4 * i + k] < 0 || row_verts[4 * i + k] >= nv)
+                return fail(ctx, TW_EINVAL, "fill_diag: vertex id out of range");
+    }
+    CK(cudaSetDevice(ctx->device));
+    if (!n) return TW_OK;
+    Scratch S;
+    const double* dm = S.up(inv_mass, nv);
+    const int* dn = S.up(nverts, n);
+    const int* dv = S.up(row_verts, 4 * (size_t)n);
+    const double* dj = S.up(jac, 12 * (size_t)n);
+    double* dd = S.out<double>(n);
+    if (S.err) return cuda_fail(ctx, S.err, "fill_diag: upload");
+    launch_fill_diag(nullptr, dm, n, dn, dv, dj, dd);
+    ++ctx->launches;
+    CK(cudaDeviceSynchronize());
+    S.down(diag, dd, n);
+    if (S.err) return cuda_fail(ctx, S.err, "fill_diag: download");
+    return TW_OK;
+}
+
+int tw_stage_linearize_ex(tw_ctx* ctx, tw_mesh* m, const double* x, int64_t np, const uint64_t* keys,
+                          const double* dist, const double* wa, const double* wb, const double* dir,
+                          const uint8_t* flags, const double* edge_targets, double delta, double sigma,
+                          int32_t family, int32_t edge_constraints, int64_t cap, uint8_t* kind, int32_t* verts,
+                          double* value, double* jac, double* diag, uint64_t* pair_key, int32_t* edge_index,
+                          uint8_t* flavor, double* ref_volume, double* gap_weights, double* denom, int64_t* nrows) {
+    int rc = tw_stage_linearize(ctx, m, x, np, keys, dist, wa, wb, dir, flags, edge_targets, delta, sigma, family,
+                                edge_constraints, cap, kind, verts, value, jac, diag, pair_key, edge_index, nrows);
+    if (rc) return rc;
+    if (!flavor || !ref_volume || !gap_weights || !denom) return fail(ctx, TW_EINVAL, "linearize_ex: null output");
+    const int64_t R = *nrows;
+    // contact rows: their re-evaluation data from the device row builder on
+    // the same pair records (pair order = key order)
+    std::vector<int32_t> kinds, pv;
+    std::vector<double> cl;
+    std::vector<int64_t> rows;
+    for (int64_t i = 0; i < R; ++i) {
+        if (kind[i] == 4) continue;
+        const uint64_t k = pair_key[i];
+        const int64_t p = std::lower_bound(keys, keys + np, k) - keys;
+        const int ka = (int)(k >> 62), kb = (int)((k >> 60) & 3);
+        const int ia = (int)((k >> 30) & 0x3fffffff), ib = (int)(k & 0x3fffffff);
+        int va[3] = {-1, -1, -1}, vb[3] = {-1, -1, -1};
+        if (ka == 0) va[0] = ia;
+        else va[0] = m->edges[2 * ia], va[1] = m->edges[2 * ia + 1];
+        if (kb == 0) vb[0] = ib;
+        else if (kb == 1) vb[0] = m->edges[2 * ib], vb[1] = m->edges[2 * ib + 1];
+        else vb[0] = verts[4 * i + 1], vb[1] = verts[4 * i + 2], vb[2] = verts[4 * i + 3];  // VT: (a, t0, t1, t2)
+        if (kb == 2 && kind[i] != 0) {  // a VT gap row keeps the same vertex order
+            vb[0] = verts[4 * i + 1], vb[1] = verts[4 * i + 2], vb[2] = verts[4 * i + 3];
+        }
+        kinds.insert(kinds.end(), {ka, kb});
+        pv.insert(pv.end(), {va[0], va[1], va[2], vb[0], vb[1], vb[2]});
+        cl.push_back(dist[p]);
+        for (int c = 0; c < 3; ++c) cl.push_back(wa[3 * p + c]);
+        for (int c = 0; c < 3; ++c) cl.push_back(wb[3 * p + c]);
+        for (int c = 0; c < 3; ++c) cl.push_back(dir[3 * p + c]);
+        cl.push_back((flags[p] & PF_DEGENERATE) ? 1.0 : 0.0);
+        rows.push_back(i);
+    }
+    const int64_t nc = (int64_t)rows.size();
+    if (nc) {
+        std::vector<uint8_t> k2(nc), f2(nc);
+        std::vector<int32_t> n2(nc), v2(4 * nc);
+        std::vector<double> val2(nc), j2(12 * nc), rv2(nc), g2(4 * nc), d2(nc);
+        rc = tw_stage_build_rows(ctx, m->nv, x, nc, kinds.data(), pv.data(), cl.data(), delta, family, k2.data(),
+                                 n2.data(), v2.data(), val2.data(), j2.data(), f2.data(), rv2.data(), g2.data(),
+                                 d2.data());
+        if (rc) return rc;
+        for (int64_t r = 0; r < nc; ++r) {
+            const int64_t i = rows[r];
+            if (val2[r] != value[i] && !(std::isnan(val2[r]) && std::isnan(value[i])))
+                return fail(ctx, TW_ECUDA, "linearize_ex: row builder disagrees with the linearization");
+            flavor[i] = f2[r];
+            ref_volume[i] = rv2[r];
+            for (int c = 0; c < 4; ++c) gap_weights[4 * i + c] = g2[4 * r + c];
+            denom[i] = d2[r];
+        }
+    }
+    for (int64_t i = 0; i < R; ++i)
+        if (kind[i] == 4) {
+            flavor[i] = 2;
+            ref_volume[i] = 0.0;
+            for (int c = 0; c < 4; ++c) gap_weights[4 * i + c] = 0.0;
+            denom[i] = edge_targets[edge_index[i]];
+        }
     return TW_OK;
 }
 

@@ -35,6 +35,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <utility>
 #include <vector>
 
 #include "tw_ctx.h"
@@ -504,6 +505,65 @@ __global__ void k_velocity(int nv, const double* inv_mass, const double* x, cons
     vel[i] = inv_mass[i / 3] == 0.0 ? 0.0 : (x[i] - x0[i]) / dt;
 }
 
+
+// ---------------------------------------------------------- normal flow
+// normal_flow_target (normal_flow.cpp:38-81): area-weighted unit normals
+// (per-vertex gather over the incident triangles in triangle order), the
+// offset y = x + beta n, cotangent edge weights (per edge over its triangles
+// in triangle order), then three Jacobi smoothing passes whose per-vertex sums
+// run over the neighbours in ascending id -- the iteration order of the
+// reference's std::map keyed (min, max).
+__global__ void k_nf_offset(int nv, const double* x, const int* vt_off, const int* vt, const int4* tris, double beta,
+                            double* y) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    d3 n = mk(0, 0, 0);
+    for (int k = vt_off[v]; k < vt_off[v + 1]; ++k) {
+        const int4 t = tris[vt[k]];
+        const d3 p0 = ld3(x, t.x);
+        n = add(n, scl(0.5, crs(sub(ld3(x, t.y), p0), sub(ld3(x, t.z), p0))));
+    }
+    const double l = nrm(n);
+    if (l > 1e-18) n = dvd(n, l);
+    const d3 o = add(ld3(x, v), scl(beta, n));
+    y[3 * v] = o.x, y[3 * v + 1] = o.y, y[3 * v + 2] = o.z;
+}
+
+// w_e = sum over the (t, k) occurrences of the edge of 0.5 cot(angle at the opposite corner)
+__global__ void k_nf_weights(int ne, const int* occ_off, const int* occ, const int4* tris, const double* y, double* w) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= ne) return;
+    double acc = 0.0;
+    for (int k = occ_off[e]; k < occ_off[e + 1]; ++k) {
+        const int4 t4 = tris[occ[k] >> 2];
+        const int c = occ[k] & 3;
+        const int tv[3] = {t4.x, t4.y, t4.z};
+        const int a = tv[c], b = tv[(c + 1) % 3], o = tv[(c + 2) % 3];
+        const d3 u = sub(ld3(y, a), ld3(y, o)), q = sub(ld3(y, b), ld3(y, o));
+        const double cr = nrm(crs(u, q));
+        acc += 0.5 * (dot(u, q) / maxd(cr, 1e-18));
+    }
+    w[e] = acc;
+}
+
+__global__ void k_nf_smooth(int nv, const int* nb_off, const int2* nb, const double* w, double alpha, const double* y,
+                            double* y_next) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    const d3 yv = ld3(y, v);
+    d3 lap = mk(0, 0, 0);
+    double ws = 0.0;
+    for (int k = nb_off[v]; k < nb_off[v + 1]; ++k) {
+        const int2 n = nb[k];  // (neighbour, edge)
+        const double we = maxd(w[n.y], 1e-6);
+        lap = add(lap, scl(we, sub(ld3(y, n.x), yv)));
+        ws += we;
+    }
+    d3 o = yv;
+    if (ws > 0.0) o = add(yv, dvd(scl(alpha, lap), ws));
+    y_next[3 * v] = o.x, y_next[3 * v + 1] = o.y, y_next[3 * v + 2] = o.z;
+}
+
 }  // namespace dyn
 }  // namespace tw
 
@@ -652,6 +712,20 @@ DynParams make_dparams(tw_dyn* D, const double* d_x) {
     return P;
 }
 
+// TW_DEBUG_SYNC=1: synchronize after every dynamics launch and name the failing one
+int debug_sync(tw_ctx* ctx, const char* what) {
+    static const bool on = getenv("TW_DEBUG_SYNC") != nullptr;
+    if (!on) return TW_OK;
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, what);
+    return TW_OK;
+}
+#define DSYNC(name)                               \
+    do {                                          \
+        const int _r = debug_sync(ctx, name);     \
+        if (_r) return _r;                        \
+    } while (0)
+
 int pcg_blocks(tw_ctx* ctx, int nv) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg, DTPB, 0);
@@ -704,6 +778,7 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
     CK(ctx->x.ensure((size_t)std::max(1, nv) * 32));
     k_pack_x4<<<std::max(1, nb), DTPB, 0, s>>>(nv, d_xk, m->d_inv_mass.as<double>(), ctx->x.as<double4>());
     ++ctx->launches;
+    DSYNC("k_pack_x4");
     long long np = 0;
     int rc = search_at_x(ctx, m, d_max, &np);
     if (rc) return rc;
@@ -721,10 +796,12 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
     if (m->ne) {
         k_edges<<<(m->ne + DTPB - 1) / DTPB, DTPB, 0, s>>>(P);
         ++ctx->launches;
+        DSYNC("k_edges");
     }
     if (np && D->model.repulsion_stiffness > 0.0) {
         k_rep_pairs<<<(unsigned)((np + DTPB - 1) / DTPB), DTPB, 0, s>>>(P);
         ++ctx->launches;
+        DSYNC("k_rep_pairs");
     }
     int counts[2] = {0, 0};
     CK(cudaMemcpyAsync(counts, D->rp_count.p, 8, cudaMemcpyDeviceToHost, s));
@@ -740,8 +817,11 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
         ctx->launches += 4;
         P.rs_key = D->rs_key2.as<unsigned long long>();
     }
+    DSYNC("sort");
     k_rep_offsets<<<(nv + 1 + DTPB - 1) / DTPB, DTPB, 0, s>>>(P.rs_key, nent, nv, P.vr_off);
+    DSYNC("k_rep_offsets");
     k_grad_diag<<<std::max(1, nb), DTPB, 0, s>>>(P);
+    DSYNC("k_grad_diag");
     ctx->launches += 2;
     if (grad_host) {
         std::vector<double4> g(nv);
@@ -752,10 +832,12 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
     const int pb = pcg_blocks(ctx, nv);
     P.nblocks = pb;
     CK(D->part.ensure((size_t)pb * 32));
+    P.part = D->part.as<double>();
     CK(cudaMemsetAsync(D->glob.p, 0, sizeof(DynGlobals), s));
     void* args[] = {&P};
     CK(cudaLaunchCooperativeKernel((void*)k_pcg, dim3(pb), dim3(DTPB), args, 0, s));
     ++ctx->launches;
+    DSYNC("k_pcg");
     DynGlobals G;
     CK(cudaMemcpyAsync(&G, D->glob.p, sizeof G, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -990,6 +1072,119 @@ int tw_step_device(tw_ctx* ctx, tw_mesh* m, tw_dyn* D, const tw_resolve_config* 
     if (rc) return rc;
     local.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (st) *st = local;
+    return TW_OK;
+}
+
+
+int tw_normal_flow_target(tw_ctx* ctx, int32_t nv, const double* x, int32_t nt, const int32_t* triangles,
+                          double beta, double alpha_smooth, double* y_out) {
+    if (!ctx || nv < 0 || nt < 0 || !x || !y_out || (nt && !triangles))
+        return fail(ctx, TW_EINVAL, "normal flow: null argument");
+    // require_closed_manifold (normal_flow.cpp:24-36): every directed edge once,
+    // and its reverse exactly once
+    if (nt == 0) return fail(ctx, TW_EINVAL, "normal flow: no triangles");
+    std::vector<uint64_t> dir;
+    dir.reserve(3 * (size_t)nt);
+    for (int t = 0; t < nt; ++t)
+        for (int k = 0; k < 3; ++k) {
+            const int a = triangles[3 * t + k], b = triangles[3 * t + (k + 1) % 3];
+            if (a < 0 || a >= nv || b < 0 || b >= nv) return fail(ctx, TW_EINVAL, "normal flow: vertex id out of range");
+            dir.push_back(((uint64_t)(uint32_t)a << 32) | (uint32_t)b);
+        }
+    std::vector<uint64_t> sorted = dir;
+    std::sort(sorted.begin(), sorted.end());
+    for (size_t i = 1; i < sorted.size(); ++i)
+        if (sorted[i] == sorted[i - 1]) return fail(ctx, TW_EINVAL, "normal flow: non-manifold edge (repeated direction)");
+    for (uint64_t d : sorted) {
+        const uint64_t rev = (d << 32) | (d >> 32);
+        if (!std::binary_search(sorted.begin(), sorted.end(), rev))
+            return fail(ctx, TW_EINVAL, "normal flow: mesh is not closed/consistently oriented");
+    }
+    // topology tables: vertex -> triangles (triangle order); undirected edges in
+    // (min, max) order with their (t, k) occurrences; vertex -> (neighbour, edge)
+    // in ascending neighbour order
+    std::vector<int> vt_off(nv + 1, 0), vt(3 * (size_t)nt);
+    for (int t = 0; t < nt; ++t)
+        for (int k = 0; k < 3; ++k) ++vt_off[triangles[3 * t + k] + 1];
+    for (int v = 0; v < nv; ++v) vt_off[v + 1] += vt_off[v];
+    {
+        std::vector<int> fill(vt_off.begin(), vt_off.end() - 1);
+        for (int t = 0; t < nt; ++t)
+            for (int k = 0; k < 3; ++k) vt[fill[triangles[3 * t + k]]++] = t;
+    }
+    std::vector<std::pair<uint64_t, int>> occ;  // (undirected key, t << 2 | k)
+    occ.reserve(3 * (size_t)nt);
+    for (int t = 0; t < nt; ++t)
+        for (int k = 0; k < 3; ++k) {
+            const int a = triangles[3 * t + k], b = triangles[3 * t + (k + 1) % 3];
+            occ.push_back({((uint64_t)(uint32_t)std::min(a, b) << 32) | (uint32_t)std::max(a, b), (t << 2) | k});
+        }
+    std::stable_sort(occ.begin(), occ.end(), [](auto& p, auto& q) { return p.first < q.first; });
+    std::vector<int> occ_off{0}, occ_v;
+    std::vector<std::pair<int, int>> ekeys;  // (min, max) per undirected edge
+    for (size_t i = 0; i < occ.size(); ++i) {
+        if (i > 0 && occ[i].first != occ[i - 1].first) occ_off.push_back((int)i);
+        if (i == 0 || occ[i].first != occ[i - 1].first)
+            ekeys.push_back({(int)(occ[i].first >> 32), (int)(occ[i].first & 0xffffffffu)});
+        occ_v.push_back(occ[i].second);
+    }
+    occ_off.push_back((int)occ.size());
+    const int ne = (int)ekeys.size();
+    std::vector<std::vector<std::pair<int, int>>> nbl(nv);
+    for (int e = 0; e < ne; ++e) {
+        nbl[ekeys[e].first].push_back({ekeys[e].second, e});
+        nbl[ekeys[e].second].push_back({ekeys[e].first, e});
+    }
+    std::vector<int> nb_off(nv + 1, 0);
+    std::vector<int2> nb;
+    for (int v = 0; v < nv; ++v) {
+        std::sort(nbl[v].begin(), nbl[v].end());
+        for (auto& p : nbl[v]) nb.push_back(make_int2(p.first, p.second));
+        nb_off[v + 1] = (int)nb.size();
+    }
+    std::vector<int4> t4(nt);
+    for (int t = 0; t < nt; ++t) t4[t] = make_int4(triangles[3 * t], triangles[3 * t + 1], triangles[3 * t + 2], 0);
+    CK(cudaSetDevice(ctx->device));
+    DevMem dx, dy0, dy1, dvto, dvt, dtris, doo, docc, dnbo, dnb, dw;
+    struct Rel {
+        std::vector<DevMem*> m;
+        ~Rel() {
+            for (DevMem* d : m) d->release();
+        }
+    } rel{{&dx, &dy0, &dy1, &dvto, &dvt, &dtris, &doo, &docc, &dnbo, &dnb, &dw}};
+    cudaError_t e = cudaSuccess;
+    auto up = [&](DevMem& d, const void* h, size_t bytes) {
+        if (e == cudaSuccess) e = d.ensure(std::max<size_t>(16, bytes));
+        if (e == cudaSuccess && bytes) e = cudaMemcpyAsync(d.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    };
+    up(dx, x, (size_t)nv * 24);
+    up(dvto, vt_off.data(), vt_off.size() * 4);
+    up(dvt, vt.data(), vt.size() * 4);
+    up(dtris, t4.data(), t4.size() * 16);
+    up(doo, occ_off.data(), occ_off.size() * 4);
+    up(docc, occ_v.data(), occ_v.size() * 4);
+    up(dnbo, nb_off.data(), nb_off.size() * 4);
+    up(dnb, nb.data(), nb.size() * 8);
+    if (e == cudaSuccess) e = dy0.ensure((size_t)std::max(1, nv) * 24);
+    if (e == cudaSuccess) e = dy1.ensure((size_t)std::max(1, nv) * 24);
+    if (e == cudaSuccess) e = dw.ensure((size_t)std::max(1, ne) * 8);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "normal flow: upload");
+    cudaStream_t s = ctx->stream;
+    const int nb_v = std::max(1, (nv + DTPB - 1) / DTPB);
+    k_nf_offset<<<nb_v, DTPB, 0, s>>>(nv, dx.as<double>(), dvto.as<int>(), dvt.as<int>(), dtris.as<int4>(), beta,
+                                       dy0.as<double>());
+    k_nf_weights<<<std::max(1, (ne + DTPB - 1) / DTPB), DTPB, 0, s>>>(ne, doo.as<int>(), docc.as<int>(),
+                                                                      dtris.as<int4>(), dy0.as<double>(), dw.as<double>());
+    DevMem* cur = &dy0;
+    DevMem* nxt = &dy1;
+    for (int pass = 0; pass < 3; ++pass) {  // NormalFlowConfig::kSmoothingIterations
+        k_nf_smooth<<<nb_v, DTPB, 0, s>>>(nv, dnbo.as<int>(), dnb.as<int2>(), dw.as<double>(), alpha_smooth,
+                                           cur->as<double>(), nxt->as<double>());
+        std::swap(cur, nxt);
+    }
+    ctx->launches += 5;
+    CK(cudaMemcpyAsync(y_out, cur->p, (size_t)nv * 24, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     return TW_OK;
 }
 

@@ -42,7 +42,16 @@ cudaError_t launch_advance(cudaStream_t s, const Params& P, int nblocks);
 cudaError_t coop_stage_linearize(cudaStream_t s, const Params& P, int nblocks);
 cudaError_t coop_ccd(cudaStream_t s, const Params& P, int nblocks);  // certification of x -> ccd_x1
 cudaError_t coop_stage_color(cudaStream_t s, const Params& P, int nblocks, long long nc);
-cudaError_t coop_stage_backward(cudaStream_t s, const Params& P, int nblocks, long long nc, int ncol);
+cudaError_t coop_stage_backward(cudaStream_t s, const Params& P, int nblocks, long long nc, int ncol, int mode);
+// row stage entries (tw_stage_build_rows / constraint_value / fill_diag)
+void launch_build_rows(cudaStream_t s, const double4* x, long long n, const int* kinds, const int* verts,
+                       const double* closest, double delta, int gap, int* kind, int* nverts, int* rv, double* value,
+                       double* jac, int* flavor, double* ref_volume, double* gw, double* denom);
+void launch_value_at(cudaStream_t s, const double4* x, long long n, const int* flavor, const int* nverts,
+                     const int* rv, const double* ref_volume, const double* gw, const double* denom,
+                     const double* sigma, double* out);
+void launch_fill_diag(cudaStream_t s, const double* inv_mass, long long n, const int* nverts, const int* rv,
+                      const double* jac, double* diag);
 cudaError_t launch_closest(cudaStream_t s, int nv, const double4* x, long long n, const int* kinds,
                            const int* verts, double* out, int* has);
 // blocks per SM the resolve kernel instance built for `minb` CTAs/SM keeps resident

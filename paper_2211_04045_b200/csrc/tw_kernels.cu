@@ -199,6 +199,73 @@ __global__ void k_stage_closest(int nv, const double4* x, long long n, const int
     (void)nv;
 }
 
+// ================================================= row stage entries
+// build_{vt,ee,vv,ve}_constraint / build_gap_constraint (constraints.cpp:56-142)
+// for n pairs given as (kinds, vertex ids, cached closest result): the row and
+// its re-evaluation data. gap = 1: build_gap_constraint for every kind.
+__global__ void k_stage_build_rows(const double4* x, long long n, const int* kinds, const int* verts,
+                                   const double* closest, double delta, int gap, int* kind, int* nverts, int* rv,
+                                   double* value, double* jac, int* flavor, double* ref_volume, double* gw,
+                                   double* denom) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int ka = kinds[2 * i], kb = kinds[2 * i + 1];
+        const int* va = verts + 6 * i;
+        const int* vb = verts + 6 * i + 3;
+        const double* c = closest + 11 * i;
+        Row r;
+        RowEval ev;
+        build_contact(ka, va, kb, vb, c + 1, c + 4, c[0], mk(c[7], c[8], c[9]), delta, gap, XLoad{x}, r, &ev);
+        kind[i] = r.kind;
+        nverts[i] = r.nverts;
+        for (int m = 0; m < 4; ++m) {
+            rv[4 * i + m] = m < r.nverts ? r.v[m] : -1;
+            const d3 j = m < r.nverts ? r.jac[m] : mk(0, 0, 0);
+            jac[12 * i + 3 * m] = j.x, jac[12 * i + 3 * m + 1] = j.y, jac[12 * i + 3 * m + 2] = j.z;
+            gw[4 * i + m] = ev.gw[m];
+        }
+        value[i] = r.value;
+        flavor[i] = ev.flavor;
+        ref_volume[i] = ev.ref_volume;
+        denom[i] = ev.denom;
+    }
+}
+
+// constraint_value_at (constraints.cpp:39-54) for n rows
+__global__ void k_stage_value_at(const double4* x, long long n, const int* flavor, const int* nverts, const int* rv,
+                                 const double* ref_volume, const double* gw, const double* denom, const double* sigma,
+                                 double* out) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int* v = rv + 4 * i;
+        double val = 0.0;
+        if (flavor[i] == FLAVOR_VOLUME) {
+            val = stencil_det(ld3(x, v[0]), ld3(x, v[1]), ld3(x, v[2]), ld3(x, v[3])) / ref_volume[i] - 1.0;
+        } else if (flavor[i] == FLAVOR_GAP) {
+            d3 g = mk(0, 0, 0);
+            for (int m = 0; m < nverts[i]; ++m) g = add(g, scl(gw[4 * i + m], ld3(x, v[m])));
+            val = nrm(g) / denom[i] - 1.0;
+        } else {
+            val = sigma[i] - nrm(sub(ld3(x, v[0]), ld3(x, v[1]))) / denom[i];
+        }
+        out[i] = val;
+    }
+}
+
+// fill_diag (constraints.cpp:175-179) for n rows
+__global__ void k_stage_fill_diag(const double* inv_mass, long long n, const int* nverts, const int* rv,
+                                  const double* jac, double* diag) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double d = 0.0;
+        for (int m = 0; m < nverts[i]; ++m) {
+            const double* J = jac + 12 * i + 3 * m;
+            d += inv_mass[rv[4 * i + m]] * sqn(mk(J[0], J[1], J[2]));
+        }
+        diag[i] = maxd(d, 1e-10);
+    }
+}
+
 // ====================================================== call prologue
 // ER compaction (edge order) and, in device-coloring mode, the static edge
 // row buckets by color (the edge-row colors are fixed for the call).
@@ -677,8 +744,10 @@ __global__ void __launch_bounds__(TPB, 4) k_stage_color(Params P, long long nc) 
 
 // assemble_lcp + sweeps + recover_target on uploaded rows (tw_stage_backward);
 // every row is handled as a contact row, y_out is written into P.x
-__global__ void __launch_bounds__(TPB, 4) k_stage_backward(Params P, long long nc, int ncol) {
-    ph_stage_q(P, nc);
+// mode bits (TW_LCP_*): 1 assemble (q and the warm-start impulse; otherwise
+// both are uploaded in c_q / imp), 2 solve (the sweeps), 4 recover (y into x).
+__global__ void __launch_bounds__(TPB, 4) k_stage_backward(Params P, long long nc, int ncol, int mode) {
+    if (mode & 1) ph_stage_q(P, nc);
     ph_stage_incidence(P, nc);
     STAGE_SYNC();
     ph_inc_totals(P);
@@ -687,9 +756,12 @@ __global__ void __launch_bounds__(TPB, 4) k_stage_backward(Params P, long long n
     STAGE_SYNC();
     ph_inc_scatter(P, nc);
     STAGE_SYNC();
-    ph_warm(P, nc, false);
-    STAGE_SYNC();
-    if (P.cfg.solver == 0) {
+    if (mode & 1) {
+        ph_warm(P, nc, false);
+        STAGE_SYNC();
+    }
+    if (!(mode & 2)) {
+    } else if (P.cfg.solver == 0) {
         ph_bucket_count(P, nc);
         STAGE_SYNC();
         ph_bucket_scatter(P, nc, ncol, false);
@@ -712,6 +784,7 @@ __global__ void __launch_bounds__(TPB, 4) k_stage_backward(Params P, long long n
         }
     }
     // recover_target (lcp.cpp:131-136): dynamic y = y_k1 + impulse, static keep y_k1
+    if (mode & 4)
     for (long long v = gtid(); v < P.nv; v += gstride()) {
         const double4 yk = P.yk1[v];
         const double4 a = P.imp[v];
@@ -955,12 +1028,30 @@ cudaError_t coop_stage_color(cudaStream_t s, const Params& P, int nblocks, long 
     void* args[] = {&p, &n};
     return coop((const void*)k_stage_color, s, nblocks, args);
 }
-cudaError_t coop_stage_backward(cudaStream_t s, const Params& P, int nblocks, long long nc, int ncol) {
+cudaError_t coop_stage_backward(cudaStream_t s, const Params& P, int nblocks, long long nc, int ncol, int mode) {
     Params p = P;
     long long n = nc;
-    int c = ncol;
-    void* args[] = {&p, &n, &c};
+    int c = ncol, md = mode;
+    void* args[] = {&p, &n, &c, &md};
     return coop((const void*)k_stage_backward, s, nblocks, args);
+}
+void launch_build_rows(cudaStream_t s, const double4* x, long long n, const int* kinds, const int* verts,
+                       const double* closest, double delta, int gap, int* kind, int* nverts, int* rv, double* value,
+                       double* jac, int* flavor, double* ref_volume, double* gw, double* denom) {
+    if (n == 0) return;
+    k_stage_build_rows<<<grid_for(n), 256, 0, s>>>(x, n, kinds, verts, closest, delta, gap, kind, nverts, rv, value,
+                                                  jac, flavor, ref_volume, gw, denom);
+}
+void launch_value_at(cudaStream_t s, const double4* x, long long n, const int* flavor, const int* nverts,
+                     const int* rv, const double* ref_volume, const double* gw, const double* denom,
+                     const double* sigma, double* out) {
+    if (n == 0) return;
+    k_stage_value_at<<<grid_for(n), 256, 0, s>>>(x, n, flavor, nverts, rv, ref_volume, gw, denom, sigma, out);
+}
+void launch_fill_diag(cudaStream_t s, const double* inv_mass, long long n, const int* nverts, const int* rv,
+                      const double* jac, double* diag) {
+    if (n == 0) return;
+    k_stage_fill_diag<<<grid_for(n), 256, 0, s>>>(inv_mass, n, nverts, rv, jac, diag);
 }
 cudaError_t launch_advance(cudaStream_t s, const Params& P, int nblocks) {
     double* md = nullptr;

@@ -300,11 +300,21 @@ struct Row {
     d3 jac[4];
 };
 
+// Re-evaluation data of a row (Constraint::flavor / ref_volume / gap_weights /
+// denom, constraints.hpp:26-33), recorded only by the stage entries.
+enum : int { FLAVOR_VOLUME = 0, FLAVOR_GAP = 1, FLAVOR_LENGTH = 2 };
+struct RowEval {
+    int flavor;
+    double ref_volume;
+    double gw[4];
+    double denom;
+};
+
 // build_gap_constraint, constraints.cpp:56-76. ids: a's then b's vertex ids
 // (na + nb <= 4); wa, wb: the pair's cached weights; sign per side.
 __device__ __forceinline__ void build_gap(int kind, int na, const int* va, int nb, const int* vb,
                                           const double* wa, const double* wb, double dist, d3 dir,
-                                          double delta, Row& c) {
+                                          double delta, Row& c, RowEval* ev = nullptr) {
     c.kind = kind;
     int n = 0;
     double gw[4];
@@ -314,6 +324,12 @@ __device__ __forceinline__ void build_gap(int kind, int na, const int* va, int n
     for (int m = n; m < 4; ++m) c.v[m] = -1, c.jac[m] = mk(0, 0, 0);
     c.value = dist / delta - 1.0;
     for (int m = 0; m < n; ++m) c.jac[m] = scl(gw[m] / delta, dir);
+    if (ev) {
+        ev->flavor = FLAVOR_GAP;
+        ev->ref_volume = 0.0;
+        ev->denom = delta;
+        for (int m = 0; m < 4; ++m) ev->gw[m] = m < n ? gw[m] : 0.0;
+    }
 }
 
 // build_vt_constraint (constraints.cpp:86-115) / build_ee_constraint
@@ -323,13 +339,13 @@ template <typename LoadX>
 __device__ __forceinline__ void build_contact(int ka, const int* va, int kb, const int* vb,
                                               const double* wa, const double* wb, double dist,
                                               d3 dir, double delta, int family, const LoadX& X,
-                                              Row& c) {
+                                              Row& c, RowEval* ev = nullptr) {
     const int kind = (ka == KV && kb == KT) ? ROW_VT
                      : (ka == KE && kb == KE) ? ROW_EE
                      : (ka == KV && kb == KE) ? ROW_VE
                                               : ROW_VV;
     if (family == 1 || kind == ROW_VE || kind == ROW_VV) {
-        build_gap(kind, ka + 1, va, kb + 1, vb, wa, wb, dist, dir, delta, c);
+        build_gap(kind, ka + 1, va, kb + 1, vb, wa, wb, dist, dir, delta, c, ev);
         return;
     }
     d3 p0, p1, p2, p3;
@@ -341,7 +357,7 @@ __device__ __forceinline__ void build_contact(int ka, const int* va, int kb, con
         d3 n = crs(sub(p2, p1), sub(p3, p1));
         const double n_len = nrm(n);
         if (n_len < 1e-20) {
-            build_gap(kind, 1, va, 3, vb, wa, wb, dist, dir, delta, c);
+            build_gap(kind, 1, va, 3, vb, wa, wb, dist, dir, delta, c, ev);
             return;
         }
         n = dvd(n, n_len);
@@ -350,7 +366,7 @@ __device__ __forceinline__ void build_contact(int ka, const int* va, int kb, con
         const d3 hn = scl(h, n);
         const double wr = stencil_det(add(p0, hn), sub(p1, hn), sub(p2, hn), sub(p3, hn));
         if (fabs(wr) < 6.0 * 1e-18) {
-            build_gap(kind, 1, va, 3, vb, wa, wb, dist, dir, delta, c);
+            build_gap(kind, 1, va, 3, vb, wa, wb, dist, dir, delta, c, ev);
             return;
         }
         c.kind = kind;
@@ -360,11 +376,12 @@ __device__ __forceinline__ void build_contact(int ka, const int* va, int kb, con
         d3 g[4];
         stencil_grad(p0, p1, p2, p3, g);
         for (int m = 0; m < 4; ++m) c.jac[m] = dvd(g[m], wr);
+        if (ev) *ev = RowEval{FLAVOR_VOLUME, wr, {0, 0, 0, 0}, 0.0};
         return;
     }
     // EE
     if (is_zero(dir)) {
-        build_gap(kind, 2, va, 2, vb, wa, wb, dist, dir, delta, c);
+        build_gap(kind, 2, va, 2, vb, wa, wb, dist, dir, delta, c, ev);
         return;
     }
     i0 = va[0], i1 = va[1], i2 = vb[0], i3 = vb[1];
@@ -373,7 +390,7 @@ __device__ __forceinline__ void build_contact(int ka, const int* va, int kb, con
     const d3 hd = scl(h, dir);
     const double wr = stencil_det(add(p0, hd), add(p1, hd), sub(p2, hd), sub(p3, hd));
     if (fabs(wr) < 6.0 * 1e-18) {
-        build_gap(kind, 2, va, 2, vb, wa, wb, dist, dir, delta, c);
+        build_gap(kind, 2, va, 2, vb, wa, wb, dist, dir, delta, c, ev);
         return;
     }
     c.kind = kind;
@@ -383,6 +400,7 @@ __device__ __forceinline__ void build_contact(int ka, const int* va, int kb, con
     d3 g[4];
     stencil_grad(p0, p1, p2, p3, g);
     for (int m = 0; m < 4; ++m) c.jac[m] = dvd(g[m], wr);
+    if (ev) *ev = RowEval{FLAVOR_VOLUME, wr, {0, 0, 0, 0}, 0.0};
 }
 
 __device__ __forceinline__ double row_jnorm(const Row& c) {

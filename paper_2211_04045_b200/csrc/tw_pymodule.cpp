@@ -1,5 +1,6 @@
 // Python module _twoway mirroring proj/bindings/module.cpp:101-186 (resolve,
-// repair, vertex_triangle_closest, edge_edge_closest) on the B200 path. Inputs
+// repair, normal_flow_target, certify_segment, vertex_triangle_closest,
+// edge_edge_closest) on the B200 path. Inputs
 // are numpy (N, 3) float64 / (T, 3) int arrays as in the reference; unknown
 // keyword arguments raise ValueError (std::invalid_argument) as there.
 #include <pybind11/numpy.h>
@@ -153,6 +154,59 @@ py::dict closest_call(int ka, std::vector<int32_t> va, int kb, std::vector<int32
     return d;
 }
 
+struct OwnedCtx {  // a context for the calls that do not go through twoway::resolve
+    tw_ctx* c = nullptr;
+    OwnedCtx() {
+        if (tw_ctx_create(0, nullptr, &c) != TW_OK) throw std::runtime_error("twoway: no CUDA device");
+    }
+    ~OwnedCtx() { tw_ctx_destroy(c); }
+    void check(int rc) const {
+        if (rc == TW_EINVAL || rc == TW_EUNSUPPORTED) throw std::invalid_argument(tw_last_error(c));
+        if (rc != TW_OK) throw std::runtime_error(tw_last_error(c));
+    }
+};
+
+// normal_flow_target binding, module.cpp:134-146
+py::array_t<double> normal_flow(const ArrD& x, const ArrI& triangles, double beta, double alpha) {
+    MeshState mesh = make_mesh(x, triangles, ArrI(std::vector<py::ssize_t>{0, 2}), ArrD(std::vector<py::ssize_t>{0}));
+    std::vector<int32_t> t;
+    for (const auto& tr : mesh.triangles) t.insert(t.end(), {tr[0], tr[1], tr[2]});
+    py::array_t<double> out({(py::ssize_t)mesh.num_vertices(), (py::ssize_t)3});
+    OwnedCtx ctx;
+    {
+        py::gil_scoped_release nogil;
+        ctx.check(tw_normal_flow_target(ctx.c, mesh.num_vertices(), x.data(), (int32_t)mesh.triangles.size(), t.data(),
+                                        beta, alpha, out.mutable_data()));
+    }
+    return out;
+}
+
+// certify_segment binding, module.cpp:148-162: the CCD check of the linear
+// motion x0 -> x1 runs on the device certifier (tw_ccd_certify)
+py::dict certify(const ArrD& x0, const ArrD& x1, const ArrI& triangles, const ArrI& strand_edges) {
+    MeshState mesh = make_mesh(x0, triangles, strand_edges, ArrD(std::vector<py::ssize_t>{0}));
+    if (x1.ndim() != 2 || x1.shape(0) != x0.shape(0) || x1.shape(1) != 3)
+        throw std::invalid_argument("x1 must match x0");
+    std::vector<int32_t> e, t;
+    for (const auto& ed : mesh.edges) e.insert(e.end(), {ed[0], ed[1]});
+    for (const auto& tr : mesh.triangles) t.insert(t.end(), {tr[0], tr[1], tr[2]});
+    OwnedCtx ctx;
+    int32_t viol = 0, certain = 0;
+    {
+        py::gil_scoped_release nogil;
+        tw_mesh* m = nullptr;
+        ctx.check(tw_mesh_create(ctx.c, mesh.num_vertices(), mesh.inv_mass.data(), (int32_t)mesh.edges.size(),
+                                 e.data(), 0, nullptr, (int32_t)mesh.triangles.size(), t.data(), &m));
+        const int rc = tw_ccd_certify(ctx.c, m, x0.data(), x1.data(), &viol, &certain, nullptr);
+        tw_mesh_destroy(m);
+        ctx.check(rc);
+    }
+    py::dict d;
+    d["certain"] = certain;
+    d["uncertain"] = viol - certain;
+    return d;
+}
+
 }  // namespace
 
 PYBIND11_MODULE(_twoway, m) {
@@ -175,6 +229,11 @@ PYBIND11_MODULE(_twoway, m) {
         },
         py::arg("x"), py::arg("y"), py::arg("triangles"), py::arg("strand_edges") = no_strands,
         py::arg("inv_mass") = no_mass, "Intersection-repair entry point (x must be intersection-free).");
+    m.def("normal_flow_target", &normal_flow, py::arg("x"), py::arg("triangles"), py::arg("beta") = 5e-4,
+          py::arg("alpha") = 0.5,
+          "Offset along area-weighted normals plus three cotangent-Jacobi smoothing passes (device).");
+    m.def("certify_segment", &certify, py::arg("x0"), py::arg("x1"), py::arg("triangles"),
+          py::arg("strand_edges") = no_strands, "CCD check of the linear motion between two states (device certifier).");
     m.def(
         "vertex_triangle_closest",
         [](std::vector<double> p, std::vector<double> a, std::vector<double> b, std::vector<double> c) {

@@ -82,7 +82,8 @@ def _setup(ctx, name, model):
 
     m, v = drape(**SCENES[name])
     x = m.positions.copy()
-    mesh = capi.Mesh(ctx, len(x), m.inv_mass, m.edges, m.strand_edges, m.triangles)
+    # both sides derive the edge order from (strands, triangles) as MeshState::finalize does
+    mesh = capi.Mesh(ctx, len(x), m.inv_mass, (), m.strand_edges, m.triangles)
     dyn = capi.Dynamics(ctx, mesh, x, **_model(name, model))
     rm = R.RefMesh(x, m.triangles, m.strand_edges, m.inv_mass, v)
     assert np.array_equal(rm.edges(), mesh.edges)
