@@ -581,6 +581,7 @@ struct tw_dyn {
     DevMem hx, hvel, x0, v0, xk, y, e_u, e_ab, rp_ids, rp_sw, rp_dir, rp_count, rs_key, rs_key2, vr_off, sort_tmp;
     DevMem sdiag, grad, pre, b, d, r, z, p, q, best, part, glob;
     long long rp_cap = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // step timing (the resolve uses the context's own events)
 };
 
 namespace {
@@ -865,7 +866,7 @@ int step_device(tw_ctx* ctx, tw_mesh* m, tw_dyn* D, const tw_resolve_config* cfg
                 tw_step_stats* st) {
     cudaStream_t s = ctx->stream;
     const size_t bytes = (size_t)m->nv * 24;
-    CK(cudaEventRecord(ctx->ev0, s));
+    CK(cudaEventRecord(D->ev0, s));
     CK(cudaMemcpyAsync(D->x0.p, d_x, bytes, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(D->v0.p, d_v, bytes, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(D->xk.p, d_x, bytes, cudaMemcpyDeviceToDevice, s));
@@ -886,10 +887,10 @@ int step_device(tw_ctx* ctx, tw_mesh* m, tw_dyn* D, const tw_resolve_config* cfg
     k_velocity<<<std::max(1, (n3 + DTPB - 1) / DTPB), DTPB, 0, s>>>(m->nv, m->d_inv_mass.as<double>(), d_x,
                                                                    D->x0.as<double>(), D->model.dt, d_v);
     ++ctx->launches;
-    CK(cudaEventRecord(ctx->ev1, s));
+    CK(cudaEventRecord(D->ev1, s));
     CK(cudaStreamSynchronize(s));
     float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    CK(cudaEventElapsedTime(&ms, D->ev0, D->ev1));
     st->device_ms = ms;
     CK(cudaGetLastError());
     return TW_OK;
@@ -979,9 +980,11 @@ int tw_dyn_create(tw_ctx* ctx, tw_mesh* m, const tw_energy_model* model, const d
         delete D;
         return cuda_fail(ctx, e, "tw_dyn_create");
     }
-    const int rc = ensure_state(D);
+    int rc = ensure_state(D);
+    if (!rc && (cudaEventCreate(&D->ev0) != cudaSuccess || cudaEventCreate(&D->ev1) != cudaSuccess))
+        rc = fail(ctx, TW_ECUDA, "dynamics: event creation failed");
     if (rc) {
-        delete D;
+        tw_dyn_destroy(D);
         return rc;
     }
     *out = D;
@@ -996,6 +999,8 @@ void tw_dyn_destroy(tw_dyn* D) {
                      &D->vr_off, &D->sort_tmp, &D->sdiag, &D->grad, &D->pre, &D->b, &D->d, &D->r, &D->z,
                      &D->p, &D->q, &D->best, &D->part, &D->glob};
     for (DevMem* d : all) d->release();
+    if (D->ev0) cudaEventDestroy(D->ev0);
+    if (D->ev1) cudaEventDestroy(D->ev1);
     delete D;
 }
 

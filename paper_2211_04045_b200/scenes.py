@@ -553,6 +553,20 @@ def bow_knot(**kw) -> Scene:
     return ply_knot(n_along=1870, **kw)
 
 
+def knot_frame(n_along: int = 1870, dt: float = 0.01, **kw):
+    """A simulation frame of the tightening knot for the dynamics step
+    (dynamics.cpp:326-349): the plies at rest (x, 2.5 mm apart) moving with
+    v0 = (y_tight - x) / dt, where y_tight is the ply_knot tightening target
+    (squeeze / slide in ``kw``). One implicit-Euler step with the paper's knot
+    time step dt = 1/100 (PAPER.md:933) then drives the plies into each other;
+    resolve makes the frame intersection-free. Returns (scene, v0)."""
+    kw = {**KNOT_DEFAULTS, **kw}
+    kw.setdefault("name", "bow_knot_frame" if n_along == 1870 else "knot_frame")
+    sc = ply_knot(n_along=n_along, **kw)
+    v0 = (sc.y - sc.x) / dt
+    return sc, v0
+
+
 def cloth_on_sphere(n: int = 64, spacing: float = 0.01, drop: float = 0.03) -> Scene:
     """CFG1: a 64x64 cloth (7,938 T) at 10 mm spacing hovering 24 mm above a
     static icosphere (s = 4, r = 0.2 m, 5,120 T); the target is one dt = 1/30 s
