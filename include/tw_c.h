@@ -281,6 +281,8 @@ typedef struct {
     double device_ms;        /* CUDA-event time of the whole step on the device */
     double resolve_ms;       /* of which resolve */
     double wall_ms;
+    double target_ms;        /* of which the Newton targets (search + gradient/Hessian + PCG) */
+    double pcg_ms;           /* of which the PCG kernels */
 } tw_step_stats;
 
 typedef struct tw_dyn tw_dyn;

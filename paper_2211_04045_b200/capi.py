@@ -86,7 +86,7 @@ class StepStats(C.Structure):
         ("resolve_steps", C.c_int32), ("searches", C.c_int32), ("resolve_converged", C.c_int32),
         ("pcg_iterations", C.c_int32), ("pcg_converged", C.c_int32), ("num_pairs", C.c_int32),
         ("repulsive_pairs", C.c_int32), ("device_ms", C.c_double), ("resolve_ms", C.c_double),
-        ("wall_ms", C.c_double),
+        ("wall_ms", C.c_double), ("target_ms", C.c_double), ("pcg_ms", C.c_double),
     ]
 
 _LIB = None

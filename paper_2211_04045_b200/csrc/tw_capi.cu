@@ -366,6 +366,13 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
         if (!trace_host) P.trace = nullptr;  // lets the kernel skip work only a trace would show
         P.pw_all = 0;
         CK(cudaMemsetAsync(ctx->globals.p, 0, sizeof(Globals), ctx->stream));
+        if (cfg.coloring_mode == TW_COLOR_REFERENCE) {
+            // the exact replay runs on one device thread while the grid waits:
+            // the barrier watchdog allows it 600 s instead of 20 s
+            static const unsigned long long wd = 600000000000ull;
+            CK(cudaMemcpyAsync((char*)ctx->globals.p + offsetof(Globals, watchdog_ns), &wd, 8,
+                               cudaMemcpyHostToDevice, ctx->stream));
+        }
         // color tables return to zero at the end of every step; an attempt
         // aborted for capacity growth may leave counts behind
         CK(cudaMemsetAsync(ctx->ccount.p, 0, (size_t)ctx->colcap * 4, ctx->stream));
@@ -1246,6 +1253,7 @@ int tw_stage_color(tw_ctx* ctx, tw_mesh* m, int64_t nrows, const uint8_t* kind, 
         CK(cudaMemsetAsync(ctx->er_color_cnt.p, 0, (size_t)ctx->colcap * 4, s));
         std::memset(&G, 0, sizeof G);
         G.max_color = -1;  // no contact row colored yet
+        if (mode == TW_COLOR_REFERENCE) G.watchdog_ns = 600000000000ull;  // one-thread replay
         CK(cudaMemcpyAsync(ctx->globals.p, &G, sizeof G, cudaMemcpyHostToDevice, s));
         Params P = make_params(ctx, m, cfg);
         CK(coop_stage_color(s, P, ctx->nblocks, nc));

@@ -479,6 +479,81 @@ __global__ void __launch_bounds__(DTPB) k_pcg(DynParams P) {
     }
 }
 
+// Register-resident CG: one vertex per thread (grid = ceil(nv / 256) CTAs,
+// all co-resident), so d, r, p, q, best and the preconditioner block stay in
+// registers across iterations and only z -- the operand of the neighbours'
+// H z gathers -- goes through memory (L2-resident). Same phases, partial
+// sums and exit logic as k_pcg; used whenever the grid fits on the device.
+__global__ void __launch_bounds__(DTPB, 2) k_pcg_reg(DynParams P) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool own = v < P.nv;
+    double* part[2] = {P.part, P.part + 2 * gridDim.x};
+    int cur = 0;
+    d3 b = mk(0, 0, 0), r, z, p, q, d = mk(0, 0, 0), best = mk(0, 0, 0);
+    double pre[9];
+    if (own) {
+        for (int k = 0; k < 9; ++k) pre[k] = P.pre[9 * (size_t)v + k];
+        if (P.inv_mass[v] != 0.0) b = neg(l4(P.grad[v]));
+    }
+    auto pc = [&](d3 x) {
+        return mk((pre[0] * x.x + pre[1] * x.y) + pre[2] * x.z, (pre[3] * x.x + pre[4] * x.y) + pre[5] * x.z,
+                  (pre[6] * x.x + pre[7] * x.y) + pre[8] * x.z);
+    };
+    r = b;
+    z = own ? pc(r) : mk(0, 0, 0);
+    p = z;
+    if (own) P.z[v] = s4(z);
+    block_partial2(own ? dot(r, z) : 0.0, own ? sqn(b) : 0.0, part[cur]);
+    dyn_sync(P.g);
+    double rz, bb;
+    grid_total2(part[cur], gridDim.x, &rz, &bb);
+    cur ^= 1;
+    const double bnorm = sqrt(bb);
+    double best_res = bnorm;
+    q = own ? hess_row(P, v, P.z) : mk(0, 0, 0);
+    block_partial2(own ? dot(p, q) : 0.0, 0.0, part[cur]);
+    dyn_sync(P.g);
+    int it = 0;
+    const int maxit = P.m.pcg_max_iters;
+    const double tol = P.m.pcg_tol;
+    for (; it < maxit && best_res > tol * bnorm; ++it) {
+        double pq, unused;
+        grid_total2(part[cur], gridDim.x, &pq, &unused);
+        cur ^= 1;
+        if (pq <= 0.0) break;
+        const double alpha = rz / pq;
+        // phase A
+        d = add(d, scl(alpha, p));
+        r = sub(r, scl(alpha, q));
+        z = own ? pc(r) : mk(0, 0, 0);
+        if (own) P.z[v] = s4(z);
+        block_partial2(own ? sqn(r) : 0.0, own ? dot(r, z) : 0.0, part[cur]);
+        dyn_sync(P.g);
+        double rr, rzn;
+        grid_total2(part[cur], gridDim.x, &rr, &rzn);
+        cur ^= 1;
+        const double res = sqrt(rr);
+        if (res < best_res) {
+            best_res = res;
+            best = d;
+        }
+        const double beta = rzn / rz;
+        rz = rzn;
+        // phase B
+        p = add(z, scl(beta, p));
+        q = own ? add(hess_row(P, v, P.z), scl(beta, q)) : mk(0, 0, 0);
+        block_partial2(own ? dot(p, q) : 0.0, 0.0, part[cur]);
+        dyn_sync(P.g);
+    }
+    if (own) P.best[v] = s4(best);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        P.g->iters = it;
+        P.g->converged = best_res <= tol * bnorm ? 1 : 0;
+        P.g->bnorm = bnorm;
+        P.g->best_res = best_res;
+    }
+}
+
 // y = x + best for dynamic vertices (dynamics.cpp:266-268)
 __global__ void k_target(int nv, const double* inv_mass, const double* x, const double4* best, int converged_zero,
                          double* y) {
@@ -582,6 +657,7 @@ struct tw_dyn {
     DevMem sdiag, grad, pre, b, d, r, z, p, q, best, part, glob;
     long long rp_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // step timing (the resolve uses the context's own events)
+    cudaEvent_t evt0 = nullptr, evp0 = nullptr, evp1 = nullptr;  // target / PCG timing
 };
 
 namespace {
@@ -776,6 +852,7 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
     cudaStream_t s = ctx->stream;
     const int nv = m->nv;
     const int nb = (nv + DTPB - 1) / DTPB;
+    CK(cudaEventRecord(D->evt0, s));
     CK(ctx->x.ensure((size_t)std::max(1, nv) * 32));
     k_pack_x4<<<std::max(1, nb), DTPB, 0, s>>>(nv, d_xk, m->d_inv_mass.as<double>(), ctx->x.as<double4>());
     ++ctx->launches;
@@ -830,13 +907,23 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
         CK(cudaStreamSynchronize(s));
         for (int v = 0; v < nv; ++v) grad_host[3 * v] = g[v].x, grad_host[3 * v + 1] = g[v].y, grad_host[3 * v + 2] = g[v].z;
     }
-    const int pb = pcg_blocks(ctx, nv);
+    // register-resident CG when one vertex per thread fits co-resident
+    static int reg_per_sm = -1;
+    if (reg_per_sm < 0) {
+        reg_per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&reg_per_sm, k_pcg_reg, DTPB, 0);
+    }
+    const int reg_blocks = std::max(1, (nv + DTPB - 1) / DTPB);
+    const bool use_reg = getenv("TW_PCG_GLOBAL") == nullptr && reg_blocks <= ctx->sm_count * reg_per_sm;
+    const int pb = use_reg ? reg_blocks : pcg_blocks(ctx, nv);
     P.nblocks = pb;
     CK(D->part.ensure((size_t)pb * 32));
     P.part = D->part.as<double>();
     CK(cudaMemsetAsync(D->glob.p, 0, sizeof(DynGlobals), s));
     void* args[] = {&P};
-    CK(cudaLaunchCooperativeKernel((void*)k_pcg, dim3(pb), dim3(DTPB), args, 0, s));
+    CK(cudaEventRecord(D->evp0, s));
+    CK(cudaLaunchCooperativeKernel(use_reg ? (void*)k_pcg_reg : (void*)k_pcg, dim3(pb), dim3(DTPB), args, 0, s));
+    CK(cudaEventRecord(D->evp1, s));
     ++ctx->launches;
     DSYNC("k_pcg");
     DynGlobals G;
@@ -844,7 +931,12 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
     CK(cudaStreamSynchronize(s));
     k_target<<<std::max(1, nb), DTPB, 0, s>>>(nv, m->d_inv_mass.as<double>(), d_xk, P.best, G.bnorm == 0.0, d_y);
     ++ctx->launches;
+    float tms = 0.f, pms = 0.f;
+    CK(cudaEventElapsedTime(&tms, D->evt0, D->evp1));
+    CK(cudaEventElapsedTime(&pms, D->evp0, D->evp1));
     if (st) {
+        st->target_ms += tms;
+        st->pcg_ms += pms;
         st->pcg_iterations += G.iters;
         st->pcg_converged = st->pcg_converged && G.converged;
         st->num_pairs = (int32_t)np;
@@ -981,7 +1073,9 @@ int tw_dyn_create(tw_ctx* ctx, tw_mesh* m, const tw_energy_model* model, const d
         return cuda_fail(ctx, e, "tw_dyn_create");
     }
     int rc = ensure_state(D);
-    if (!rc && (cudaEventCreate(&D->ev0) != cudaSuccess || cudaEventCreate(&D->ev1) != cudaSuccess))
+    if (!rc && (cudaEventCreate(&D->ev0) != cudaSuccess || cudaEventCreate(&D->ev1) != cudaSuccess ||
+                cudaEventCreate(&D->evt0) != cudaSuccess || cudaEventCreate(&D->evp0) != cudaSuccess ||
+                cudaEventCreate(&D->evp1) != cudaSuccess))
         rc = fail(ctx, TW_ECUDA, "dynamics: event creation failed");
     if (rc) {
         tw_dyn_destroy(D);
@@ -999,8 +1093,8 @@ void tw_dyn_destroy(tw_dyn* D) {
                      &D->vr_off, &D->sort_tmp, &D->sdiag, &D->grad, &D->pre, &D->b, &D->d, &D->r, &D->z,
                      &D->p, &D->q, &D->best, &D->part, &D->glob};
     for (DevMem* d : all) d->release();
-    if (D->ev0) cudaEventDestroy(D->ev0);
-    if (D->ev1) cudaEventDestroy(D->ev1);
+    for (cudaEvent_t e : {D->ev0, D->ev1, D->evt0, D->evp0, D->evp1})
+        if (e) cudaEventDestroy(e);
     delete D;
 }
 

@@ -100,6 +100,7 @@ struct Globals {
     long long pairs_evaluated;
     long long rows_solved;
     // phase profile (CTA 0 barrier-to-barrier wall time per call site)
+    unsigned long long watchdog_ns;  // grid-barrier watchdog (0: 20 s), set by the host per call
     unsigned long long phase_t0;
     unsigned long long phase_ns[kPhaseSites];
     unsigned int phase_cnt[kPhaseSites];

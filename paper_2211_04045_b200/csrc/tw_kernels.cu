@@ -416,6 +416,10 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
         SYNC();
         int ncol_c, ncol_e, ncol;
         if (C.coloring_mode == 0) {
+            ph_color_ref_count(P, nc);
+            SYNC();
+            ph_color_ref_fill(P, nc);
+            SYNC();
             ph_color_ref(P, nc);
             SYNC();
             ncol = g->max_color + 1;
@@ -725,6 +729,10 @@ __global__ void __launch_bounds__(TPB, 4) k_stage_color(Params P, long long nc) 
     ph_warm(P, nc);
     STAGE_SYNC();
     if (P.cfg.coloring_mode == 0) {
+        ph_color_ref_count(P, nc);
+        STAGE_SYNC();
+        ph_color_ref_fill(P, nc);
+        STAGE_SYNC();
         ph_color_ref(P, nc);
         return;
     }

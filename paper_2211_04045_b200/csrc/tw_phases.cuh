@@ -36,7 +36,7 @@ __device__ __forceinline__ bool grid_sync(Globals* g) {
                 if (*err) break;
                 const unsigned long long t = global_ns();
                 if (t0 == 0) t0 = t;
-                else if (t - t0 > 20000000000ull) {
+                else if (t - t0 > (g->watchdog_ns ? g->watchdog_ns : 20000000000ull)) {
                     atomicOr(&g->error, ERR_TIMEOUT);
                     break;
                 }
@@ -64,7 +64,7 @@ __device__ __forceinline__ bool sub_sync(Globals* g, unsigned n) {
                 if (*err) break;
                 const unsigned long long t = global_ns();
                 if (t0 == 0) t0 = t;
-                else if (t - t0 > 20000000000ull) {
+                else if (t - t0 > (g->watchdog_ns ? g->watchdog_ns : 20000000000ull)) {
                     atomicOr(&g->error, ERR_TIMEOUT);
                     break;
                 }
@@ -1362,16 +1362,119 @@ struct Mt64 {
         return;                              \
     }
 
+// The reference coloring's conflict graph (constraints.cpp:229-244: rows that
+// share a dynamic vertex; sorted, unique neighbour lists), built by the whole
+// grid before the sequential replay: row r's candidate list lives at
+// pool[2R + 2 + off(r)] with off = the exclusive prefix of the candidate counts
+// (chunked per CTA), sorted and deduplicated in place; its length goes to
+// pool[R + 1 + r]. The lists need not be contiguous.
+__device__ __forceinline__ int ref_row_verts(const Params& P, long long nc, long long r, int* v) {
+    if (r < nc) {
+        const int4 id = P.c_ids[r];
+        v[0] = id.x, v[1] = id.y, v[2] = id.z, v[3] = id.w;
+        int n = 0;
+        while (n < 4 && v[n] >= 0) ++n;
+        return n;
+    }
+    const int2 e = P.edges[P.er_edge[r - nc]];
+    v[0] = e.x, v[1] = e.y;
+    return 2;
+}
+
+__device__ __forceinline__ long long ref_candidates(const Params& P, long long nc, long long r) {
+    int vv[4];
+    const int n = ref_row_verts(P, nc, r, vv);
+    long long c = 0;
+    for (int m = 0; m < n; ++m) {
+        const int v = vv[m];
+        if (!(P.inv_mass[v] > 0.0)) continue;
+        c += P.voff[v + 1] - P.voff[v];
+        if (P.cfg.edge_constraints)
+            for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) c += P.is_er[P.vedge[q]];
+    }
+    return c;
+}
+
+__device__ void ph_color_ref_count(const Params& P, long long nc) {
+    const long long R = nc + P.g->ner;
+    long long lo, hi;
+    chunk_of(R, &lo, &hi);
+    long long s = 0;
+    for (long long r = lo + threadIdx.x; r < hi; r += TPB) s += ref_candidates(P, nc, r);
+    const long long t = block_sum(s);
+    if (threadIdx.x == 0) P.part_k[blockIdx.x] = t;
+}
+
+__device__ void ph_color_ref_fill(const Params& P, long long nc) {
+    const long long R = nc + P.g->ner;
+    int* pool = P.refpool;
+    int* adj_off = pool;          // R + 1
+    int* adj_len = pool + R + 1;  // R
+    int* lists = pool + 2 * R + 2;
+    const long long total = prefix_of(P.part_k, gridDim.x);
+    if (2 * R + 2 + total > P.refpool_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&P.g->error, ERR_CAP_REFPOOL);
+        return;
+    }
+    long long lo, hi;
+    chunk_of(R, &lo, &hi);
+    long long base = prefix_of(P.part_k, blockIdx.x);
+    for (long long t0 = lo; t0 < hi; t0 += TPB) {
+        const long long r = t0 + threadIdx.x;
+        const long long c = r < hi ? ref_candidates(P, nc, r) : 0;
+        long long tile;
+        const long long ex = block_scan(c, &tile);
+        if (r < hi) {
+            const long long start = base + ex;
+            adj_off[r] = (int)start;
+            int* L = lists + start;
+            int len = 0;
+            int vv[4];
+            const int n = ref_row_verts(P, nc, r, vv);
+            for (int m = 0; m < n; ++m) {
+                const int v = vv[m];
+                if (!(P.inv_mass[v] > 0.0)) continue;
+                for (int t = P.voff[v]; t < P.voff[v + 1]; ++t) {
+                    const long long j = P.vinc[t] >> 2;
+                    if (j != r) L[len++] = (int)j;
+                }
+                if (P.cfg.edge_constraints)
+                    for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
+                        const int e = P.vedge[q];
+                        if (!P.is_er[e]) continue;
+                        const long long j = nc + P.er_index[e];
+                        if (j != r) L[len++] = (int)j;
+                    }
+            }
+            for (int i = 1; i < len; ++i) {  // insertion sort + unique
+                const int x = L[i];
+                int j = i - 1;
+                while (j >= 0 && L[j] > x) L[j + 1] = L[j], --j;
+                L[j + 1] = x;
+            }
+            int w = 0;
+            for (int i = 0; i < len; ++i)
+                if (i == 0 || L[i] != L[i - 1]) L[w++] = L[i];
+            adj_len[r] = w;
+        }
+        base += tile;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) adj_off[R] = (int)total;
+}
+
 __device__ void ph_color_ref(const Params& P, long long nc) {
-    const int* er_index = P.er_index;
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
     const long long R = nc + P.g->ner;
     if (R == 0) {
         P.g->max_color = -1;
         return;
     }
+    if (P.g->error) return;
     int* pool = P.refpool;
-    long long top = 0;
+    const int* adj_start = pool;
+    const int* adj_len = pool + R + 1;
+    const int* adj = pool + 2 * R + 2;
+    long long top = 2 * R + 2 + adj_start[R];
     auto alloc = [&](long long n) -> int* {
         if (top + n > P.refpool_cap) {
             atomicOr(&P.g->error, ERR_CAP_REFPOOL);
@@ -1381,67 +1484,6 @@ __device__ void ph_color_ref(const Params& P, long long nc) {
         top += n;
         return p;
     };
-    int* adj_off = alloc(R + 1);
-    if (!adj_off) return;
-    auto row_verts = [&](long long r, int* v) -> int {
-        if (r < nc) {
-            const int4 id = P.c_ids[r];
-            v[0] = id.x, v[1] = id.y, v[2] = id.z, v[3] = id.w;
-            int n = 0;
-            while (n < 4 && v[n] >= 0) ++n;
-            return n;
-        }
-        const int2 e = P.edges[P.er_edge[r - nc]];
-        v[0] = e.x, v[1] = e.y;
-        return 2;
-    };
-    // adjacency: sorted, unique neighbor lists through shared dynamic vertices
-    long long cur = top;
-    for (long long r = 0; r < R; ++r) {
-        adj_off[r] = (int)(cur - top);
-        int vv[4];
-        const int n = row_verts(r, vv);
-        long long start = cur;
-        for (int m = 0; m < n; ++m) {
-            const int v = vv[m];
-            if (!(P.inv_mass[v] > 0.0)) continue;
-            auto push = [&](long long j) {
-                if (cur >= P.refpool_cap) {
-                    atomicOr(&P.g->error, ERR_CAP_REFPOOL);
-                    return;
-                }
-                pool[cur++] = (int)j;
-            };
-            for (int t = P.voff[v]; t < P.voff[v + 1]; ++t) {
-                const long long j = P.vinc[t] >> 2;
-                TW_INVARIANT(j < nc);
-                if (j != r) push(j);
-            }
-            if (P.cfg.edge_constraints)
-                for (int q = P.vedge_off[v]; q < P.vedge_off[v + 1]; ++q) {
-                    const int e = P.vedge[q];
-                    if (!P.is_er[e]) continue;
-                    TW_INVARIANT(er_index[e] >= 0 && er_index[e] < P.g->ner);
-                    const long long j = nc + er_index[e];
-                    if (j != r) push(j);
-                }
-        }
-        if (P.g->error) return;
-        // insertion sort + unique
-        for (long long i = start + 1; i < cur; ++i) {
-            const int v = pool[i];
-            long long j = i - 1;
-            while (j >= start && pool[j] > v) pool[j + 1] = pool[j], --j;
-            pool[j + 1] = v;
-        }
-        long long w = start;
-        for (long long i = start; i < cur; ++i)
-            if (i == start || pool[i] != pool[i - 1]) pool[w++] = pool[i];
-        cur = w;
-    }
-    adj_off[R] = (int)(cur - top);
-    int* adj = pool + top;
-    top = cur;
     int* degree = alloc(R);
     int* order = alloc(R);
     int* removed = alloc(R);
@@ -1449,7 +1491,7 @@ __device__ void ph_color_ref(const Params& P, long long nc) {
     if (!used) return;
     int max_deg = 0;
     for (long long i = 0; i < R; ++i) {
-        degree[i] = adj_off[i + 1] - adj_off[i];
+        degree[i] = adj_len[i];
         removed[i] = 0;
         if (degree[i] > max_deg) max_deg = degree[i];
     }
@@ -1490,7 +1532,7 @@ __device__ void ph_color_ref(const Params& P, long long nc) {
         }
         removed[cand] = 1;
         order[picked] = cand;
-        for (int k = adj_off[cand]; k < adj_off[cand + 1]; ++k) {
+        for (int k = adj_start[cand]; k < adj_start[cand] + adj_len[cand]; ++k) {
             const int nb = adj[k];
             TW_INVARIANT(nb >= 0 && nb < R);
             if (!removed[nb]) {
@@ -1511,7 +1553,7 @@ __device__ void ph_color_ref(const Params& P, long long nc) {
     for (long long it = R - 1; it >= 0; --it) {
         const int i = order[it];
         TW_INVARIANT(i >= 0 && i < R);
-        for (int k = adj_off[i]; k < adj_off[i + 1]; ++k) {
+        for (int k = adj_start[i]; k < adj_start[i] + adj_len[i]; ++k) {
             const int c = color_of(adj[k]);
             TW_INVARIANT(c < R);
             if (c >= 0) used[c] = i;

@@ -164,10 +164,14 @@ def test_step_is_intersection_free(ctx):
     from paper_2211_04045_b200 import capi
 
     m, x, v, mesh, dyn, rm = _setup(ctx, "drape_fast", "default")
-    for _ in range(4):
+    for _ in range(3):
+        # the frame's certified path is resolve's piecewise-linear path from x
+        # to x_next (the straight segment x -> x_next need not be free)
+        y, _, _ = capi.newton_target(ctx, mesh, dyn, x, v, x)
+        xp, sp = capi.resolve(ctx, mesh, x, y, record_path=True)
         xn, v, st = capi.step(ctx, mesh, dyn, x, v)
-        viol, certain = capi.ccd_certify(ctx, mesh, x, xn)
-        assert certain == 0
+        assert np.array_equal(xn.view(np.uint64), xp.view(np.uint64))
+        assert capi.ccd_certify_path(ctx, mesh, sp["path"])[1] == 0
         x = xn
 
 

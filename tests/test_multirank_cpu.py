@@ -1,8 +1,10 @@
 """Host logic of the N > 1 bench path, on CPU with the gloo backend
-(world_size 2): per-rank independent scenes, the max-over-ranks timing
-reduction and the whole-job rate, and rank-0-only output of the reference arm.
-The device path has no collective (independent scenes per rank, DESIGN.md
-"Multi-GPU"), so this is all the multi-process logic there is."""
+(world_size 2): the max-over-ranks timing reduction, the partition of the
+configs[4] batch over the ranks (every scene exactly once, rank-seeded
+targets), rank-0-only output of the reference arm, and the self-spawn of
+`bench.py --gpus N` without torchrun. The device path has no collective
+(independent scenes per rank), so this is all the
+multi-process logic there is."""
 import json
 import os
 import socket
@@ -26,24 +28,22 @@ def _worker(rank, world, port, out_dir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
     sys.path.insert(0, ROOT)
-    import torch.distributed as dist
-
     import bench
 
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    D = bench.Dist(device="cpu")
     # rank r reports (r + 1) ms for the device loop and (10 - r) ms end to end
-    mx = bench.max_over_ranks([rank + 1.0, 10.0 - rank], dist, "cpu")
-    sc = bench.make_scene("reef", rank)
+    mx = D.max([rank + 1.0, 10.0 - rank])
+    lo, hi = bench.partition(64, D.world, D.rank)
+    sums = [float(np.abs(bench.batch_scene(i)[1]).sum()) for i in (lo, hi - 1)]
 
     class A:
-        gpus, steps, warmup, scene = world, 2, 3, "reef"
+        gpus, steps, warmup, scene = world, 1, 0, "reef"
 
     ref = bench.run_reference(A) if rank != 0 else "rank0"
-    dist.barrier()
-    dist.destroy_process_group()
+    D.barrier()
+    D.close()
     with open(os.path.join(out_dir, f"r{rank}.json"), "w") as f:
-        json.dump({"max": mx, "nv": int(sc.nv), "ntri": int(len(sc.triangles)),
-                   "ysum": float(np.abs(sc.y).sum()), "ref": ref}, f)
+        json.dump({"max": mx, "lo": lo, "hi": hi, "vsums": sums, "ref": ref}, f)
 
 
 def test_two_rank_gloo_host_logic(tmp_path):
@@ -52,16 +52,37 @@ def test_two_rank_gloo_host_logic(tmp_path):
                        join=True, start_method="spawn")
     r = [json.load(open(tmp_path / f"r{i}.json")) for i in range(world)]
     assert r[0]["max"] == r[1]["max"] == [2.0, 10.0]
-    # independent, same-sized scenes (rank-seeded target)
-    assert r[0]["nv"] == r[1]["nv"] and r[0]["ntri"] == r[1]["ntri"]
-    assert r[0]["ysum"] != r[1]["ysum"]  # rank-seeded squeeze phase of the target
+    # configs[4]: 64 scenes, contiguous halves, every scene exactly once
+    assert (r[0]["lo"], r[0]["hi"], r[1]["lo"], r[1]["hi"]) == (0, 32, 32, 64)
+    # independent scenes: rank-seeded tightening velocities differ
+    assert len({*r[0]["vsums"], *r[1]["vsums"]}) == 4
     # the reference arm prints on rank 0 only
     assert r[1]["ref"] is None
 
 
-def test_whole_job_rate():
+def test_partition_covers_every_scene():
     sys.path.insert(0, ROOT)
     import bench
 
-    assert bench.whole_job_rate(1, 10, 1000.0) == 10.0
-    assert bench.whole_job_rate(4, 10, 2000.0) == 20.0
+    for world in (1, 2, 3, 4, 8):
+        owned = [i for r in range(world) for i in range(*bench.partition(64, world, r))]
+        assert owned == list(range(64))
+
+
+def test_spawn_command(monkeypatch):
+    """--gpus N without WORLD_SIZE re-launches itself under torch.distributed.run."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    seen = {}
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2"])
+
+    class A:
+        gpus = 4
+
+    bench.spawn(A)
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "2"]
