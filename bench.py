@@ -237,6 +237,10 @@ class Dist:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         if device == "cuda":
             torch.cuda.set_device(self.local)
+            # one explicit stream shared by torch (flush, copies, events) and the
+            # device contexts (capi.Context(stream=...)): every op is ordered
+            self.stream = torch.cuda.Stream()
+            torch.cuda.set_stream(self.stream)
         self.dist = None
         if self.world > 1:
             import torch.distributed as dist
@@ -524,6 +528,8 @@ def run_batch_frames(args, D, nscenes):
             ms += a.elapsed_time(b)
             frames += 1
             rsteps += st["resolve_steps"]
+            if os.environ.get("TW_BENCH_VERBOSE"):
+                print(f"batch frame {frames}: {a.elapsed_time(b):.2f} ms, {st}", file=sys.stderr, flush=True)
     clk = clocks.stop()
     (ms_max,) = D.max([ms])
     base.close()
@@ -653,8 +659,8 @@ def main():
     if D.rank == 0 and D.world == 1 and not args.no_extras:
         out["resolve_only"] = run_resolve_only(ctx, args, "device", args.steps)
         out["exact_parity_mode"] = run_resolve_only(ctx, args, "reference", max(2, args.steps // 5))
-        res = run_batch_frames(args, D, 16)
-        out["batch_configs4_one_gpu"] = {"scenes": 16, "steps_per_s": round(res["value"], 3),
+        res = run_batch_frames(args, D, 8)
+        out["batch_configs4_one_gpu"] = {"scenes": 8, "steps_per_s": round(res["value"], 3),
                                          "resolve_steps_per_frame": round(res["resolve_steps_per_frame"], 2)}
     if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)

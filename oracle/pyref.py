@@ -90,6 +90,7 @@ def lib():
         L.ref_incremental_energy.restype = C.c_double
         L.ref_incremental_energy.argtypes = [P, P, C.POINTER(EnergyParams), P]
         L.ref_normal_flow_target.argtypes = [P, P, C.c_double, C.c_double, P]
+        L.ref_frame_sample.argtypes = [P, P, C.POINTER(EnergyParams), C.POINTER(Config), P]
         L.ref_ccd_certify.argtypes = [P, P, P, P]
         L.ref_fixture.restype = P
         L.ref_fixture.argtypes = [C.c_uint64, C.c_int, C.c_int, P, P, P, C.c_char_p, C.c_int]
@@ -246,6 +247,20 @@ def step(mesh: RefMesh, rest_x, energy=None, **kw):
     if n < 0:
         raise RuntimeError(_err())
     return xo, vo, n, s.value
+
+
+def frame_sample(mesh: RefMesh, rest_x, energy=None, **kw):
+    """Timed pieces of one reference frame (seconds): target (search +
+    gradient/Hessian + repulsion + PCG), one proximity_search, one non-search
+    Alg.-1 iteration; plus that iteration's contact rows and colors."""
+    ep = energy_params(**(energy or {}))
+    cfg = default_config(**kw)
+    out = np.zeros(5)
+    rc = lib().ref_frame_sample(mesh.h, _p(_f64(rest_x)), C.byref(ep), C.byref(cfg), _p(out))
+    if rc != 0:
+        raise RuntimeError(_err())
+    return {"target_s": out[0], "search_s": out[1], "iteration_s": out[2], "contact_rows": int(out[3]),
+            "colors": int(out[4])}
 
 
 def normal_flow_target(mesh: RefMesh, x, beta=5e-4, alpha_smooth=0.5):

@@ -290,6 +290,71 @@ double ref_incremental_energy(void* mp, const double* rest_x, const EnergyParams
     return incremental_energy(model, *m, to_pos(m->num_vertices(), x));
 }
 
+// Timed pieces of one simulation frame of the reference (seconds), for the
+// bench's reference arm: the Newton target (step()'s search, gradient /
+// Hessian, repulsion, PCG; dynamics.cpp:334-337), one proximity_search at the
+// start state (the cost of every re-search of resolve) and one non-search
+// Alg.-1 iteration at the start state towards the target (linearize_all,
+// warm-start-free color_constraints, assemble_lcp, pgs_sweeps, recover_target,
+// advance, refresh_distances, shrink_bound: resolve.cpp:84-137), all the
+// reference's own functions. out[0..2] = t_target, t_search, t_iteration;
+// out[3] = contact rows of that iteration; out[4] = colors.
+int ref_frame_sample(void* mp, const double* rest_x, const EnergyParams* ep, const or_config* cfg, double* out) {
+    auto* m = static_cast<MeshState*>(mp);
+    try {
+        using clk = std::chrono::steady_clock;
+        auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+        EnergyModel model = to_model(ep);
+        MeshState rest = *m;
+        rest.positions = to_pos(m->num_vertices(), rest_x);
+        model.prepare(rest);
+        const ResolveConfig rc = to_cfg(cfg);
+        const Positions x = m->positions;
+        const auto t0 = clk::now();
+        ProximitySet set0 = proximity_search(x, *m, rc.d_max);
+        GradientHessian gh = gradient_and_hessian(model, *m, x);
+        add_repulsion(model, set0, x, gh);
+        NewtonResult nt = newton_target(model, *m, x, gh);
+        const auto t1 = clk::now();
+        ProximitySet set = proximity_search(x, *m, rc.d_max);
+        const auto t2 = clk::now();
+        Positions yk1 = nt.y;
+        for (int v = 0; v < m->num_vertices(); ++v)
+            if (m->inv_mass[v] == 0.0) yk1[v] = x[v];
+        std::vector<double> targets(m->edges.size());
+        for (size_t e = 0; e < m->edges.size(); ++e) targets[e] = (yk1[m->edges[e][0]] - yk1[m->edges[e][1]]).norm();
+        AssemblyOptions opts;
+        opts.delta = rc.delta;
+        opts.sigma = rc.sigma;
+        opts.family = rc.family;
+        opts.edge_constraints = rc.edge_constraints;
+        AdvanceState st;
+        st.reset(x);
+        const auto t3 = clk::now();
+        std::vector<Constraint> rows = linearize_all(set, st.x, *m, targets, opts);
+        const int nc = color_constraints(rows, m->inv_mass, rc.color_seed);
+        LcpSystem sys = assemble_lcp(rows, st.x, yk1, m->inv_mass, nc);
+        pgs_sweeps(sys, rc.sweeps);
+        const Positions y = recover_target(sys, yk1);
+        advance(st, y, set, rc.gamma, m->inv_mass);
+        const double bound_before = set.bound;
+        refresh_distances(set, st.x);
+        shrink_bound(set, st.last_max_disp);
+        const auto t4 = clk::now();
+        (void)bound_before;
+        int contacts = 0;
+        for (const Constraint& c : rows) contacts += c.kind != ConstraintKind::EdgeLength;
+        out[0] = secs(t0, t1);
+        out[1] = secs(t1, t2);
+        out[2] = secs(t3, t4);
+        out[3] = contacts;
+        out[4] = nc;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 // ---- normal flow (normal_flow.cpp) ----
 int ref_normal_flow_target(void* mp, const double* x, double beta, double alpha_smooth,
                            double* y_out) {

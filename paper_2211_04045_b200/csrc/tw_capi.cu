@@ -561,7 +561,10 @@ int tw_ctx_create(int device, void* stream, tw_ctx** out) {
     if (stream) {
         ctx->stream = (cudaStream_t)stream;
     } else {
-        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        // a blocking stream: ordered with the legacy default stream, so callers
+        // that enqueue their inputs there (e.g. torch's default stream) never
+        // race the context's kernels
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault) != cudaSuccess) {
             delete ctx;
             return TW_ECUDA;
         }
