@@ -136,6 +136,12 @@ int tw_resolve(tw_ctx* ctx, tw_mesh* mesh, const double* x_start, const double* 
                const tw_resolve_config* cfg, double* x_out, tw_resolve_stats* stats,
                double* step_max_disp, double* path, tw_step_trace* trace);
 
+/* The path of the last resolve run with cfg->record_path (x^(0) .. x^(final),
+ * ResolveStats::path, resolve.hpp:48): kept on the device in a buffer that
+ * grows on demand (no step_limit-sized allocation); copies min(cap_states,
+ * states) states of nv * 3 doubles into out and the state count into *nstates. */
+int tw_last_path(tw_ctx* ctx, int64_t cap_states, double* out, int32_t* nstates);
+
 /* Same with device pointers already resident in HBM (nv * 3 doubles each). */
 int tw_resolve_device(tw_ctx* ctx, tw_mesh* mesh, const double* d_x_start,
                       const double* d_y_target, const tw_resolve_config* cfg, double* d_x_out,

@@ -66,7 +66,9 @@ EXPORTS = [
     "tw_mesh_destroy", "tw_resolve", "tw_resolve_device", "tw_stage_closest", "tw_stage_search",
     "tw_stage_refresh", "tw_stage_linearize", "tw_stage_color", "tw_stage_backward",
     "tw_stage_advance", "tw_ccd_certify", "tw_default_energy_model", "tw_dyn_create", "tw_dyn_destroy",
-    "tw_dyn_num_hinges", "tw_newton_target", "tw_step", "tw_step_device",
+    "tw_dyn_num_hinges", "tw_newton_target", "tw_step", "tw_step_device", "tw_stage_lcp",
+    "tw_stage_linearize_ex", "tw_stage_build_rows", "tw_stage_constraint_value", "tw_stage_fill_diag",
+    "tw_normal_flow_target", "tw_last_path",
 ]
 
 
@@ -124,6 +126,7 @@ def lib():
         L.tw_stage_color.argtypes = [P, P, C.c_int64, P, P, P, P, C.c_uint64, C.c_int32, C.c_int32, P, P]
         L.tw_stage_backward.argtypes = [P, C.c_int32, P, C.c_int64, P, P, P, P, P, C.c_int32, P, P, C.c_int32,
                                         C.c_int32, C.c_double, P, P, P]
+        L.tw_last_path.argtypes = [P, C.c_int64, P, C.POINTER(C.c_int32)]
         L.tw_default_energy_model.argtypes = [C.POINTER(EnergyModel)]
         L.tw_dyn_create.argtypes = [P, P, C.POINTER(EnergyModel), P, C.POINTER(P)]
         L.tw_dyn_destroy.argtypes = [P]
@@ -237,9 +240,8 @@ def resolve(ctx: Context, mesh: Mesh, x, y, trace=False, out=None, **kw):
     xo = np.zeros_like(x) if out is None else out
     st = Stats()
     smd = np.zeros(max(1, cfg.step_limit))
-    path = np.zeros((cfg.step_limit + 1, mesh.nv, 3)) if cfg.record_path else None
     tr = (StepTrace * cfg.step_limit)() if trace else None
-    rc = lib().tw_resolve(ctx.h, mesh.h, _p(x), _p(y), C.byref(cfg), _p(xo), C.byref(st), _p(smd), _p(path),
+    rc = lib().tw_resolve(ctx.h, mesh.h, _p(x), _p(y), C.byref(cfg), _p(xo), C.byref(st), _p(smd), None,
                           C.cast(tr, C.c_void_p) if tr is not None else None)
     if rc == TW_EINVAL:
         raise ValueError(lib().tw_last_error(ctx.h).decode())
@@ -248,8 +250,11 @@ def resolve(ctx: Context, mesh: Mesh, x, y, trace=False, out=None, **kw):
     ctx.check(rc)
     stats = {k: getattr(st, k) for k, _ in Stats._fields_}
     stats["step_max_disp"] = smd[:st.steps].copy()
-    if path is not None:
-        stats["path"] = path[:st.steps + 1].copy()
+    if cfg.record_path:  # exactly the recorded states (the device buffer grows on demand)
+        path = np.empty((st.steps + 1, mesh.nv, 3))
+        n = C.c_int32(0)
+        ctx.check(lib().tw_last_path(ctx.h, st.steps + 1, _p(path), C.byref(n)))
+        stats["path"] = path[:n.value]
     if tr is not None:
         stats["trace"] = [{k: getattr(tr[i], k) for k, _ in StepTrace._fields_} for i in range(st.steps)]
     return xo, stats

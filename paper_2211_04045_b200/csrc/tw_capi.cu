@@ -178,7 +178,12 @@ int ensure_buffers(tw_ctx* ctx, const tw_mesh* m, const tw_resolve_config& cfg) 
     CK(ctx->box.ensure(64));
     CK(ctx->smd.ensure((size_t)cfg.step_limit * 8));
     CK(ctx->trace.ensure((size_t)cfg.step_limit * sizeof(Trace)));
-    if (cfg.record_path) CK(ctx->path.ensure(((size_t)cfg.step_limit + 1) * nv * 24));
+    if (cfg.record_path) {
+        // the path buffer starts small and grows through the capacity retry
+        if (ctx->path_cap == 0) ctx->path_cap = 33;
+        ctx->path_cap = std::min(ctx->path_cap, cfg.step_limit + 1);
+        CK(ctx->path.ensure((size_t)ctx->path_cap * nv * 24));
+    }
     size_t tb = bvh_tmp_bytes(m->nv);  // the vertex order sorts nv codes
     for (int c = 0; c < 3; ++c) tb = std::max(tb, bvh_tmp_bytes(m->bvh[c].n));
 
@@ -297,6 +302,7 @@ Params make_params(tw_ctx* ctx, tw_mesh* m, const tw_resolve_config& c) {
     P.g = ctx->globals.as<Globals>();
     P.step_max_disp = ctx->smd.as<double>();
     P.path = c.record_path ? ctx->path.as<double>() : nullptr;
+    P.path_cap = c.record_path ? ctx->path_cap : 0;
     P.trace = ctx->trace.as<Trace>();
     P.dbg = ctx->dbg_dev;
     return P;
@@ -412,7 +418,7 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
                                            std::to_string(G.internal_line) + " (step " +
                                            std::to_string(G.steps) + ")");
         const int cap = G.error & (ERR_CAP_SLOTS | ERR_CAP_PAIRS | ERR_CAP_ARCH | ERR_CAP_COLORS | ERR_CAP_REFPOOL |
-                                   ERR_CAP_STACK | ERR_CAP_CAND);
+                                   ERR_CAP_STACK | ERR_CAP_CAND | ERR_CAP_PATH);
         if (!cap) break;
         if (++retries > 12) return fail(ctx, TW_ECAPACITY, "resolve: capacity growth did not converge");
         if (G.error & ERR_CAP_STACK) return fail(ctx, TW_ECAPACITY, "resolve: BVH traversal stack overflow");
@@ -422,8 +428,11 @@ int run_resolve(tw_ctx* ctx, tw_mesh* m, const double* d_xs, const double* d_ys,
         if (G.error & ERR_CAP_ARCH) grow_ll(ctx->arch_cap, ctx->arch_cap * 2);
         if (G.error & ERR_CAP_COLORS) ctx->colcap *= 4;
         if (G.error & ERR_CAP_REFPOOL) ctx->refpool_cap *= 4;
+        if (G.error & ERR_CAP_PATH) ctx->path_cap = std::min(cfg.step_limit + 1, ctx->path_cap * 4);
     }
     ctx->last = G;
+    ctx->last_path_states = cfg.record_path ? G.steps + 1 : 0;
+    ctx->last_nv = m->nv;
     std::memset(st, 0, sizeof *st);
     st->steps = G.steps;
     st->searches = G.searches;
@@ -554,6 +563,7 @@ int tw_ctx_create(int device, void* stream, tw_ctx** out) {
     if (const char* s = std::getenv("TW_QUERY_SLOTS")) ctx->K = std::max(4, std::atoi(s));
     if (std::getenv("TW_TINY_CAPS")) {  // start every capacity tiny: exercises the grow-and-rerun paths
         ctx->pcap = 256, ctx->ccap = 256, ctx->K = 4, ctx->arch_cap = 16, ctx->refpool_cap = 1024;
+        ctx->path_cap = 2;
         ctx->colcap = 8;
     }
     const int per_sm = std::max(1, std::min(resolve_blocks_per_sm(want), want));
@@ -809,6 +819,18 @@ int tw_resolve_device(tw_ctx* ctx, tw_mesh* m, const double* d_x, const double* 
 }
 
 // ---------------------------------------------------------------- stages
+int tw_last_path(tw_ctx* ctx, int64_t cap_states, double* out, int32_t* nstates) {
+    if (!ctx || !nstates || (cap_states > 0 && !out)) return fail(ctx, TW_EINVAL, "last_path: bad argument");
+    *nstates = ctx->last_path_states;
+    const int64_t n = std::min<int64_t>(cap_states, ctx->last_path_states);
+    if (n > 0) {
+        CK(cudaSetDevice(ctx->device));
+        CK(cudaMemcpyAsync(out, ctx->path.p, (size_t)n * ctx->last_nv * 24, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return TW_OK;
+}
+
 int32_t tw_ctx_phase_profile(const tw_ctx* ctx, int32_t* sites, double* ms, int32_t* counts, int32_t cap) {
     if (!ctx) return 0;
     int n = 0;

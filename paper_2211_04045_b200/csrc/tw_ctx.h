@@ -72,6 +72,7 @@ struct tw_ctx {
     long long arch_cap = 0;
     int colcap = 1024;
     long long refpool_cap = 0;
+    int path_cap = 0;  // record_path states on the device (grown on demand up to step_limit + 1)
     // buffers
     DevMem xs, ys, xo;  // N x 3 staging
     DevMem x, yk1, r, imp, dmin, voff, vcnt, vinc, c_slot, erank, part_v;
@@ -90,7 +91,9 @@ struct tw_ctx {
     // TW_DEBUG progress markers (host-mapped)
     int* dbg_host = nullptr;
     int* dbg_dev = nullptr;
-    tw::Globals last{};  // device globals of the last resolve (phase profile)
+    tw::Globals last{};
+    int last_path_states = 0;  // record_path states of the last resolve (kept on the device)
+    int last_nv = 0;  // device globals of the last resolve (phase profile)
 };
 
 struct tw_mesh {

@@ -33,6 +33,7 @@ enum : int {
     ERR_CAP_STACK = 64,   // BVH traversal stack overflow
     ERR_INTERNAL = 128,   // invariant violated (line in Globals::internal_line)
     ERR_CAP_CAND = 256,   // broad-phase candidate buffer full (count in Globals::ncand)
+    ERR_CAP_PATH = 512,   // record_path: more states than the path buffer holds
 };
 
 enum : uint8_t { PF_ACTIVE = 1, PF_ALL_STATIC = 2, PF_DEGENERATE = 4, PF_CONTACT = 8 };
@@ -218,6 +219,7 @@ struct Params {
     double* new_val;
     // reference coloring scratch
     long long refpool_cap;
+    int path_cap;    // record_path: states the path buffer holds
     int* refpool;
     // runs of consecutive PGS colors with at most this many rows each run on
     // one CTA (ph_pgs_tail); 0 disables

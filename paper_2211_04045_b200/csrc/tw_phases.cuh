@@ -1917,9 +1917,13 @@ __device__ void ph_advance(const Params& P, double bound, int step, long long nc
         }
         if (!isnan(P.r[v])) rs_bits = max(rs_bits, to_b(P.r[v]));  // max_remainder, advance.hpp:21-25
         if (P.cfg.record_path) {
-            const double4 xn = P.x[v];
-            double* o = P.path + ((long long)(step + 1) * P.nv + v) * 3;
-            o[0] = xn.x, o[1] = xn.y, o[2] = xn.z;
+            if (step + 1 < P.path_cap) {
+                const double4 xn = P.x[v];
+                double* o = P.path + ((long long)(step + 1) * P.nv + v) * 3;
+                o[0] = xn.x, o[1] = xn.y, o[2] = xn.z;
+            } else if (v == gtid()) {  // path buffer full: the host grows it and reruns
+                atomicOr(&P.g->error, ERR_CAP_PATH);
+            }
         }
     }
     md_bits = block_max_u64(md_bits);

@@ -81,3 +81,22 @@ def test_partner_sort_paths_agree(wide_slots, sc):
     xn, sn = capi.resolve(normal, mn, sc.x, sc.y, delta=5e-4, step_limit=3)
     xw, sw = capi.resolve(wide, mw, sc.x, sc.y, delta=5e-4, step_limit=3)
     assert np.array_equal(_bits(xn), _bits(xw)) and sn["num_pairs"] == sw["num_pairs"]
+
+
+def test_record_path_grows_on_demand(ctxs):
+    """record_path keeps the path on the device in a buffer that starts small
+    (2 states in a tiny context, 33 normally) and grows through the capacity
+    rerun: the recorded path has exactly steps + 1 states, starts at x, ends at
+    x_out, and equals a normally sized context's path bit for bit."""
+    normal, tiny = ctxs
+    for sc in S.scene_fixtures(0)[9:12]:  # random fixtures: tens to hundreds of steps
+        out = []
+        for c in (normal, tiny):
+            m = capi.Mesh.from_scene(c, sc)
+            x, st = capi.resolve(c, m, sc.x, sc.y, record_path=True)
+            p = st["path"]
+            assert len(p) == st["steps"] + 1
+            assert np.array_equal(_bits(p[0]), _bits(sc.x)) and np.array_equal(_bits(p[-1]), _bits(x))
+            out.append(p)
+            m.close()
+        assert np.array_equal(_bits(out[0]), _bits(out[1]))

@@ -1,0 +1,156 @@
+"""Parity at the benchmark sizes (BASELINE configs[1] reef knot 37K V / 71K T,
+configs[2] bow knot 75K V / 142K T), against committed digests of the REAL
+reference build's outputs (tests/golden/large_digests.json, written by
+tools/make_golden_large.py from oracle/_ref; the C oracle agreed bit for bit
+when they were made):
+
+  * the device proximity search at x and at y: sorted pair keys and
+    distances, bit for bit (sha256 of the exact bytes);
+  * resolve in reference-coloring mode: x_out, the per-step max displacement,
+    step / search counts and the per-step trace (pairs, contact rows = the
+    active-constraint set size, edge rows, colors, active pairs), bit for bit
+    with the reference;
+  * resolve in device-coloring mode: the same against the C oracle's
+    statement of the device coloring;
+  * device vs reference coloring: both converge and certify intersection-free
+    on the device certifier; on the non-penetrating targets the two outputs
+    agree within TOL_COLOR of the largest displacement (a different but valid
+    Gauss-Seidel order).
+The penetrating (+0.2 mm squeeze) targets run the reference-coloring replay for
+30+ steps (minutes on the one-thread replay): set TW_LARGE_REF=1 to include
+them in reference mode.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2211_04045_b200 import scenes as S
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "large_digests.json")
+DIGESTS = json.load(open(GOLD)) if os.path.exists(GOLD) else {}
+DELTA = 5e-4
+# device vs reference coloring on a non-penetrating target: |dx|_inf <= TOL_COLOR * max step
+TOL_COLOR = 0.05
+
+MAKE = {
+    "reef": lambda: S.reef_knot(),
+    "reef_pen": lambda: S.reef_knot(squeeze=0.2e-3),
+    "bow": lambda: S.bow_knot(),
+    "bow_pen": lambda: S.bow_knot(squeeze=0.2e-3),
+}
+NAMES = [n for n in MAKE if n in DIGESTS]
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2211_04045_b200 import capi
+
+    c = capi.Context(0)
+    yield c
+    c.close()
+
+
+_SCENES = {}
+
+
+def scene(name):
+    if name not in _SCENES:
+        _SCENES[name] = MAKE[name]()
+    return _SCENES[name]
+
+
+def _trace(st):
+    return [[t["num_pairs"], t["num_contact_rows"], t["num_edge_rows"], t["num_colors"], t["num_active_pairs"]]
+            for t in st["trace"]]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_scene_inputs_match_digest(name):
+    sc, d = scene(name), DIGESTS[name]
+    assert (sc.nv, len(sc.triangles), len(sc.edges)) == (d["nv"], d["nt"], d["ne"])
+    assert sha(sc.x) == d["x"] and sha(sc.y) == d["y"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_search_matches_reference(ctx, name):
+    from paper_2211_04045_b200 import capi
+
+    sc, d = scene(name), DIGESTS[name]
+    mesh = capi.Mesh.from_scene(ctx, sc)
+    for where, pos in (("x", sc.x), ("y", sc.y)):
+        P = capi.search(ctx, mesh, pos, 4e-3)
+        assert len(P) == d[f"search_{where}"]["n"], where
+        assert sha(P.keys) == d[f"search_{where}"]["keys"], where
+        assert sha(P.dist) == d[f"search_{where}"]["dist"], where
+    mesh.close()
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_resolve_device_coloring_matches_oracle(ctx, name):
+    from paper_2211_04045_b200 import capi
+
+    sc, d = scene(name), DIGESTS[name]["resolve_device"]
+    mesh = capi.Mesh.from_scene(ctx, sc)
+    x, st = capi.resolve(ctx, mesh, sc.x, sc.y, trace=True, delta=DELTA, coloring_mode="device")
+    assert (st["steps"], st["searches"], int(st["converged"])) == (d["steps"], d["searches"], d["converged"])
+    assert _trace(st) == d["trace"]
+    assert sha(st["step_max_disp"]) == d["step_max_disp"]
+    assert sha(x) == d["x_out"]
+    mesh.close()
+
+
+@pytest.mark.parametrize("name", [n for n in NAMES if not n.endswith("_pen") or os.environ.get("TW_LARGE_REF")])
+def test_resolve_reference_coloring_matches_reference(ctx, name):
+    from paper_2211_04045_b200 import capi
+
+    sc, d = scene(name), DIGESTS[name]["resolve_reference"]
+    mesh = capi.Mesh.from_scene(ctx, sc)
+    x, st = capi.resolve(ctx, mesh, sc.x, sc.y, trace=True, delta=DELTA, coloring_mode="reference")
+    assert (st["steps"], st["searches"], int(st["converged"])) == (d["steps"], d["searches"], d["converged"])
+    assert _trace(st) == d["trace"]
+    assert sha(st["step_max_disp"]) == d["step_max_disp"]
+    assert sha(x) == d["x_out"]
+    mesh.close()
+
+
+@pytest.mark.parametrize("name", [n for n in ("reef", "bow") if n in DIGESTS])
+def test_device_vs_reference_coloring_tolerance(ctx, name):
+    from paper_2211_04045_b200 import capi
+
+    sc = scene(name)
+    mesh = capi.Mesh.from_scene(ctx, sc)
+    xd, sd = capi.resolve(ctx, mesh, sc.x, sc.y, record_path=True, delta=DELTA, coloring_mode="device")
+    xr, sr = capi.resolve(ctx, mesh, sc.x, sc.y, record_path=True, delta=DELTA, coloring_mode="reference")
+    assert sd["converged"] and sr["converged"]
+    step = max(np.abs(xr - sc.x).max(), np.abs(xd - sc.x).max())
+    assert np.abs(xd - xr).max() <= TOL_COLOR * step, (np.abs(xd - xr).max(), step)
+    for st in (sd, sr):
+        assert capi.ccd_certify_path(ctx, mesh, st["path"])[1] == 0
+    mesh.close()
+
+
+@pytest.mark.parametrize("name", [n for n in ("reef_pen", "bow_pen") if n in DIGESTS])
+def test_penetrating_targets_certify(ctx, name):
+    """Penetrating targets: the device-coloring resolve converges and its whole
+    path certifies intersection-free (device certifier)."""
+    from paper_2211_04045_b200 import capi
+
+    sc = scene(name)
+    mesh = capi.Mesh.from_scene(ctx, sc)
+    x, st = capi.resolve(ctx, mesh, sc.x, sc.y, record_path=True, delta=DELTA, coloring_mode="device")
+    assert st["converged"]
+    viol, certain = capi.ccd_certify_path(ctx, mesh, st["path"])
+    assert certain == 0
+    mesh.close()
