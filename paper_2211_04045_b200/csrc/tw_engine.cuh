@@ -36,7 +36,12 @@ enum : int {
     ERR_CAP_PATH = 512,   // record_path: more states than the path buffer holds
 };
 
-enum : uint8_t { PF_ACTIVE = 1, PF_ALL_STATIC = 2, PF_DEGENERATE = 4, PF_CONTACT = 8 };
+// PF_FAR: the pair's last refresh found it inactive by distance with a margin
+// (d >= bound + kFarMargin); the Alg.-1 bound shrinks by exactly the distance
+// the pair's vertices can have closed since (2 max_disp per step), so it stays
+// inactive until the next search and later refreshes skip it.
+enum : uint8_t { PF_ACTIVE = 1, PF_ALL_STATIC = 2, PF_DEGENERATE = 4, PF_CONTACT = 8, PF_FAR = 16 };
+constexpr double kFarMargin = 1e-9;  // m: >> the FP slop of the bound / distance arithmetic
 
 struct Bvh {
     int n;            // primitives (leaves); nodes = 2n-1, internal 0..n-2, leaves n-1..2n-2

@@ -1995,6 +1995,8 @@ __device__ void ph_refresh(const Params& P, double bound, bool next_search) {
     const long long np = P.g->np;
     long long nact = 0, nev = 0;
     for_pair_tiles(P, np, [&](long long p) -> bool {
+        const uint8_t old_fl = P.pflag[p];
+        if (old_fl & PF_FAR) return false;  // provably still inactive: nothing observable changes
         ++nev;
         const uint64_t key = P.pkey[p];
         const int ka = key_ka(key), kb = key_kb(key);
@@ -2002,7 +2004,7 @@ __device__ void ph_refresh(const Params& P, double bound, bool next_search) {
         split_ids(ka, kb, P.pids[p], va, vb);
         Closest c;
         const int h = pair_closest(ka, va, kb, vb, XLoad{P.x}, c);
-        uint8_t fl = P.pflag[p] & PF_ALL_STATIC;
+        uint8_t fl = old_fl & PF_ALL_STATIC;
         double4 dd;
         double4 w;
         if (h != 1) {
@@ -2021,6 +2023,7 @@ __device__ void ph_refresh(const Params& P, double bound, bool next_search) {
             P.pdd[p] = dd;
             if (c.degenerate) fl |= PF_DEGENERATE;
             if (c.dist < bound) fl |= PF_ACTIVE;
+            else if (c.dist >= bound + kFarMargin) fl |= PF_FAR;
         }
         if (fl & PF_ACTIVE) {
             ++nact;
