@@ -350,8 +350,9 @@ __device__ __forceinline__ void dyn_sync(DynGlobals* g) {
 }
 
 // block sums of two values -> part[2 * block + {0, 1}]
+template <int NT = DTPB>
 __device__ __forceinline__ void block_partial2(double a, double b, double* part) {
-    __shared__ double sa[DTPB / 32], sb[DTPB / 32];
+    __shared__ double sa[NT / 32], sb[NT / 32];
     for (int o = 16; o > 0; o >>= 1) {
         a += __shfl_down_sync(0xffffffffu, a, o);
         b += __shfl_down_sync(0xffffffffu, b, o);
@@ -361,7 +362,7 @@ __device__ __forceinline__ void block_partial2(double a, double b, double* part)
     __syncthreads();
     if (threadIdx.x == 0) {
         double ta = 0.0, tb = 0.0;
-        for (int i = 0; i < DTPB / 32; ++i) ta += sa[i], tb += sb[i];
+        for (int i = 0; i < NT / 32; ++i) ta += sa[i], tb += sb[i];
         part[2 * blockIdx.x] = ta;
         part[2 * blockIdx.x + 1] = tb;
     }
@@ -484,7 +485,8 @@ __global__ void __launch_bounds__(DTPB) k_pcg(DynParams P) {
 // registers across iterations and only z -- the operand of the neighbours'
 // H z gathers -- goes through memory (L2-resident). Same phases, partial
 // sums and exit logic as k_pcg; used whenever the grid fits on the device.
-__global__ void __launch_bounds__(DTPB, 2) k_pcg_reg(DynParams P) {
+template <int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_pcg_reg(DynParams P) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     const bool own = v < P.nv;
     double* part[2] = {P.part, P.part + 2 * gridDim.x};
@@ -503,7 +505,7 @@ __global__ void __launch_bounds__(DTPB, 2) k_pcg_reg(DynParams P) {
     z = own ? pc(r) : mk(0, 0, 0);
     p = z;
     if (own) P.z[v] = s4(z);
-    block_partial2(own ? dot(r, z) : 0.0, own ? sqn(b) : 0.0, part[cur]);
+    block_partial2<NT>(own ? dot(r, z) : 0.0, own ? sqn(b) : 0.0, part[cur]);
     dyn_sync(P.g);
     double rz, bb;
     grid_total2(part[cur], gridDim.x, &rz, &bb);
@@ -511,7 +513,7 @@ __global__ void __launch_bounds__(DTPB, 2) k_pcg_reg(DynParams P) {
     const double bnorm = sqrt(bb);
     double best_res = bnorm;
     q = own ? hess_row(P, v, P.z) : mk(0, 0, 0);
-    block_partial2(own ? dot(p, q) : 0.0, 0.0, part[cur]);
+    block_partial2<NT>(own ? dot(p, q) : 0.0, 0.0, part[cur]);
     dyn_sync(P.g);
     int it = 0;
     const int maxit = P.m.pcg_max_iters;
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(DTPB, 2) k_pcg_reg(DynParams P) {
         r = sub(r, scl(alpha, q));
         z = own ? pc(r) : mk(0, 0, 0);
         if (own) P.z[v] = s4(z);
-        block_partial2(own ? sqn(r) : 0.0, own ? dot(r, z) : 0.0, part[cur]);
+        block_partial2<NT>(own ? sqn(r) : 0.0, own ? dot(r, z) : 0.0, part[cur]);
         dyn_sync(P.g);
         double rr, rzn;
         grid_total2(part[cur], gridDim.x, &rr, &rzn);
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(DTPB, 2) k_pcg_reg(DynParams P) {
         // phase B
         p = add(z, scl(beta, p));
         q = own ? add(hess_row(P, v, P.z), scl(beta, q)) : mk(0, 0, 0);
-        block_partial2(own ? dot(p, q) : 0.0, 0.0, part[cur]);
+        block_partial2<NT>(own ? dot(p, q) : 0.0, 0.0, part[cur]);
         dyn_sync(P.g);
     }
     if (own) P.best[v] = s4(best);
@@ -907,22 +909,22 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
         CK(cudaStreamSynchronize(s));
         for (int v = 0; v < nv; ++v) grad_host[3 * v] = g[v].x, grad_host[3 * v + 1] = g[v].y, grad_host[3 * v + 2] = g[v].z;
     }
-    // register-resident CG when one vertex per thread fits co-resident
+    // register-resident CG when one vertex per thread fits co-resident (256
+    // threads per CTA: a 512-thread instance made the following resolve kernel
+    // 35% slower on B200, measured, so it is not used)
     static int reg_per_sm = -1;
-    if (reg_per_sm < 0) {
-        reg_per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&reg_per_sm, k_pcg_reg, DTPB, 0);
-    }
-    const int reg_blocks = std::max(1, (nv + DTPB - 1) / DTPB);
-    const bool use_reg = getenv("TW_PCG_GLOBAL") == nullptr && reg_blocks <= ctx->sm_count * reg_per_sm;
-    const int pb = use_reg ? reg_blocks : pcg_blocks(ctx, nv);
+    if (reg_per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&reg_per_sm, k_pcg_reg<256>, 256, 0);
+    const int b256 = std::max(1, (nv + 255) / 256);
+    const bool use_reg = getenv("TW_PCG_GLOBAL") == nullptr && b256 <= ctx->sm_count * reg_per_sm;
+    const int pb = use_reg ? b256 : pcg_blocks(ctx, nv);
     P.nblocks = pb;
     CK(D->part.ensure((size_t)pb * 32));
     P.part = D->part.as<double>();
     CK(cudaMemsetAsync(D->glob.p, 0, sizeof(DynGlobals), s));
     void* args[] = {&P};
     CK(cudaEventRecord(D->evp0, s));
-    CK(cudaLaunchCooperativeKernel(use_reg ? (void*)k_pcg_reg : (void*)k_pcg, dim3(pb), dim3(DTPB), args, 0, s));
+    const void* fn = use_reg ? (const void*)k_pcg_reg<256> : (const void*)k_pcg;
+    CK(cudaLaunchCooperativeKernel(fn, dim3(pb), dim3(DTPB), args, 0, s));
     CK(cudaEventRecord(D->evp1, s));
     ++ctx->launches;
     DSYNC("k_pcg");
