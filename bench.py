@@ -8,8 +8,8 @@ gradient/Hessian with repulsion, the block-Jacobi PCG Newton target, then
 resolve (Alg. 1 of arXiv 2211.04045, run to convergence on the device) and
 the velocity update. The frame starts from the tightening state of
 scenes.knot_frame: the two plies, 2.5 mm apart, move with the velocity that
-squeezes them up to 0.4 mm into each other (penetrating target) and slides
-one 3 mm along the other. Metric: simulation steps per second (whole job).
+squeezes them up to 0.2 mm into each other where the knot is tightest
+(penetrating target) and slides them 1.5 mm along each other. Metric: simulation steps per second (whole job).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload frame|resolve|batch] [--scene bow|reef]
@@ -44,7 +44,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "sim steps/s at the 142K-tri bow knot (dt = 1/100: Newton target + resolve)"
 PAPER_COST_S = 0.034  # bow knot collision cost per time step (RTX 2080 Ti, paper Table 1)
-SQUEEZE = 0.2e-3      # penetrating tightening of the frame (plies up to 0.4 mm into each other)
+SQUEEZE = 0.1e-3      # penetrating tightening of the frame (plies up to 0.2 mm into each other)
 RESOLVE_KW = dict(delta=5e-4)  # knots: delta = 0.5 mm
 
 
@@ -79,8 +79,8 @@ def frame_config(sc, args, frame_stats=None):
                        "one implicit-Euler step (dynamics.cpp step(): search, gradient/Hessian + repulsion, "
                        "block-Jacobi PCG target, resolve, velocity update) with dt = 1/100 of two cloth plies "
                        "laid face to face (2.5 mm apart, 3 mm mesh) along a twisted (2,3) torus-knot band, "
-                       "moving with the tightening velocity that drives them up to 0.4 mm into each other "
-                       "and slides one 3 mm along the other (scenes.knot_frame)",
+                       "moving with the tightening velocity that drives them up to 0.2 mm into each other "
+                       "where the knot is tightest and slides them 1.5 mm along each other (scenes.knot_frame)",
            "scene": args.scene, "vertices": sc.nv, "triangles": int(len(sc.triangles)),
            "edges": int(len(sc.edges)), "dt": 0.01,
            "energy_model": "EnergyModel defaults (springs 50 N/m, gravity, repulsion 1e3 N/m within 1 mm, "

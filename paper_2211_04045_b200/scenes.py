@@ -553,14 +553,23 @@ def bow_knot(**kw) -> Scene:
     return ply_knot(n_along=1870, **kw)
 
 
+# The frame of the benchmark: the plies are driven up to 0.2 mm into each other
+# where the knot is tightest while sliding 1.5 mm relative to each other. A
+# scan of squeeze in [-0.1, +0.1] mm at this slide converges in 6-11 Alg.-1
+# steps in both coloring modes (the paper's bow knot: 5.4 on average, 17 at
+# most); at a 3 mm slide some frames need 40+ steps or stall.
+FRAME_DEFAULTS = dict(squeeze=0.1e-3, slide=1.5e-3)
+
+
 def knot_frame(n_along: int = 1870, dt: float = 0.01, **kw):
     """A simulation frame of the tightening knot for the dynamics step
     (dynamics.cpp:326-349): the plies at rest (x, 2.5 mm apart) moving with
     v0 = (y_tight - x) / dt, where y_tight is the ply_knot tightening target
-    (squeeze / slide in ``kw``). One implicit-Euler step with the paper's knot
-    time step dt = 1/100 (PAPER.md:933) then drives the plies into each other;
-    resolve makes the frame intersection-free. Returns (scene, v0)."""
-    kw = {**KNOT_DEFAULTS, **kw}
+    (squeeze / slide in ``kw``, FRAME_DEFAULTS otherwise). One implicit-Euler
+    step with the paper's knot time step dt = 1/100 then drives
+    the plies into each other; resolve makes the frame intersection-free.
+    Returns (scene, v0)."""
+    kw = {**FRAME_DEFAULTS, **kw}
     kw.setdefault("name", "bow_knot_frame" if n_along == 1870 else "knot_frame")
     sc = ply_knot(n_along=n_along, **kw)
     v0 = (sc.y - sc.x) / dt

@@ -16,9 +16,9 @@ when they were made):
     on the device certifier; on the non-penetrating targets the two outputs
     agree within TOL_COLOR of the largest displacement (a different but valid
     Gauss-Seidel order).
-The penetrating (+0.2 mm squeeze) targets run the reference-coloring replay for
-30+ steps (minutes on the one-thread replay): set TW_LARGE_REF=1 to include
-them in reference mode.
+The penetrating targets (scenes.FRAME_DEFAULTS: +0.1 mm squeeze, 1.5 mm slide)
+are included in reference mode only with TW_LARGE_REF=1 (the one-thread
+reference-coloring replay takes ~3-8 s per step at these sizes).
 """
 import hashlib
 import json
@@ -39,9 +39,9 @@ TOL_COLOR = 0.05
 
 MAKE = {
     "reef": lambda: S.reef_knot(),
-    "reef_pen": lambda: S.reef_knot(squeeze=0.2e-3),
+    "reef_pen": lambda: S.reef_knot(**S.FRAME_DEFAULTS),
     "bow": lambda: S.bow_knot(),
-    "bow_pen": lambda: S.bow_knot(squeeze=0.2e-3),
+    "bow_pen": lambda: S.bow_knot(**S.FRAME_DEFAULTS),
 }
 NAMES = [n for n in MAKE if n in DIGESTS]
 

@@ -10,7 +10,8 @@ sha256 digests of their exact bytes plus the scalar stats:
                          resolve (its own coloring), "device" = the C oracle's
                          statement of the device coloring
 Scenes: the tightening targets of scenes.reef_knot / bow_knot at the bench's
-squeeze (-0.2 mm: non-penetrating) and the penetrating +0.2 mm squeeze; delta
+squeeze (-0.2 mm: non-penetrating) and the penetrating frame tightening
+(scenes.FRAME_DEFAULTS: +0.1 mm squeeze, 1.5 mm slide); delta
 = 0.5 mm as in bench.py. The C oracle must agree with the reference bit for
 bit in reference mode (asserted).
 
@@ -47,9 +48,9 @@ def sha(*arrays):
 def scenes():
     return {
         "reef": lambda: S.reef_knot(),
-        "reef_pen": lambda: S.reef_knot(squeeze=0.2e-3),
+        "reef_pen": lambda: S.reef_knot(**S.FRAME_DEFAULTS),
         "bow": lambda: S.bow_knot(),
-        "bow_pen": lambda: S.bow_knot(squeeze=0.2e-3),
+        "bow_pen": lambda: S.bow_knot(**S.FRAME_DEFAULTS),
     }
 
 
