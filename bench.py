@@ -568,7 +568,7 @@ def reference_frame(scene, squeeze=SQUEEZE):
     return time.perf_counter() - t0, nsteps, nsearch, sc
 
 
-CPU_SAMPLE_ALONG = 187  # a tenth of the bow knot's length
+CPU_SAMPLE_ALONG = 467  # a quarter of the bow knot's length
 
 
 def cpu_baseline(args):

@@ -82,6 +82,12 @@ struct DynParams {
     // per edge (this Newton iteration)
     double4* e_u;            // (u, k * strain); u = 0 for an inactive edge
     double2* e_ab;           // (a, b): K = a I + b u u^T (0, 0 inactive)
+    // the same per vertex incidence (CSR order of vedge), written by k_grad_diag
+    // so the CG's H z gathers one level shallower: (u, b), a, and the other end
+    // (-1 when it is static: no z_o term; a = b = 0 for rows of static vertices)
+    double4* inc_u;
+    double* inc_a;
+    int* inc_o;
     // repulsive pairs: compacted records and the vertex -> slot CSR
     const uint64_t* pkey;
     const int4* pids;
@@ -222,6 +228,16 @@ __global__ void k_grad_diag(DynParams P) {
     }
     B[0] = B[4] = B[8] = s;
     P.sdiag[v] = s;
+    for (int k = P.vedge_off[v]; k < P.vedge_off[v + 1]; ++k) {  // incidence data for the CG
+        const int e = P.vedge[k];
+        const double4 u4 = P.e_u[e];
+        const double2 ab = dyn ? P.e_ab[e] : make_double2(0.0, 0.0);
+        const int2 ij = P.edges[e];
+        const int o = ij.x == v ? ij.y : ij.x;
+        P.inc_u[k] = make_double4(u4.x, u4.y, u4.z, ab.y);
+        P.inc_a[k] = ab.x;
+        P.inc_o[k] = P.inv_mass[o] != 0.0 ? o : -1;
+    }
     if (dyn) {
         for (int k = P.vedge_off[v]; k < P.vedge_off[v + 1]; ++k) {
             const int e = P.vedge[k];
@@ -291,16 +307,15 @@ __device__ __forceinline__ d3 hess_row(const DynParams& P, int v, const double4*
     d3 out = scl(P.sdiag[v], zv);
     if (dyn) {
         for (int k = P.vedge_off[v]; k < P.vedge_off[v + 1]; ++k) {
-            const int e = P.vedge[k];
-            const double2 ab = P.e_ab[e];
-            if (ab.x == 0.0 && ab.y == 0.0) continue;
-            const int2 ij = P.edges[e];
-            const int o = ij.x == v ? ij.y : ij.x;
-            const d3 u = l4(P.e_u[e]);
+            const double a = P.inc_a[k];
+            const double4 ub = P.inc_u[k];
+            if (a == 0.0 && ub.w == 0.0) continue;
+            const int o = P.inc_o[k];
+            const d3 u = l4(ub);
             // K z_v - K z_o (the second only when the other end is dynamic)
             d3 t = zv;
-            if (P.inv_mass[o] != 0.0) t = sub(zv, l4(z[o]));
-            out = add(out, add(scl(ab.x, t), scl(ab.y * dot(u, t), u)));
+            if (o >= 0) t = sub(zv, l4(z[o]));
+            out = add(out, add(scl(a, t), scl(ub.w * dot(u, t), u)));
         }
         for (int k = P.vh_off[v]; k < P.vh_off[v + 1]; ++k) {
             const int h = P.vh[k] >> 2, i = P.vh[k] & 3;
@@ -655,7 +670,7 @@ struct tw_dyn {
     tw_energy_model model{};
     int nh = 0;
     DevMem rest, hv, hk, vh_off, vh;
-    DevMem hx, hvel, x0, v0, xk, y, e_u, e_ab, rp_ids, rp_sw, rp_dir, rp_count, rs_key, rs_key2, vr_off, sort_tmp;
+    DevMem inc_u, inc_a, inc_o, hx, hvel, x0, v0, xk, y, e_u, e_ab, rp_ids, rp_sw, rp_dir, rp_count, rs_key, rs_key2, vr_off, sort_tmp;
     DevMem sdiag, grad, pre, b, d, r, z, p, q, best, part, glob;
     long long rp_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // step timing (the resolve uses the context's own events)
@@ -770,6 +785,9 @@ DynParams make_dparams(tw_dyn* D, const double* d_x) {
     P.x = d_x;
     P.e_u = D->e_u.as<double4>();
     P.e_ab = D->e_ab.as<double2>();
+    P.inc_u = D->inc_u.as<double4>();
+    P.inc_a = D->inc_a.as<double>();
+    P.inc_o = D->inc_o.as<int>();
     P.pkey = ctx->pkey.as<uint64_t>();
     P.pids = ctx->pids.as<int4>();
     P.pdd = ctx->pdd.as<double4>();
@@ -1002,6 +1020,9 @@ int ensure_state(tw_dyn* D) {
     CK(D->vr_off.ensure((nv + 1) * 4));
     CK(D->e_u.ensure(ne * 32));
     CK(D->e_ab.ensure(ne * 16));
+    CK(D->inc_u.ensure(2 * ne * 32));
+    CK(D->inc_a.ensure(2 * ne * 8));
+    CK(D->inc_o.ensure(2 * ne * 4));
     CK(D->rp_count.ensure(16));
     CK(D->glob.ensure(sizeof(DynGlobals)));
     if (D->rp_cap == 0) {
@@ -1090,7 +1111,7 @@ int tw_dyn_create(tw_ctx* ctx, tw_mesh* m, const tw_energy_model* model, const d
 void tw_dyn_destroy(tw_dyn* D) {
     if (!D) return;
     cudaSetDevice(D->ctx ? D->ctx->device : 0);
-    DevMem* all[] = {&D->hx, &D->hvel, &D->rest, &D->hv, &D->hk, &D->vh_off, &D->vh, &D->x0, &D->v0, &D->xk, &D->y, &D->e_u,
+    DevMem* all[] = {&D->inc_u, &D->inc_a, &D->inc_o, &D->hx, &D->hvel, &D->rest, &D->hv, &D->hk, &D->vh_off, &D->vh, &D->x0, &D->v0, &D->xk, &D->y, &D->e_u,
                      &D->e_ab, &D->rp_ids, &D->rp_sw, &D->rp_dir, &D->rp_count, &D->rs_key, &D->rs_key2,
                      &D->vr_off, &D->sort_tmp, &D->sdiag, &D->grad, &D->pre, &D->b, &D->d, &D->r, &D->z,
                      &D->p, &D->q, &D->best, &D->part, &D->glob};
