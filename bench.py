@@ -573,10 +573,11 @@ CPU_SAMPLE_ALONG = 467  # a quarter of the bow knot's length
 
 def cpu_baseline(args):
     """cpu_baseline of the ours-arm line (rank 0, N = 1): the reference build
-    on a bounded sample of the workload -- the same knot frame at a tenth of
-    the bow knot's length (~10-30 s of one core) -- timed once; value = its
-    frame rate divided by the size ratio (linear scaling, stated). The
-    unscaled full bow-knot frame is the --impl reference arm."""
+    on a bounded sample of the workload -- the same knot frame at a quarter of
+    the bow knot's length (~1 min of one core: 18,680 V, 8 resolve steps, 3
+    searches) -- timed once; value = its frame rate divided by the size ratio
+    (linear scaling, stated). The unscaled full bow-knot frame is the --impl
+    reference arm."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyref
 

@@ -1,20 +1,20 @@
 # Round measurement pass: default bench line (with cpu_baseline), the reference
-# arm, the ncu launch list of the bench command, and one --set full capture of
-# the resolve kernel and of the search stage. Each ncu pass only after the
-# same command exited 0 without ncu.
+# arm, the ncu launch list of the bench command, and --set full captures of the
+# frame's resolve kernel, its CG kernel and the search stage. Each ncu pass
+# only after the same command exited 0 without ncu.
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/bench_full.log 2> gpurun_out/bench_full.err; echo "bench rc=$?"
-tail -c 600 gpurun_out/bench_full.log
-timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
-tail -c 400 gpurun_out/bench_ref.log
-timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/b2.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+timeout 1500 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_full.log 2> gpurun_out/bench_full.err; echo "bench rc=$?"
+tail -c 400 gpurun_out/bench_full.log
+timeout 1800 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
+tail -c 600 gpurun_out/bench_ref.log
+timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/b2.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/ncu_launch.log 2>&1
 echo "launches rc=$?"
 timeout 300 python tools/prof_drive.py > gpurun_out/plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_resolve -c 1 \
+timeout 1200 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"k_resolve|k_pcg_reg" -c 2 \
     -o gpurun_out/prof_resolve -f python tools/prof_drive.py > gpurun_out/ncu_full.log 2>&1
-echo "ncu resolve rc=$?"; tail -2 gpurun_out/ncu_full.log
+echo "ncu frame rc=$?"; tail -2 gpurun_out/ncu_full.log
 timeout 300 python tools/prof_search.py > gpurun_out/plain2.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_stage -c 2 \
     -o gpurun_out/prof_search -f python tools/prof_search.py > gpurun_out/ncu_search.log 2>&1

@@ -98,7 +98,7 @@ def launch_summary(path):
         agg[r[ki]][1] += v
     tot = sum(t for _, t in agg.values())
     out = ["# ncu --metrics gpu__time_duration.sum --clock-control none launch list of",
-           "#   python bench.py --steps 2 --warmup 3 --no-cpu-baseline",
+           "#   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras",
            "# (cold-cache, serialised replay: compare shares, not absolute times)",
            f"{'launches':>8s} {'total ms':>10s} {'share':>7s}  kernel"]
     for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
@@ -111,12 +111,14 @@ def main():
     shutil.copy(os.path.join(OUT, "launches.csv"), os.path.join(PROF, f"{tag}_launches.csv"))
     open(os.path.join(PROF, f"{tag}_launch_summary.txt"), "w").write(launch_summary(os.path.join(OUT, "launches.csv")))
     json.dump(last_json(os.path.join(OUT, "bench_full.log")), open(os.path.join(PROF, f"{tag}_bench.json"), "w"), indent=1)
+    if os.path.exists(os.path.join(OUT, "acc_b200.log")):
+        shutil.copy(os.path.join(OUT, "acc_b200.log"), os.path.join(PROF, f"{tag}_reference_acceptance_on_b200.txt"))
     json.dump(last_json(os.path.join(OUT, "bench_ref.log")), open(os.path.join(PROF, f"{tag}_bench_reference.json"), "w"),
               indent=1)
     txt, h, u, rows = summarize(os.path.join(OUT, "prof_resolve.ncu-rep"), "k_resolve",
-                                "k_resolve: one bow-knot resolve (tools/prof_drive.py)")
+                                "k_pcg_reg + k_resolve: one bow-knot simulation frame (tools/prof_drive.py)")
     open(os.path.join(PROF, f"{tag}_ncu_resolve.txt"), "w").write(txt)
-    row = rows[0]
+    row = next(r for r in rows if "k_resolve" in r[h.index("Kernel Name")])
     gb = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
     rd = float(row[h.index("dram__bytes_read.sum")].replace(",", "")) * gb[u[h.index("dram__bytes_read.sum")]]
     wr = float(row[h.index("dram__bytes_write.sum")].replace(",", "")) * gb[u[h.index("dram__bytes_write.sum")]]

@@ -1,18 +1,20 @@
-"""Drive bow-knot resolves for ncu: warm-up calls (capacity growth happens
-there), then ONE profiled call inside cudaProfilerStart/Stop (run ncu with
---profile-from-start off so only that call's kernels are captured)."""
+"""Drive bow-knot simulation frames for ncu: warm-up steps (capacity growth
+happens there), then ONE profiled step inside cudaProfilerStart/Stop (run ncu
+with --profile-from-start off so only that step's kernels are captured:
+the search, the dynamics kernels, k_pcg_reg and k_resolve)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch
 from paper_2211_04045_b200 import capi, scenes as S
-sc = S.bow_knot()
+sc, v0 = S.knot_frame(n_along=1870)
 ctx = capi.Context(0)
 m = capi.Mesh.from_scene(ctx, sc)
+dyn = capi.Dynamics(ctx, m, sc.x)
 for i in range(3):
-    x, st = capi.resolve(ctx, m, sc.x, sc.y, delta=5e-4)
+    x, v, st = capi.step(ctx, m, dyn, sc.x, v0, delta=5e-4)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-x, st = capi.resolve(ctx, m, sc.x, sc.y, delta=5e-4)
+x, v, st = capi.step(ctx, m, dyn, sc.x, v0, delta=5e-4)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
-print("steps", st["steps"], "kernel_ms", st["kernel_ms"], "retries", st.get("retries"))
+print("frame", st)
