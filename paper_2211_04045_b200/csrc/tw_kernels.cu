@@ -456,8 +456,10 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
             SYNC();
         }
         if (C.solver == 0) {
-            // the color phases run on the first pgs_ctas CTAs (one per SM) with
-            // their own barrier; the rest of the grid waits at the join
+            // the color phases run on the first pgs_ctas block indices
+            // (sm_count x TW_PGS_CTAS_PER_SM, default 2 per SM on average; a
+            // cooperative launch does not fix their placement) behind their own
+            // sub-grid barrier; the rest of the grid waits at the join
             const int nsub = P.pgs_ctas;
             if ((int)blockIdx.x < nsub) {
                 for (int sw = 0; sw < C.sweeps; ++sw) {

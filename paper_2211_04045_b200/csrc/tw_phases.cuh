@@ -1771,7 +1771,7 @@ __device__ void ph_pgs_color(const Params& P, int c, int ncol_contact, int ncol_
 // color would cost a grid barrier for a handful of rows. small_color_run
 // returns the end of the run of consecutive colors with at most `tail_rows`
 // rows each that starts at cfirst; ph_pgs_tail runs such a run in order on
-// CTA 0 alone, with CTA barriers between colors (one grid barrier per run).
+// CTA 0 alone, with CTA barriers between colors (one sub-grid barrier per run).
 __device__ int small_color_run(const Params& P, int cfirst, int ncol, int ncol_contact, int ncol_edge,
                                long long tail_rows) {
     int c = cfirst;

@@ -100,3 +100,24 @@ def test_record_path_grows_on_demand(ctxs):
             out.append(p)
             m.close()
         assert np.array_equal(_bits(out[0]), _bits(out[1]))
+
+
+@pytest.mark.parametrize("ctas", ["1", "4"])
+def test_pgs_subgrid_size_is_invisible(normal, ctas):
+    """The PGS color phases run on a sub-grid of sm_count x TW_PGS_CTAS_PER_SM
+    CTAs (default 2): 1 and 4 per SM must give bit-identical results."""
+    os.environ["TW_PGS_CTAS_PER_SM"] = ctas
+    try:
+        other = capi.Context(0)
+    finally:
+        del os.environ["TW_PGS_CTAS_PER_SM"]
+    for sc, kw in [(S.scene_fixtures(0)[3], {}), (S.reef_knot(**S.FRAME_DEFAULTS), dict(delta=5e-4))]:
+        out = []
+        for c in (normal, other):
+            m = capi.Mesh.from_scene(c, sc)
+            x, st = capi.resolve(c, m, sc.x, sc.y, coloring_mode="device", **kw)
+            out.append((x, st["steps"], st["step_max_disp"]))
+            m.close()
+        assert np.array_equal(_bits(out[0][0]), _bits(out[1][0])) and out[0][1] == out[1][1]
+        assert np.array_equal(_bits(out[0][2]), _bits(out[1][2]))
+    other.close()

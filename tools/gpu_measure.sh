@@ -3,6 +3,7 @@
 # frame's resolve kernel, its CG kernel and the search stage. Each ncu pass
 # only after the same command exited 0 without ncu.
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+(time timeout 900 ./oracle/_ref/b200/acceptance_groups 1_2_6 3 4 10 11) > gpurun_out/acc_b200.log 2>&1
 timeout 1500 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_full.log 2> gpurun_out/bench_full.err; echo "bench rc=$?"
 tail -c 400 gpurun_out/bench_full.log
 timeout 1800 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
