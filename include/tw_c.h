@@ -110,6 +110,10 @@ void tw_default_config(tw_resolve_config* cfg);
 int tw_ctx_create(int device, void* stream, tw_ctx** out);
 void tw_ctx_destroy(tw_ctx* ctx);
 const char* tw_last_error(const tw_ctx* ctx);
+/* Share the device with parts - 1 other contexts that run concurrently on
+ * their own streams (independent scenes, BASELINE configs[4]): this context's
+ * persistent kernels use 1/parts of the co-resident CTAs. */
+int tw_ctx_set_grid_share(tw_ctx* ctx, int32_t parts);
 /* kernels launched by this context since creation */
 int64_t tw_ctx_kernel_launches(const tw_ctx* ctx);
 /* Per-phase wall time of the last resolve (CTA 0, barrier to barrier):

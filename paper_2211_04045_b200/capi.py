@@ -68,7 +68,7 @@ EXPORTS = [
     "tw_stage_advance", "tw_ccd_certify", "tw_default_energy_model", "tw_dyn_create", "tw_dyn_destroy",
     "tw_dyn_num_hinges", "tw_newton_target", "tw_step", "tw_step_device", "tw_stage_lcp",
     "tw_stage_linearize_ex", "tw_stage_build_rows", "tw_stage_constraint_value", "tw_stage_fill_diag",
-    "tw_normal_flow_target", "tw_last_path",
+    "tw_normal_flow_target", "tw_last_path", "tw_ctx_set_grid_share",
 ]
 
 
@@ -127,6 +127,7 @@ def lib():
         L.tw_stage_backward.argtypes = [P, C.c_int32, P, C.c_int64, P, P, P, P, P, C.c_int32, P, P, C.c_int32,
                                         C.c_int32, C.c_double, P, P, P]
         L.tw_last_path.argtypes = [P, C.c_int64, P, C.POINTER(C.c_int32)]
+        L.tw_ctx_set_grid_share.argtypes = [P, C.c_int32]
         L.tw_default_energy_model.argtypes = [C.POINTER(EnergyModel)]
         L.tw_dyn_create.argtypes = [P, P, C.POINTER(EnergyModel), P, C.POINTER(P)]
         L.tw_dyn_destroy.argtypes = [P]
@@ -174,6 +175,10 @@ class Context:
     def check(self, rc):
         if rc != TW_OK:
             raise TwError(rc, lib().tw_last_error(self.h).decode())
+
+    def set_grid_share(self, parts: int):
+        """Use 1/parts of the device (for parts concurrent contexts)."""
+        self.check(lib().tw_ctx_set_grid_share(self.h, int(parts)))
 
     @property
     def kernel_launches(self) -> int:

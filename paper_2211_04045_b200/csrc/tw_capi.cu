@@ -819,6 +819,15 @@ int tw_resolve_device(tw_ctx* ctx, tw_mesh* m, const double* d_x, const double* 
 }
 
 // ---------------------------------------------------------------- stages
+int tw_ctx_set_grid_share(tw_ctx* ctx, int32_t parts) {
+    if (!ctx || parts < 1) return fail(ctx, TW_EINVAL, "set_grid_share: parts must be >= 1");
+    const int per_sm = std::max(1, std::min(resolve_blocks_per_sm(ctx->minb), ctx->minb));
+    const int full = std::min(ctx->sm_count * per_sm, tw::MAX_BLOCKS);
+    ctx->grid_parts = parts;
+    ctx->nblocks = std::max(1, full / parts);
+    return TW_OK;
+}
+
 int tw_last_path(tw_ctx* ctx, int64_t cap_states, double* out, int32_t* nstates) {
     if (!ctx || !nstates || (cap_states > 0 && !out)) return fail(ctx, TW_EINVAL, "last_path: bad argument");
     *nstates = ctx->last_path_states;

@@ -59,6 +59,7 @@ struct tw_ctx {
     std::string err;
     int sm_count = 0;
     int nblocks = 0;
+    int grid_parts = 1;  // tw_ctx_set_grid_share: this context's share of the device
     int minb = 4;  // resolve-kernel instance (CTAs per SM)
     long long pgs_tail_rows = 256;  // TW_PGS_TAIL
     int pgs_per_sm = 2;             // TW_PGS_CTAS_PER_SM (measured: 1: 152, 2: 154.7, 4: 148.4 resolves/s)

@@ -933,8 +933,9 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
     static int reg_per_sm = -1;
     if (reg_per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&reg_per_sm, k_pcg_reg<256>, 256, 0);
     const int b256 = std::max(1, (nv + 255) / 256);
-    const bool use_reg = getenv("TW_PCG_GLOBAL") == nullptr && b256 <= ctx->sm_count * reg_per_sm;
-    const int pb = use_reg ? b256 : pcg_blocks(ctx, nv);
+    const int parts = std::max(1, ctx->grid_parts);  // concurrent contexts share the device
+    const bool use_reg = getenv("TW_PCG_GLOBAL") == nullptr && b256 <= ctx->sm_count * reg_per_sm / parts;
+    const int pb = use_reg ? b256 : std::max(1, pcg_blocks(ctx, nv) / parts);
     P.nblocks = pb;
     CK(D->part.ensure((size_t)pb * 32));
     P.part = D->part.as<double>();
