@@ -457,7 +457,7 @@ def run_resolve_only(ctx, args, coloring, steps):
     d_out = torch.empty_like(d_x)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    for _ in range(2):
+    for _ in range(2 if coloring == "device" else 1):
         capi.resolve_device_ptr(ctx, mesh, d_x.data_ptr(), d_y.data_ptr(), d_out.data_ptr(), **kw)
     ms, st = 0.0, None
     for i in range(steps):
@@ -473,6 +473,81 @@ def run_resolve_only(ctx, args, coloring, steps):
                         "gap, non-penetrating), inputs in HBM", "coloring": coloring,
             "resolves_per_s": round(steps / (ms / 1e3), 3), "ms": round(ms / steps, 4),
             "alg1_steps": st["steps"], "searches": st["searches"], "kernel_ms": round(st["kernel_ms"], 4)}
+
+
+def run_configs(ctx, args, peak):
+    """The other BASELINE configs on one B200, device-timed (inputs in HBM, L2
+    flushed between calls): configs[0] CFG1 cloth on a static sphere (resolve of
+    one dt = 1/30 fall; with the reference build's own resolve on the same input
+    timed on the host), configs[1] CFG2 the reef-knot frame (the headline's
+    step at half the size), configs[3] CFG4 the codimensional mix (closed
+    bodies, 1,000 strands, 96K particles: VV / VE / VT / EE pairs). Each with
+    the k_resolve roofline fraction."""
+    import torch
+
+    from paper_2211_04045_b200 import capi, scenes
+
+    out = {}
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    n = max(3, min(args.steps, 10))
+    for key, make, kw in (("cfg1_cloth_on_sphere", scenes.cloth_on_sphere, {}),
+                          ("cfg4_codim_mix", scenes.codim_mix, {})):
+        sc = make()
+        mesh = capi.Mesh.from_scene(ctx, sc)
+        d_x, d_y = torch.from_numpy(sc.x).cuda(), torch.from_numpy(sc.y).cuda()
+        d_o = torch.empty_like(d_x)
+        for _ in range(2):
+            capi.resolve_device_ptr(ctx, mesh, d_x.data_ptr(), d_y.data_ptr(), d_o.data_ptr(), **kw)
+        _, tr = capi.resolve(ctx, mesh, sc.x, sc.y, trace=True, **kw)
+        ms = kern = 0.0
+        for i in range(n):
+            flush.fill_(i & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st = capi.resolve_device_ptr(ctx, mesh, d_x.data_ptr(), d_y.data_ptr(), d_o.data_ptr(), **kw)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms += a.elapsed_time(b)
+            kern += st["kernel_ms"]
+        gbs = bytes_per_resolve(tr["trace"], sc) / (kern / n / 1e3) / 1e9
+        out[key] = {"vertices": sc.nv, "triangles": int(len(sc.triangles)), "edges": int(len(sc.edges)),
+                    "resolves_per_s": round(n / (ms / 1e3), 2), "ms": round(ms / n, 3),
+                    "alg1_steps": st["steps"], "searches": st["searches"], "final_pairs": st["num_pairs"],
+                    "roofline": {"kernel": "k_resolve", "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}}
+        if key.startswith("cfg1") and not args.no_cpu_baseline:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import pyref
+
+            if pyref.available():
+                rm = pyref.RefMesh.from_scene(sc)
+                t0 = time.perf_counter()
+                _, rs = pyref.resolve(rm, sc.x, sc.y, **kw)
+                secs = time.perf_counter() - t0
+                out[key]["cpu_baseline"] = {"value": round(1.0 / secs, 4), "unit": "resolves/s", "cores": 1,
+                                            "kind": "reference", "sample": f"one full resolve on the reference "
+                                            f"build: {secs:.1f} s, {rs['steps']} steps, {rs['searches']} searches"}
+        mesh.close()
+    fr = FrameRunner(ctx, "reef", args)
+    for _ in range(2):
+        fr.reset()
+        fr.step_device()
+    ms = 0.0
+    for i in range(n):
+        fr.reset()
+        flush.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        st = fr.step_device()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms += a.elapsed_time(b)
+    out["cfg2_reef_knot_frame"] = {"vertices": fr.sc.nv, "triangles": int(len(fr.sc.triangles)),
+                                   "steps_per_s": round(n / (ms / 1e3), 2), "ms": round(ms / n, 3),
+                                   "resolve_alg1_steps": st["resolve_steps"], "searches": st["searches"],
+                                   "pcg_ms": round(st["pcg_ms"], 3), "resolve_ms": round(st["resolve_ms"], 3)}
+    fr.close()
+    return out
 
 
 def partition(n, world, rank):
@@ -696,7 +771,8 @@ def main():
     out, ctx, sc = run_frame(args, D)
     if D.rank == 0 and D.world == 1 and not args.no_extras:
         out["resolve_only"] = run_resolve_only(ctx, args, "device", args.steps)
-        out["exact_parity_mode"] = run_resolve_only(ctx, args, "reference", max(2, args.steps // 5))
+        out["exact_parity_mode"] = run_resolve_only(ctx, args, "reference", 1)
+        out["configs"] = run_configs(ctx, args, peaks()[0])
         # configs[4] at N = 1: the N > 1 default workload (64 reef frames), so
         # the multi-GPU lines have their one-GPU point in the same run
         res = run_batch_frames(args, D, args.batch)
