@@ -412,7 +412,7 @@ def run_frame(args, D):
                       "pcg_iterations": avg("pcg_iterations"), "pcg_converged": stats[-1]["pcg_converged"],
                       "resolve_alg1_steps": avg("resolve_steps"), "resolve_searches": avg("searches"),
                       "resolve_converged": stats[-1]["resolve_converged"],
-                      "target_pairs": stats[-1]["num_pairs"], "repulsive_pairs": stats[-1]["repulsive_pairs"],
+                      "target_search_pairs": stats[-1]["num_pairs"], "repulsive_pairs": stats[-1]["repulsive_pairs"],
                       "fps_target_17": round(value / D.world, 2) >= 17.0,
                       "paper_collision_cost_ratio": round(PAPER_COST_S / (avg("resolve_ms") / 1e3), 3)},
             "resolve": {"alg1_steps": rtr["steps"], "searches": rtr["searches"], "final_pairs": rtr["num_pairs"],

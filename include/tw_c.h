@@ -286,7 +286,7 @@ typedef struct {
     int32_t resolve_converged;
     int32_t pcg_iterations;  /* summed over Newton iterations */
     int32_t pcg_converged;
-    int32_t num_pairs;       /* |P| of the last target search */
+    int32_t num_pairs;       /* pairs of the last target's search (cutoff min(d_max, repulsion_radius)) */
     int32_t repulsive_pairs; /* pairs closer than repulsion_radius */
     double device_ms;        /* CUDA-event time of the whole step on the device */
     double resolve_ms;       /* of which resolve */

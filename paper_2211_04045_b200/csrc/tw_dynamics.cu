@@ -500,35 +500,58 @@ __global__ void __launch_bounds__(DTPB) k_pcg(DynParams P) {
 // registers across iterations and only z -- the operand of the neighbours'
 // H z gathers -- goes through memory (L2-resident). Same phases, partial
 // sums and exit logic as k_pcg; used whenever the grid fits on the device.
-template <int NT>
-__global__ void __launch_bounds__(NT, 512 / NT) k_pcg_reg(DynParams P) {
-    const int v = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool own = v < P.nv;
+template <int NT, int VPT>
+__global__ void __launch_bounds__(NT, VPT == 1 ? 2 : 1) k_pcg_reg(DynParams P) {
+    // thread owns vertices (blockIdx.x * VPT + k) * NT + threadIdx.x, k < VPT
     double* part[2] = {P.part, P.part + 2 * gridDim.x};
     int cur = 0;
-    d3 b = mk(0, 0, 0), r, z, p, q, d = mk(0, 0, 0), best = mk(0, 0, 0);
-    double pre[9];
-    if (own) {
-        for (int k = 0; k < 9; ++k) pre[k] = P.pre[9 * (size_t)v + k];
-        if (P.inv_mass[v] != 0.0) b = neg(l4(P.grad[v]));
+    int vv[VPT];
+    bool own[VPT];
+    d3 b[VPT], r[VPT], z[VPT], p[VPT], q[VPT], d[VPT], best[VPT];
+    double pre[VPT][9];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        vv[k] = (blockIdx.x * VPT + k) * NT + threadIdx.x;
+        own[k] = vv[k] < P.nv;
+        b[k] = d[k] = best[k] = mk(0, 0, 0);
+        if (own[k]) {
+            for (int i = 0; i < 9; ++i) pre[k][i] = P.pre[9 * (size_t)vv[k] + i];
+            if (P.inv_mass[vv[k]] != 0.0) b[k] = neg(l4(P.grad[vv[k]]));
+        } else {
+            for (int i = 0; i < 9; ++i) pre[k][i] = 0.0;
+        }
     }
-    auto pc = [&](d3 x) {
-        return mk((pre[0] * x.x + pre[1] * x.y) + pre[2] * x.z, (pre[3] * x.x + pre[4] * x.y) + pre[5] * x.z,
-                  (pre[6] * x.x + pre[7] * x.y) + pre[8] * x.z);
+    auto pc = [&](int k, d3 x) {
+        const double* m = pre[k];
+        return mk((m[0] * x.x + m[1] * x.y) + m[2] * x.z, (m[3] * x.x + m[4] * x.y) + m[5] * x.z,
+                  (m[6] * x.x + m[7] * x.y) + m[8] * x.z);
     };
-    r = b;
-    z = own ? pc(r) : mk(0, 0, 0);
-    p = z;
-    if (own) P.z[v] = s4(z);
-    block_partial2<NT>(own ? dot(r, z) : 0.0, own ? sqn(b) : 0.0, part[cur]);
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        r[k] = b[k];
+        z[k] = own[k] ? pc(k, r[k]) : mk(0, 0, 0);
+        p[k] = z[k];
+        if (own[k]) {
+            P.z[vv[k]] = s4(z[k]);
+            s0 += dot(r[k], z[k]);
+            s1 += sqn(b[k]);
+        }
+    }
+    block_partial2<NT>(s0, s1, part[cur]);
     dyn_sync(P.g);
     double rz, bb;
     grid_total2(part[cur], gridDim.x, &rz, &bb);
     cur ^= 1;
     const double bnorm = sqrt(bb);
     double best_res = bnorm;
-    q = own ? hess_row(P, v, P.z) : mk(0, 0, 0);
-    block_partial2<NT>(own ? dot(p, q) : 0.0, 0.0, part[cur]);
+    s0 = 0.0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        q[k] = own[k] ? hess_row(P, vv[k], P.z) : mk(0, 0, 0);
+        if (own[k]) s0 += dot(p[k], q[k]);
+    }
+    block_partial2<NT>(s0, 0.0, part[cur]);
     dyn_sync(P.g);
     int it = 0;
     const int maxit = P.m.pcg_max_iters;
@@ -540,29 +563,43 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_pcg_reg(DynParams P) {
         if (pq <= 0.0) break;
         const double alpha = rz / pq;
         // phase A
-        d = add(d, scl(alpha, p));
-        r = sub(r, scl(alpha, q));
-        z = own ? pc(r) : mk(0, 0, 0);
-        if (own) P.z[v] = s4(z);
-        block_partial2<NT>(own ? sqn(r) : 0.0, own ? dot(r, z) : 0.0, part[cur]);
+        s0 = s1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            d[k] = add(d[k], scl(alpha, p[k]));
+            r[k] = sub(r[k], scl(alpha, q[k]));
+            z[k] = own[k] ? pc(k, r[k]) : mk(0, 0, 0);
+            if (own[k]) {
+                P.z[vv[k]] = s4(z[k]);
+                s0 += sqn(r[k]);
+                s1 += dot(r[k], z[k]);
+            }
+        }
+        block_partial2<NT>(s0, s1, part[cur]);
         dyn_sync(P.g);
         double rr, rzn;
         grid_total2(part[cur], gridDim.x, &rr, &rzn);
         cur ^= 1;
         const double res = sqrt(rr);
-        if (res < best_res) {
-            best_res = res;
-            best = d;
-        }
+        const bool improved = res < best_res;
+        if (improved) best_res = res;
         const double beta = rzn / rz;
         rz = rzn;
         // phase B
-        p = add(z, scl(beta, p));
-        q = own ? add(hess_row(P, v, P.z), scl(beta, q)) : mk(0, 0, 0);
-        block_partial2<NT>(own ? dot(p, q) : 0.0, 0.0, part[cur]);
+        s0 = 0.0;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            if (improved) best[k] = d[k];
+            p[k] = add(z[k], scl(beta, p[k]));
+            q[k] = own[k] ? add(hess_row(P, vv[k], P.z), scl(beta, q[k])) : mk(0, 0, 0);
+            if (own[k]) s0 += dot(p[k], q[k]);
+        }
+        block_partial2<NT>(s0, 0.0, part[cur]);
         dyn_sync(P.g);
     }
-    if (own) P.best[v] = s4(best);
+#pragma unroll
+    for (int k = 0; k < VPT; ++k)
+        if (own[k]) P.best[vv[k]] = s4(best[k]);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         P.g->iters = it;
         P.g->converged = best_res <= tol * bnorm ? 1 : 0;
@@ -877,9 +914,18 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
     k_pack_x4<<<std::max(1, nb), DTPB, 0, s>>>(nv, d_xk, m->d_inv_mass.as<double>(), ctx->x.as<double4>());
     ++ctx->launches;
     DSYNC("k_pack_x4");
+    // add_repulsion (dynamics.cpp:176-181) only reads pairs closer than the
+    // repulsion radius, and the search is exact (every pair below its cutoff,
+    // in key order), so searching with min(d_max, radius) yields exactly the
+    // repulsive pairs of step()'s d_max search -- in the same order -- at a
+    // fraction of the broad-phase cost; no repulsion, no search.
     long long np = 0;
-    int rc = search_at_x(ctx, m, d_max, &np);
-    if (rc) return rc;
+    const bool repel = D->model.repulsion_stiffness > 0.0 && D->model.repulsion_radius > 0.0;
+    if (repel) {
+        const int rc0 = search_at_x(ctx, m, std::min(d_max, D->model.repulsion_radius), &np);
+        if (rc0) return rc0;
+    }
+    int rc = TW_OK;
     if (D->rp_cap < np + 1) {
         D->rp_cap = np + 1024;
         CK(D->rp_ids.ensure((size_t)D->rp_cap * 16));
@@ -927,22 +973,31 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
         CK(cudaStreamSynchronize(s));
         for (int v = 0; v < nv; ++v) grad_host[3 * v] = g[v].x, grad_host[3 * v + 1] = g[v].y, grad_host[3 * v + 2] = g[v].z;
     }
-    // register-resident CG when one vertex per thread fits co-resident (256
-    // threads per CTA: a 512-thread instance made the following resolve kernel
-    // 35% slower on B200, measured, so it is not used)
-    static int reg_per_sm = -1;
-    if (reg_per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&reg_per_sm, k_pcg_reg<256>, 256, 0);
-    const int b256 = std::max(1, (nv + 255) / 256);
+    // register-resident CG: one vertex per thread (2 CTAs/SM) or, when that
+    // grid would not fit (or TW_PCG_VPT=2), two per thread at 1 CTA/SM. A
+    // 512-thread instance made the following resolve kernel 35% slower on
+    // B200 (measured), so CTAs stay at 256 threads.
+    static int occ[2] = {-1, -1};
+    if (occ[0] < 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_pcg_reg<256, 1>, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_pcg_reg<256, 2>, 256, 0);
+    }
     const int parts = std::max(1, ctx->grid_parts);  // concurrent contexts share the device
-    const bool use_reg = getenv("TW_PCG_GLOBAL") == nullptr && b256 <= ctx->sm_count * reg_per_sm / parts;
-    const int pb = use_reg ? b256 : std::max(1, pcg_blocks(ctx, nv) / parts);
+    const int b1 = std::max(1, (nv + 255) / 256), b2 = std::max(1, (nv + 511) / 512);
+    const char* vpt_env = getenv("TW_PCG_VPT");
+    const bool want2 = vpt_env && std::atoi(vpt_env) == 2;
+    const bool fit1 = b1 <= ctx->sm_count * occ[0] / parts, fit2 = b2 <= ctx->sm_count * occ[1] / parts;
+    const int vpt = getenv("TW_PCG_GLOBAL") ? 0 : (want2 && fit2) ? 2 : fit1 ? 1 : fit2 ? 2 : 0;
+    const bool use_reg = vpt != 0;
+    const int pb = vpt == 1 ? b1 : vpt == 2 ? b2 : std::max(1, pcg_blocks(ctx, nv) / parts);
     P.nblocks = pb;
     CK(D->part.ensure((size_t)pb * 32));
     P.part = D->part.as<double>();
     CK(cudaMemsetAsync(D->glob.p, 0, sizeof(DynGlobals), s));
     void* args[] = {&P};
     CK(cudaEventRecord(D->evp0, s));
-    const void* fn = use_reg ? (const void*)k_pcg_reg<256> : (const void*)k_pcg;
+    const void* fn = vpt == 1 ? (const void*)k_pcg_reg<256, 1> : vpt == 2 ? (const void*)k_pcg_reg<256, 2>
+                                                                        : (const void*)k_pcg;
     CK(cudaLaunchCooperativeKernel(fn, dim3(pb), dim3(DTPB), args, 0, s));
     CK(cudaEventRecord(D->evp1, s));
     ++ctx->launches;
