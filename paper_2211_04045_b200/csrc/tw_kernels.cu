@@ -583,7 +583,8 @@ __global__ void __launch_bounds__(TPB, 4) k_stage_search(Params P) {
 }
 
 // refresh + per-vertex bound into P.r (min(bound, dmin))
-__global__ void __launch_bounds__(TPB, 4) k_stage_refresh(Params P, double bound) {
+template <int MINB>
+__global__ void __launch_bounds__(TPB, MINB) k_stage_refresh(Params P, double bound) {
     ph_refresh(P, bound, false);
     if (!grid_sync(P.g)) return;
     for (long long v = gtid(); v < P.nv; v += gstride()) P.r[v] = mind(bound, to_d(P.dmin[v]));
@@ -1032,7 +1033,10 @@ cudaError_t coop_refresh(cudaStream_t s, const Params& P, int nblocks, double bo
     Params p = P;
     double b = bound;
     void* args[] = {&p, &b};
-    return coop((const void*)k_stage_refresh, s, nblocks, args);
+    // TW_REFRESH_MINB=2: the 128-register instance (register-budget experiment)
+    static const int minb = std::getenv("TW_REFRESH_MINB") ? std::atoi(std::getenv("TW_REFRESH_MINB")) : 4;
+    if (minb == 2) return coop((const void*)k_stage_refresh<2>, s, std::min(nblocks, resolve_blocks_per_sm(2) * 148), args);
+    return coop((const void*)k_stage_refresh<4>, s, nblocks, args);
 }
 cudaError_t coop_ccd(cudaStream_t s, const Params& P, int nblocks) {
     Params p = P;
