@@ -1462,11 +1462,23 @@ __device__ void ph_color_ref_fill(const Params& P, long long nc) {
     if (blockIdx.x == 0 && threadIdx.x == 0) adj_off[R] = (int)total;
 }
 
+// The smallest-last peel and the greedy pass of constraints.cpp:245-287 on
+// warp 0 of CTA 0. The order-carrying parts stay sequential (the random pick,
+// swap-pop, on lane 0); the per-neighbour work of a picked row is spread over
+// the 32 lanes with every bucket append landing at the position the sequential
+// loop would give it (lanes grouped by target bucket, ranked by neighbour
+// order: a bucket's contents and order are exactly the reference's), and the
+// greedy pass marks neighbour colors in parallel and finds the first free
+// color with ballots. Bit-identical to the one-thread replay (tests compare
+// with the oracle / the reference build), several times faster.
 __device__ void ph_color_ref(const Params& P, long long nc) {
-    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x;
+    const unsigned lt_mask = (1u << lane) - 1u;
     const long long R = nc + P.g->ner;
     if (R == 0) {
-        P.g->max_color = -1;
+        if (lane == 0) P.g->max_color = -1;
         return;
     }
     if (P.g->error) return;
@@ -1474,10 +1486,11 @@ __device__ void ph_color_ref(const Params& P, long long nc) {
     const int* adj_start = pool;
     const int* adj_len = pool + R + 1;
     const int* adj = pool + 2 * R + 2;
-    long long top = 2 * R + 2 + adj_start[R];
+    long long top = 2 * R + 2 + adj_start[R];  // identical on every lane (allocations are warp-uniform)
+    bool bad = false;
     auto alloc = [&](long long n) -> int* {
         if (top + n > P.refpool_cap) {
-            atomicOr(&P.g->error, ERR_CAP_REFPOOL);
+            bad = true;
             return nullptr;
         }
         int* p = pool + top;
@@ -1488,83 +1501,151 @@ __device__ void ph_color_ref(const Params& P, long long nc) {
     int* order = alloc(R);
     int* removed = alloc(R);
     int* used = alloc(R + 1);
-    if (!used) return;
+    if (bad) {
+        if (lane == 0) atomicOr(&P.g->error, ERR_CAP_REFPOOL);
+        return;
+    }
     int max_deg = 0;
-    for (long long i = 0; i < R; ++i) {
+    for (long long i = lane; i < R; i += 32) {
         degree[i] = adj_len[i];
         removed[i] = 0;
-        if (degree[i] > max_deg) max_deg = degree[i];
+        max_deg = max(max_deg, adj_len[i]);
     }
+    for (int o = 16; o > 0; o >>= 1) max_deg = max(max_deg, __shfl_xor_sync(FULL, max_deg, o));
     // buckets as growable vectors in the pool: (ptr offset, size, cap)
     int* bptr = alloc(max_deg + 1);
     int* bsize = alloc(max_deg + 1);
     int* bcap = alloc(max_deg + 1);
-    if (!bcap) return;
-    for (int d = 0; d <= max_deg; ++d) bptr[d] = -1, bsize[d] = 0, bcap[d] = 0;
-    auto bpush = [&](int d, int x) {
-        if (bsize[d] == bcap[d]) {
-            const int nc2 = bcap[d] ? bcap[d] * 2 : 4;
-            int* nb = alloc(nc2);
-            if (!nb) return;
-            for (int i = 0; i < bsize[d]; ++i) nb[i] = pool[bptr[d] + i];
-            bptr[d] = (int)(nb - pool);
-            bcap[d] = nc2;
+    if (bad) {
+        if (lane == 0) atomicOr(&P.g->error, ERR_CAP_REFPOOL);
+        return;
+    }
+    for (int d = lane; d <= max_deg; d += 32) bptr[d] = -1, bsize[d] = 0, bcap[d] = 0;
+    __syncwarp();
+    // Appends x to bucket d for every active lane, in lane order within a
+    // bucket (= the sequential order of the pushes); a full bucket doubles
+    // (4, 8, 16, ...) with its contents copied, as the sequential growth does.
+    auto warp_push = [&](bool act, int d, int x) {
+        unsigned m = __ballot_sync(FULL, act);
+        while (m) {
+            const int leader = __ffs(m) - 1;
+            const int dl = __shfl_sync(FULL, d, leader);
+            const unsigned grp = __ballot_sync(FULL, act && d == dl);
+            const int cnt = __popc(grp);
+            int base = 0, ptr = 0;
+            if (lane == leader) {
+                const int need = bsize[dl] + cnt;
+                if (need > bcap[dl]) {
+                    int cap = bcap[dl];
+                    while (cap < need) cap = cap ? cap * 2 : 4;
+                    int* nb = alloc(cap);
+                    if (nb) {
+                        for (int i = 0; i < bsize[dl]; ++i) nb[i] = pool[bptr[dl] + i];
+                        bptr[dl] = (int)(nb - pool);
+                        bcap[dl] = cap;
+                    }
+                }
+                base = bsize[dl];
+                ptr = bptr[dl];
+                if (!bad) bsize[dl] = need;
+            }
+            top = __shfl_sync(FULL, top, leader);
+            bad = __shfl_sync(FULL, bad ? 1 : 0, leader) != 0;
+            base = __shfl_sync(FULL, base, leader);
+            ptr = __shfl_sync(FULL, ptr, leader);
+            if (!bad && act && d == dl) pool[ptr + base + __popc(grp & lt_mask)] = x;
+            m &= ~grp;
         }
-        pool[bptr[d] + bsize[d]++] = x;
+        __syncwarp();
     };
-    for (long long i = 0; i < R; ++i) bpush(degree[i], (int)i);
-    if (P.g->error) return;
+    for (long long i0 = 0; i0 < R && !bad; i0 += 32) {
+        const long long i = i0 + lane;
+        warp_push(i < R, i < R ? degree[i] : 0, (int)i);
+    }
+    if (bad) {
+        if (lane == 0) atomicOr(&P.g->error, ERR_CAP_REFPOOL);
+        return;
+    }
     Mt64 rng;
-    rng.seed(P.cfg.color_seed);
+    if (lane == 0) rng.seed(P.cfg.color_seed);
     for (long long picked = 0; picked < R; ++picked) {
-        int d = 0, cand = -1;
-        while (cand < 0) {
-            while (d <= max_deg && bsize[d] == 0) ++d;
-            TW_INVARIANT(d <= max_deg);
-            const unsigned long long at = rng.below((unsigned long long)bsize[d]);
-            TW_INVARIANT(at < (unsigned long long)bsize[d] && bptr[d] >= 0);
-            int* b = pool + bptr[d];
-            const int c = b[at];
-            TW_INVARIANT(c >= 0 && c < R);
-            b[at] = b[bsize[d] - 1];
-            --bsize[d];
-            if (!removed[c] && degree[c] == d) cand = c;
-        }
-        removed[cand] = 1;
-        order[picked] = cand;
-        for (int k = adj_start[cand]; k < adj_start[cand] + adj_len[cand]; ++k) {
-            const int nb = adj[k];
-            TW_INVARIANT(nb >= 0 && nb < R);
-            if (!removed[nb]) {
-                TW_INVARIANT(degree[nb] > 0);
-                bpush(--degree[nb], nb);
+        int cand = -1;
+        if (lane == 0) {
+            int d = 0;
+            while (cand < 0) {
+                while (d <= max_deg && bsize[d] == 0) ++d;
+                if (d > max_deg) break;  // invariant broken (reported below)
+                const unsigned long long at = rng.below((unsigned long long)bsize[d]);
+                int* b = pool + bptr[d];
+                const int c = b[at];
+                if (c < 0 || c >= R) break;
+                b[at] = b[bsize[d] - 1];
+                --bsize[d];
+                if (!removed[c] && degree[c] == d) cand = c;
+            }
+            if (cand >= 0) {
+                removed[cand] = 1;
+                order[picked] = cand;
             }
         }
-        if (P.g->error) return;
+        cand = __shfl_sync(FULL, cand, 0);
+        __syncwarp();
+        if (cand < 0) {  // the peel ran out of candidates: an invariant is broken
+            if (lane == 0) {
+                atomicOr(&P.g->error, ERR_INTERNAL);
+                P.g->internal_line = __LINE__;
+            }
+            return;
+        }
+        const int k0 = adj_start[cand], k1 = k0 + adj_len[cand];
+        for (int kb = k0; kb < k1 && !bad; kb += 32) {
+            const int k = kb + lane;
+            int nb = -1, nd = 0;
+            bool act = false;
+            if (k < k1) {
+                nb = adj[k];
+                if (!removed[nb]) {  // distinct neighbours: no two lanes touch one degree
+                    nd = --degree[nb];
+                    act = true;
+                }
+            }
+            warp_push(act, nd, nb);
+        }
+        if (bad) {
+            if (lane == 0) atomicOr(&P.g->error, ERR_CAP_REFPOOL);
+            return;
+        }
     }
     // colors: -1 initially
+    for (long long r = lane; r < nc; r += 32) P.c_color[r] = -1;
+    for (long long k = lane; k < P.g->ner; k += 32) P.er_color[P.er_edge[k]] = -1;
+    for (long long i = lane; i <= R; i += 32) used[i] = -1;
+    __syncwarp();
     auto color_of = [&](long long r) -> int {
         return r < nc ? P.c_color[r] : P.er_color[P.er_edge[r - nc]];
     };
-    for (long long r = 0; r < nc; ++r) P.c_color[r] = -1;
-    for (long long k = 0; k < P.g->ner; ++k) P.er_color[P.er_edge[k]] = -1;
-    for (long long i = 0; i <= R; ++i) used[i] = -1;
     int maxc = -1;
     for (long long it = R - 1; it >= 0; --it) {
         const int i = order[it];
-        TW_INVARIANT(i >= 0 && i < R);
-        for (int k = adj_start[i]; k < adj_start[i] + adj_len[i]; ++k) {
+        for (int k = adj_start[i] + lane; k < adj_start[i] + adj_len[i]; k += 32) {
             const int c = color_of(adj[k]);
-            TW_INVARIANT(c < R);
             if (c >= 0) used[c] = i;
         }
-        int col = 0;
-        while (used[col] == i) ++col;
-        if (i < nc) P.c_color[i] = col;
-        else P.er_color[P.er_edge[i - nc]] = col;
-        if (col > maxc) maxc = col;
+        __syncwarp();
+        int col = -1;
+        for (int c0 = 0; col < 0; c0 += 32) {  // used has R + 1 slots: a free color always exists
+            const unsigned busy = __ballot_sync(FULL, c0 + lane <= R && used[c0 + lane] == i);
+            const unsigned freeb = ~busy;
+            if (freeb) col = c0 + __ffs(freeb) - 1;
+        }
+        if (lane == 0) {
+            if (i < nc) P.c_color[i] = col;
+            else P.er_color[P.er_edge[i - nc]] = col;
+        }
+        maxc = max(maxc, col);
+        __syncwarp();
     }
-    P.g->max_color = maxc;
+    if (lane == 0) P.g->max_color = maxc;
 }
 
 // D: bucket rows by color. Contact counts ccount come from the coloring

@@ -184,3 +184,45 @@ def test_friction_is_rejected(ctx):
         capi.step(ctx, mesh, d2, x, v)
     with pytest.raises(ValueError):
         capi.Dynamics(ctx, mesh, x, dt=0.0)
+
+
+def test_concurrent_contexts_are_deterministic():
+    """Two contexts sharing the device (tw_ctx_set_grid_share, own streams,
+    threads) step independent frames at the same time and return bit for bit
+    what one full-device context returns (the configs[4] batch mode)."""
+    import threading
+
+    from paper_2211_04045_b200 import capi
+
+    scenes = [S.knot_frame(n_along=300, jitter_seed=s) for s in (1, 2, 3, 4)]
+    solo = capi.Context(0)
+    ref = []
+    for sc, v in scenes:
+        m = capi.Mesh.from_scene(solo, sc)
+        d = capi.Dynamics(solo, m, sc.x)
+        ref.append(capi.step(solo, m, d, sc.x, v, delta=5e-4)[:2])
+        d.close()
+        m.close()
+    solo.close()
+    out = [None] * len(scenes)
+
+    def work(k):
+        c = capi.Context(0)
+        c.set_grid_share(2)
+        for i in range(k, len(scenes), 2):
+            sc, v = scenes[i]
+            m = capi.Mesh.from_scene(c, sc)
+            d = capi.Dynamics(c, m, sc.x)
+            out[i] = capi.step(c, m, d, sc.x, v, delta=5e-4)[:2]
+            d.close()
+            m.close()
+        c.close()
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for (xa, va), (xb, vb) in zip(ref, out):
+        assert np.array_equal(xa.view(np.uint64), xb.view(np.uint64))
+        assert np.array_equal(va.view(np.uint64), vb.view(np.uint64))
