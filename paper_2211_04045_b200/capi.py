@@ -128,6 +128,10 @@ def lib():
                                         C.c_int32, C.c_double, P, P, P]
         L.tw_last_path.argtypes = [P, C.c_int64, P, C.POINTER(C.c_int32)]
         L.tw_ctx_set_grid_share.argtypes = [P, C.c_int32]
+        L.tw_stage_linearize_ex.argtypes = [P, P, P, C.c_int64, P, P, P, P, P, P, P, C.c_double, C.c_double,
+                                            C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P, P, P, P, P, P, P]
+        L.tw_stage_constraint_value.argtypes = [P, C.c_int32, P, C.c_int64, P, P, P, P, P, P, P, P]
+        L.tw_normal_flow_target.argtypes = [P, C.c_int32, P, C.c_int32, P, C.c_double, C.c_double, P]
         L.tw_default_energy_model.argtypes = [C.POINTER(EnergyModel)]
         L.tw_dyn_create.argtypes = [P, P, C.POINTER(EnergyModel), P, C.POINTER(P)]
         L.tw_dyn_destroy.argtypes = [P]
@@ -395,7 +399,7 @@ class Rows:
 
 
 def linearize(ctx: Context, mesh: Mesh, x, pairs: Pairs, edge_targets, delta=1e-3, sigma=1.1, family=0,
-              edge_constraints=True) -> Rows:
+              edge_constraints=True, ex=False) -> Rows:
     """linearize_all (constraints.cpp:181-220) on the device."""
     x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
     et = np.ascontiguousarray(edge_targets if edge_targets is not None else np.zeros(1), np.float64)
@@ -403,12 +407,52 @@ def linearize(ctx: Context, mesh: Mesh, x, pairs: Pairs, edge_targets, delta=1e-
     cap = len(pairs) + len(mesh.edges) + 16
     R = Rows(cap)
     n = C.c_int64(0)
-    ctx.check(lib().tw_stage_linearize(ctx.h, mesh.h, _p(x), len(pairs), _p(pairs.keys), _p(pairs.dist),
-                                       _p(pairs.wa), _p(pairs.wb), _p(pairs.dir), _p(pairs.flags), _p(et), delta,
-                                       sigma, family, int(bool(edge_constraints)), cap, _p(R.kind), _p(R.verts),
-                                       _p(R.value), _p(R.jac), _p(R.diag), _p(R.pair_key), _p(R.edge_index),
-                                       C.byref(n)))
-    return R.take(n.value)
+    if not ex:
+        ctx.check(lib().tw_stage_linearize(ctx.h, mesh.h, _p(x), len(pairs), _p(pairs.keys), _p(pairs.dist),
+                                           _p(pairs.wa), _p(pairs.wb), _p(pairs.dir), _p(pairs.flags), _p(et),
+                                           delta, sigma, family, int(bool(edge_constraints)), cap, _p(R.kind),
+                                           _p(R.verts), _p(R.value), _p(R.jac), _p(R.diag), _p(R.pair_key),
+                                           _p(R.edge_index), C.byref(n)))
+        return R.take(n.value)
+    # tw_stage_linearize_ex: plus each row's re-evaluation data
+    flavor, refv = np.zeros(cap, np.uint8), np.zeros(cap)
+    gw, den = np.zeros((cap, 4)), np.zeros(cap)
+    ctx.check(lib().tw_stage_linearize_ex(ctx.h, mesh.h, _p(x), len(pairs), _p(pairs.keys), _p(pairs.dist),
+                                          _p(pairs.wa), _p(pairs.wb), _p(pairs.dir), _p(pairs.flags), _p(et),
+                                          delta, sigma, family, int(bool(edge_constraints)), cap, _p(R.kind),
+                                          _p(R.verts), _p(R.value), _p(R.jac), _p(R.diag), _p(R.pair_key),
+                                          _p(R.edge_index), _p(flavor), _p(refv), _p(gw), _p(den), C.byref(n)))
+    out = R.take(n.value)
+    k = n.value
+    out.flavor, out.ref_volume, out.gap_weights, out.denom = flavor[:k], refv[:k], gw[:k], den[:k]
+    return out
+
+
+def constraint_value_at(ctx: Context, rows, x, sigma=1.1):
+    """constraint_value_at (constraints.cpp:39-54) of every row (rows from linearize(..., ex=True))."""
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    n = len(rows)
+    nv_rows = np.ascontiguousarray((rows.verts >= 0).sum(1), np.int32)
+    out = np.zeros(max(1, n))
+    sig = np.full(max(1, n), sigma)
+    ctx.check(lib().tw_stage_constraint_value(ctx.h, len(x), _p(x), n, _p(np.ascontiguousarray(rows.flavor, np.uint8)),
+                                              _p(nv_rows), _p(np.ascontiguousarray(rows.verts, np.int32)),
+                                              _p(np.ascontiguousarray(rows.ref_volume)),
+                                              _p(np.ascontiguousarray(rows.gap_weights)),
+                                              _p(np.ascontiguousarray(rows.denom)), _p(sig), _p(out)))
+    return out[:n]
+
+
+def normal_flow_target(ctx: Context, x, triangles, beta=5e-4, alpha=0.5):
+    """normal_flow_target (normal_flow.cpp:38-81) on the device."""
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(triangles, np.int32).reshape(-1, 3)
+    y = np.zeros_like(x)
+    rc = lib().tw_normal_flow_target(ctx.h, len(x), _p(x), len(t), _p(t), beta, alpha, _p(y))
+    if rc == TW_EINVAL:
+        raise ValueError(lib().tw_last_error(ctx.h).decode())
+    ctx.check(rc)
+    return y
 
 
 def color(ctx: Context, mesh: Mesh, rows: Rows, seed=0x5EED, mode="device", edge_constraints=True):
