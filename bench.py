@@ -74,7 +74,7 @@ def frame_scene(scene, jitter=None):
     return scenes.knot_frame(n_along=n_along(scene), squeeze=SQUEEZE, jitter_seed=jitter)
 
 
-def frame_config(sc, args, frame_stats=None):
+def frame_config(sc, args):
     cfg = {"workload": f"{sc.name}: {sc.nv} vertices, {len(sc.triangles)} triangles, {len(sc.edges)} edges; "
                        "one implicit-Euler step (dynamics.cpp step(): search, gradient/Hessian + repulsion, "
                        "block-Jacobi PCG target, resolve, velocity update) with dt = 1/100 of two cloth plies "

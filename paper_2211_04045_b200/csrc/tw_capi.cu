@@ -1440,10 +1440,10 @@ int tw_stage_build_rows(tw_ctx* ctx, int32_t nv, const double* x, int64_t n, con
     double *oval = S.out<double>(n), *ojac = S.out<double>(12 * n), *orefv = S.out<double>(n),
            *ogw = S.out<double>(4 * n), *oden = S.out<double>(n);
     if (S.err) return cuda_fail(ctx, S.err, "build_rows: upload");
-    launch_build_rows(nullptr, dx, n, dk, dv, dc, delta, gap ? 1 : 0, okind, onv, orv, oval, ojac, ofl, orefv, ogw,
+    launch_build_rows(ctx->stream, dx, n, dk, dv, dc, delta, gap ? 1 : 0, okind, onv, orv, oval, ojac, ofl, orefv, ogw,
                       oden);
     ++ctx->launches;
-    CK(cudaDeviceSynchronize());
+    CK(cudaStreamSynchronize(ctx->stream));
     std::vector<int> hk(n), hf(n);
     S.down(hk.data(), okind, n);
     S.down(nverts, onv, n);
@@ -1485,9 +1485,9 @@ int tw_stage_constraint_value(tw_ctx* ctx, int32_t nv, const double* x, int64_t 
     const double* ds = S.up(sigma, n);
     double* dout = S.out<double>(n);
     if (S.err) return cuda_fail(ctx, S.err, "constraint_value: upload");
-    launch_value_at(nullptr, dx, n, df, dn, dv, drv, dg, dd, ds, dout);
+    launch_value_at(ctx->stream, dx, n, df, dn, dv, drv, dg, dd, ds, dout);
     ++ctx->launches;
-    CK(cudaDeviceSynchronize());
+    CK(cudaStreamSynchronize(ctx->stream));
     S.down(out, dout, n);
     if (S.err) return cuda_fail(ctx, S.err, "constraint_value: download");
     return TW_OK;
@@ -1512,9 +1512,9 @@ int tw_stage_fill_diag(tw_ctx* ctx, int32_t nv, const double* inv_mass, int64_t 
     const double* dj = S.up(jac, 12 * (size_t)n);
     double* dd = S.out<double>(n);
     if (S.err) return cuda_fail(ctx, S.err, "fill_diag: upload");
-    launch_fill_diag(nullptr, dm, n, dn, dv, dj, dd);
+    launch_fill_diag(ctx->stream, dm, n, dn, dv, dj, dd);
     ++ctx->launches;
-    CK(cudaDeviceSynchronize());
+    CK(cudaStreamSynchronize(ctx->stream));
     S.down(diag, dd, n);
     if (S.err) return cuda_fail(ctx, S.err, "fill_diag: download");
     return TW_OK;

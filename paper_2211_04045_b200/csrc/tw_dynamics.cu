@@ -176,8 +176,7 @@ __global__ void k_rep_pairs(DynParams P) {
         const double bw[3] = {w.x, w.y, w.z};
         for (int k = 0; k < nb; ++k) vid[1 + k] = bid[k], sw[1 + k] = -(kb == KV ? 1.0 : bw[k]);
     }
-    const int slot = atomicAdd(P.rp_count, 1);
-    (void)slot;
+    atomicAdd(P.rp_count, 1);  // repulsive pairs (diagnostics)
     // records are indexed by pair index (sparse, only repulsive ones written);
     // the CSR keys carry the pair index so the gather runs in pair order
     for (int k = 0; k < 4; ++k) {
