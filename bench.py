@@ -235,6 +235,12 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # TW_BENCH_ONE_DEVICE=1 (testing the N > 1 host path on a one-GPU box):
+        # every rank on device 0, the process group on gloo. The ranks share no
+        # data and never wait on each other's kernels.
+        self.one_device = os.environ.get("TW_BENCH_ONE_DEVICE") == "1"
+        if self.one_device:
+            self.local = 0
         if device == "cuda":
             torch.cuda.set_device(self.local)
             # one explicit stream shared by torch (flush, copies, events) and the
@@ -246,7 +252,7 @@ class Dist:
             import torch.distributed as dist
 
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            if device == "cuda":
+            if device == "cuda" and not self.one_device:
                 dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             else:
                 dist.init_process_group("gloo")
@@ -264,7 +270,7 @@ class Dist:
         """Elementwise max over ranks of per-rank timings; identity at N = 1."""
         import torch
 
-        t = torch.tensor(vals, dtype=torch.float64, device=self.device)
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if self.one_device else self.device)
         if self.dist is not None:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return [float(v) for v in t.tolist()]
@@ -661,6 +667,8 @@ def batch_line(args, D, res, nscenes):
                        "l2": "L2 flushed between timed steps", "parallelism": "scenes partitioned over ranks, "
                                                                                "no collective"},
             "frame": {"resolve_alg1_steps_per_frame": round(res["resolve_steps_per_frame"], 2)},
+            "n1_point": "the same workload at N = 1: `bench.py --workload batch`, or the batch_configs4_one_gpu "
+                        "key of the default N = 1 line (whose headline value is the bow-knot frame)",
             "gpu_launches": res["gpu_launches"], "clocks": res["clocks"]}
 
 
