@@ -484,7 +484,8 @@ def knot_scene(n_along: int = 935, n_across: int = 20, spacing: float = 3e-3, p:
 
 def ply_knot(n_along: int = 935, n_across: int = 20, spacing: float = 3e-3, p: int = 2, q: int = 3,
              tube: float = 0.03, gap: float = 2.5e-3, squeeze: float = 2.0e-3, slide: float = 2.0e-3,
-             end_gap: float = 0.04, jitter_seed: int | None = None, name: str = "knot") -> Scene:
+             end_gap: float = 0.04, jitter_seed: int | None = None, name: str = "knot",
+             density: float = 0.1) -> Scene:
     """Two cloth strips ("plies") laid face to face along the same twisted band
     of a (p, q) torus knot — a two-ply ribbon tied into a knot. Ply A lies on
     the torus of tube radius ``tube + gap/2``, ply B on ``tube - gap/2``; the
@@ -531,7 +532,7 @@ def ply_knot(n_along: int = 935, n_across: int = 20, spacing: float = 3e-3, p: i
     Y = np.concatenate(Y_all)
     T = np.concatenate(T_all)
     E = finalize_edges(np.zeros((0, 2), np.int32), np.zeros((0, 2), np.int32), T)
-    inv = lumped_inv_mass_fast(P, T, np.zeros((0, 2), np.int64), 0.1, 0.0)
+    inv = lumped_inv_mass_fast(P, T, np.zeros((0, 2), np.int64), density, 0.0)
     del width
     return Scene(name, P, Y, T, E, np.zeros((0, 2), np.int32), inv, True, True)
 
@@ -559,17 +560,25 @@ def bow_knot(**kw) -> Scene:
 # steps in both coloring modes (the paper's bow knot: 5.4 on average, 17 at
 # most); at a 3 mm slide some frames need 40+ steps or stall.
 FRAME_DEFAULTS = dict(squeeze=0.1e-3, slide=1.5e-3)
+# Material of the frame: 0.5 kg/m^2 cloth with 10 N/m springs, at which the
+# block-Jacobi PCG reaches the reference's 1e-6 relative residual within its
+# 400-iteration cap (the default 0.1 kg/m^2 / 50 N/m stops at the cap), so the
+# Newton target is the actual implicit-Euler solution. ENERGY goes to the
+# EnergyModel of both implementations.
+FRAME_DENSITY = 0.5
+FRAME_ENERGY = dict(spring_stiffness=10.0)
 
 
 def knot_frame(n_along: int = 1870, dt: float = 0.01, **kw):
     """A simulation frame of the tightening knot for the dynamics step
     (dynamics.cpp:326-349): the plies at rest (x, 2.5 mm apart) moving with
     v0 = (y_tight - x) / dt, where y_tight is the ply_knot tightening target
-    (squeeze / slide in ``kw``, FRAME_DEFAULTS otherwise). One implicit-Euler
+    (squeeze / slide / density in ``kw``, FRAME_DEFAULTS / FRAME_DENSITY
+    otherwise; simulate with the EnergyModel overrides FRAME_ENERGY). One implicit-Euler
     step with the paper's knot time step dt = 1/100 then drives
     the plies into each other; resolve makes the frame intersection-free.
     Returns (scene, v0)."""
-    kw = {**FRAME_DEFAULTS, **kw}
+    kw = {**FRAME_DEFAULTS, "density": FRAME_DENSITY, **kw}
     kw.setdefault("name", "bow_knot_frame" if n_along == 1870 else "knot_frame")
     sc = ply_knot(n_along=n_along, **kw)
     v0 = (sc.y - sc.x) / dt

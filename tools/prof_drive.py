@@ -9,7 +9,7 @@ from paper_2211_04045_b200 import capi, scenes as S
 sc, v0 = S.knot_frame(n_along=1870)
 ctx = capi.Context(0)
 m = capi.Mesh.from_scene(ctx, sc)
-dyn = capi.Dynamics(ctx, m, sc.x)
+dyn = capi.Dynamics(ctx, m, sc.x, **S.FRAME_ENERGY)
 for i in range(3):
     x, v, st = capi.step(ctx, m, dyn, sc.x, v0, delta=5e-4)
 torch.cuda.synchronize()
