@@ -11,7 +11,7 @@ NVFLAGS   := $(ARCH) -O3 -std=c++17 -lineinfo -fmad=false -Xcompiler -fPIC -Iinc
              --expt-relaxed-constexpr -diag-suppress 550 $(NVEXTRA)
 LIB       := $(PKG)/libtwoway_b200.so
 CU_SRCS   := $(CSRC)/tw_kernels.cu $(CSRC)/tw_capi.cu $(CSRC)/tw_dynamics.cu
-CU_HDRS   := $(CSRC)/tw_ctx.h $(CSRC)/tw_math.cuh $(CSRC)/tw_engine.cuh $(CSRC)/tw_phases.cuh $(CSRC)/tw_internal.h include/tw_c.h
+CU_HDRS   := $(CSRC)/tw_ctx.h $(CSRC)/tw_math.cuh $(CSRC)/tw_engine.cuh $(CSRC)/tw_phases.cuh $(CSRC)/tw_barrier.cuh $(CSRC)/tw_internal.h include/tw_c.h
 PY_EXT    := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_config_var('EXT_SUFFIX'))" 2>/dev/null)
 PYMOD     := $(PKG)/_twoway$(PY_EXT)
 PY_INC    := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_paths()['include'])" 2>/dev/null)

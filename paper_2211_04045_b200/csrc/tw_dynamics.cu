@@ -39,6 +39,7 @@
 #include <vector>
 
 #include "tw_ctx.h"
+#include "tw_barrier.cuh"
 #include "tw_math.cuh"
 
 namespace tw {
@@ -352,13 +353,9 @@ __device__ __forceinline__ d3 precond(const DynParams& P, int v, d3 r) {
 __device__ __forceinline__ void dyn_sync(DynGlobals* g) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
-        __threadfence();
-        const unsigned old = atomicAdd(&g->bar, inc);
-        volatile unsigned* cnt = &g->bar;
-        while (((old ^ *cnt) & 0x80000000u) == 0u) {
+        const unsigned old = bar_arrive(&g->bar, blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u);
+        while (!bar_flipped(old, bar_poll(&g->bar))) {
         }
-        __threadfence();
     }
     __syncthreads();
 }

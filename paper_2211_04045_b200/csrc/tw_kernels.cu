@@ -338,9 +338,9 @@ __device__ bool prologue(const Params& P) {
         if (!grid_sync(g)) return;                                                \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                                \
             const unsigned long long now_ = global_ns();                          \
-            g->phase_ns[__LINE__ % kPhaseSites] += now_ - g->phase_t0;                    \
-            g->phase_cnt[__LINE__ % kPhaseSites] += 1;                                    \
-            g->phase_t0 = now_;                                                   \
+            atomicAdd(&g->phase_ns[__LINE__ % kPhaseSites], now_ - ph_t0);         \
+            atomicAdd(&g->phase_cnt[__LINE__ % kPhaseSites], 1u);                  \
+            ph_t0 = now_;                                                         \
         }                                                                         \
     } while (0)
 
@@ -350,9 +350,9 @@ __device__ bool prologue(const Params& P) {
         if (!sub_sync(g, (n))) return;                                            \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                                \
             const unsigned long long now_ = global_ns();                          \
-            g->phase_ns[__LINE__ % kPhaseSites] += now_ - g->phase_t0;            \
-            g->phase_cnt[__LINE__ % kPhaseSites] += 1;                            \
-            g->phase_t0 = now_;                                                   \
+            atomicAdd(&g->phase_ns[__LINE__ % kPhaseSites], now_ - ph_t0);         \
+            atomicAdd(&g->phase_cnt[__LINE__ % kPhaseSites], 1u);                  \
+            ph_t0 = now_;                                                         \
         }                                                                         \
     } while (0)
 
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
     int dbg_step = 0;
     if (g->nonfinite || g->error) return;  // non-finite input detected by k_unpack
     if (!prologue(P)) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) g->phase_t0 = global_ns();
+    unsigned long long ph_t0 = (blockIdx.x == 0 && threadIdx.x == 0) ? global_ns() : 0ull;
     const Config& C = P.cfg;
     double bound = 0.0;  // forces a search on step 0
     int searches = 0;
@@ -462,25 +462,31 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
             // sub-grid barrier; the rest of the grid waits at the join
             const int nsub = P.pgs_ctas;
             if ((int)blockIdx.x < nsub) {
+                const PgsRanges R = pgs_ranges(P, ncol, ncol_c, ncol_e, nc);
+                const long long tail_rows = P.pgs_tail_rows;
+                PgsRow pre;
+                pre.color = -1;
                 for (int sw = 0; sw < C.sweeps; ++sw) {
-                    for (int c = 0; c < ncol;) {
-                        long long c0, nci, e0, nrow;
-                        pgs_color_range(P, c, ncol_c, ncol_e, &c0, &nci, &e0, &nrow);
-                        if (nrow == 0) {  // an unused color: no phase, no barrier
-                            ++c;
-                            continue;
-                        }
-                        if (nrow <= P.pgs_tail_rows) {
+                    int c = 0;
+                    while (c < ncol && R.rows(P, c) == 0) ++c;  // unused colors: no phase, no barrier
+                    if (c < ncol && R.rows(P, c) > tail_rows) pgs_prefetch(P, R, c, nsub, pre);
+                    while (c < ncol) {
+                        const long long nrow = R.rows(P, c);
+                        int next;
+                        if (nrow <= tail_rows) {
                             // a run of small colors: CTA 0 alone, CTA barriers between them
-                            const int cend = small_color_run(P, c, ncol, ncol_c, ncol_e, P.pgs_tail_rows);
-                            ph_pgs_tail(P, c, cend, ncol_c, ncol_e);
-                            SUBSYNC(nsub);
-                            c = cend;
-                            continue;
+                            next = c;
+                            while (next < ncol && R.rows(P, next) <= tail_rows) ++next;
+                            ph_pgs_tail_r(P, R, c, next);
+                        } else {
+                            ph_pgs_color_pre(P, R, c, nsub, pre);
+                            next = c + 1;
                         }
-                        ph_pgs_color(P, c, ncol_c, ncol_e, nsub);
+                        while (next < ncol && R.rows(P, next) == 0) ++next;
+                        // the next large color's static row data, in flight across the barrier
+                        if (next < ncol && R.rows(P, next) > tail_rows) pgs_prefetch(P, R, next, nsub, pre);
                         SUBSYNC(nsub);
-                        ++c;
+                        c = next;
                     }
                 }
             }

@@ -4,6 +4,7 @@
 // grid_sync(). Reference citations are into /root/reference/proj.
 #pragma once
 
+#include "tw_barrier.cuh"
 #include "tw_engine.cuh"
 
 namespace tw {
@@ -15,35 +16,30 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-// Grid barrier over all CTAs of a cooperative launch, one atomic per CTA:
-// CTA 0 adds 2^31 - (nblocks - 1), every other CTA adds 1, so the arrival
-// that completes the count flips bit 31 and the waiters watch for the flip
-// (no separate release store: ~1.6 us per barrier at 592 CTAs on B200 against
-// 3.3 us for arrive + generation bump, tools/bar_bench.cu). A waiter also
-// leaves when the error word is set — CTAs that bail out on an error may
-// never arrive — and a 20 s watchdog turns any other hang into ERR_TIMEOUT.
-__device__ __forceinline__ bool grid_sync(Globals* g) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
-        __threadfence();
-        const unsigned old = atomicAdd(&g->bar_count, inc);
-        volatile unsigned* cnt = &g->bar_count;
-        volatile int* err = &g->error;
-        unsigned long long t0 = 0;
-        for (unsigned it = 0; ((old ^ *cnt) & 0x80000000u) == 0u; ++it) {
-            if ((it & 63u) == 63u) {
-                if (*err) break;
-                const unsigned long long t = global_ns();
-                if (t0 == 0) t0 = t;
-                else if (t - t0 > (g->watchdog_ns ? g->watchdog_ns : 20000000000ull)) {
-                    atomicOr(&g->error, ERR_TIMEOUT);
-                    break;
-                }
+// Grid barrier over all CTAs of a cooperative launch (flip-bit, one release
+// atomic per CTA: tw_barrier.cuh). A waiter also leaves when the error word is
+// set -- CTAs that bail out on an error may never arrive -- and a watchdog
+// (20 s, or Globals::watchdog_ns) turns any other hang into ERR_TIMEOUT.
+__device__ __forceinline__ void flip_wait(Globals* g, unsigned* w, unsigned inc) {
+    const unsigned old = bar_arrive(w, inc);
+    volatile int* err = &g->error;
+    unsigned long long t0 = 0;
+    for (unsigned it = 0; !bar_flipped(old, bar_poll(w)); ++it) {
+        if ((it & 63u) == 63u) {
+            if (*err) break;
+            const unsigned long long t = global_ns();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > (g->watchdog_ns ? g->watchdog_ns : 20000000000ull)) {
+                atomicOr(&g->error, ERR_TIMEOUT);
+                break;
             }
         }
-        __threadfence();
     }
+}
+
+__device__ __forceinline__ bool grid_sync(Globals* g) {
+    __syncthreads();
+    if (threadIdx.x == 0) flip_wait(g, &g->bar_count, blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u);
     __syncthreads();
     return *((volatile int*)&g->error) == 0;
 }
@@ -52,26 +48,7 @@ __device__ __forceinline__ bool grid_sync(Globals* g) {
 // its own counter); the other CTAs wait at the next grid barrier.
 __device__ __forceinline__ bool sub_sync(Globals* g, unsigned n) {
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (n - 1u) : 1u;
-        __threadfence();
-        const unsigned old = atomicAdd(&g->sub_count, inc);
-        volatile unsigned* cnt = &g->sub_count;
-        volatile int* err = &g->error;
-        unsigned long long t0 = 0;
-        for (unsigned it = 0; ((old ^ *cnt) & 0x80000000u) == 0u; ++it) {
-            if ((it & 63u) == 63u) {
-                if (*err) break;
-                const unsigned long long t = global_ns();
-                if (t0 == 0) t0 = t;
-                else if (t - t0 > (g->watchdog_ns ? g->watchdog_ns : 20000000000ull)) {
-                    atomicOr(&g->error, ERR_TIMEOUT);
-                    break;
-                }
-            }
-        }
-        __threadfence();
-    }
+    if (threadIdx.x == 0) flip_wait(g, &g->sub_count, blockIdx.x == 0 ? 0x80000000u - (n - 1u) : 1u);
     __syncthreads();
     return *((volatile int*)&g->error) == 0;
 }
@@ -1024,12 +1001,66 @@ __device__ __forceinline__ void warm_edges(const Params& P, int v, double im, d3
     }
 }
 
-// Short vertex segments (<= 32 entries) are handled by one thread per
-// vertex; long ones by one warp per vertex (rank-by-counting sort in shared
-// memory up to WARM_WARP_MAX entries, lane 0 beyond; lanes form the terms,
-// lane 0 adds them in row order). Both loops stride over the vertices, so
-// the busy contact region spreads over the whole grid.
-constexpr int WARM_SHORT = 32, WARM_WARP_MAX = 256;
+// The vertices v = gwarp() + j * gwarps() (j = 0, 1, ...) for which take(v)
+// holds, visited one at a time by the whole warp; the predicate is evaluated
+// for 32 vertices at once (one load round instead of 32 dependent ones).
+template <typename T, typename F>
+__device__ __forceinline__ void for_warp_vertices(long long nv, T&& take, F&& f) {
+    const int lane = threadIdx.x & 31;
+    const long long w0 = gwarp(), G = gwarps();
+    for (long long j0 = 0; w0 + j0 * G < nv; j0 += 32) {
+        const long long v = w0 + (j0 + lane) * G;
+        unsigned m = __ballot_sync(0xffffffffu, v < nv && take((int)v));
+        while (m) {
+            const int q = __ffs(m) - 1;
+            m &= m - 1;
+            f((int)(w0 + (j0 + q) * G));
+        }
+    }
+}
+
+// a += the lanes' terms t (where nz) in lane order, in every lane
+__device__ __forceinline__ void warp_ordered_add(d3& a, const d3& t, bool nz) {
+    const unsigned nzm = __ballot_sync(0xffffffffu, nz);
+    for (int q = 0; q < 32; ++q) {
+        if (!((nzm >> q) & 1u)) continue;
+        const double tx = __shfl_sync(0xffffffffu, t.x, q);
+        const double ty = __shfl_sync(0xffffffffu, t.y, q);
+        const double tz = __shfl_sync(0xffffffffu, t.z, q);
+        a.x = a.x + tx, a.y = a.y + ty, a.z = a.z + tz;
+    }
+}
+
+// warm_edges with the terms formed by the lanes (same order and arithmetic)
+__device__ __forceinline__ void warm_edges_warp(const Params& P, int v, double im, d3& a) {
+    if (!P.cfg.edge_constraints) return;
+    const int lane = threadIdx.x & 31;
+    const int b = P.vedge_off[v], e1 = P.vedge_off[v + 1];
+    for (int k0 = b; k0 < e1; k0 += 32) {
+        const int k = k0 + lane;
+        bool nz = false;
+        d3 t = mk(0, 0, 0);
+        if (k < e1) {
+            const int e = P.vedge[k];
+            if (P.is_er[e]) {
+                const double lam = P.edge_lambda[e];
+                if (lam != 0.0) {
+                    const double sc = im * lam;
+                    const d3 j = edge_jac(P.er_g[e], P.edges[e].x == v ? 0 : 1);
+                    t = mk(sc * j.x, sc * j.y, sc * j.z);
+                    nz = true;
+                }
+            }
+        }
+        warp_ordered_add(a, t, nz);
+    }
+}
+
+// Vertices with contact entries are handled by one warp each (rank-by-counting
+// sort of the segment in shared memory up to WARM_WARP_MAX entries, lane 0
+// beyond; lanes form the terms, which are added in row order, then the edge
+// terms in edge order); the others -- most vertices -- by one thread each.
+constexpr int WARM_WARP_MAX = 256;
 
 __device__ void ph_warm(const Params& P, long long nc, bool reset_colors = true) {
     static_assert(sizeof(int) * (TPB / 32) * WARM_WARP_MAX <= SCRATCH_BYTES, "");
@@ -1037,22 +1068,9 @@ __device__ void ph_warm(const Params& P, long long nc, bool reset_colors = true)
     for (long long vl = gtid(); vl < P.nv; vl += gstride()) {
         const int v = (int)vl;
         const double im = P.inv_mass[v];
-        const int b = P.voff[v], n = P.voff[v + 1] - b;
-        if (!(im > 0.0) || n <= WARM_SHORT) {
+        if (!(im > 0.0) || P.voff[v + 1] == P.voff[v]) {
             d3 a = mk(0, 0, 0);
-            if (im > 0.0) {
-                sort_segment(P.vinc + b, n);
-                for (int k = 0; k < n; ++k) P.erank[P.vinc[b + k]] = k;  // rank inside the vertex clique
-                for_sorted_entries(P, v, [&](int e) {
-                    const int row = e >> 2, m = e & 3;
-                    const double lam = P.c_lambda[row];
-                    if (lam != 0.0) {
-                        const double* J = P.c_jac + (long long)row * 12 + 3 * m;
-                        imp_add(a, im * lam, mk(J[0], J[1], J[2]));
-                    }
-                });
-                warm_edges(P, v, im, a);
-            }
+            if (im > 0.0) warm_edges(P, v, im, a);
             P.imp[v] = make_double4(a.x, a.y, a.z, im);  // w: inv_mass, read with the impulse by the PGS
         }
         if (P.cfg.coloring_mode == 1) {
@@ -1070,10 +1088,9 @@ __device__ void ph_warm(const Params& P, long long nc, bool reset_colors = true)
         }
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (long long vl = gwarp(); vl < P.nv; vl += gwarps()) {
-        const int v = (int)vl;
+    // (static vertices have no entries)
+    for_warp_vertices(P.nv, [&](int v) { return P.voff[v + 1] > P.voff[v]; }, [&](int v) {
         const int b = P.voff[v], n = P.voff[v + 1] - b;
-        if (n <= WARM_SHORT) continue;  // (static vertices have no entries)
         const double im = P.inv_mass[v];
         int* seg = P.vinc + b;
         if (n <= WARM_WARP_MAX) {
@@ -1097,7 +1114,7 @@ __device__ void ph_warm(const Params& P, long long nc, bool reset_colors = true)
                 if (rk[r] >= 0) {
                     sseg[w][rk[r]] = ev[r];
                     seg[rk[r]] = ev[r];
-                    P.erank[ev[r]] = rk[r];
+                    P.erank[ev[r]] = rk[r];  // rank inside the vertex clique
                 }
             __syncwarp();
         } else {
@@ -1124,21 +1141,12 @@ __device__ void ph_warm(const Params& P, long long nc, bool reset_colors = true)
                     nz = true;
                 }
             }
-            const unsigned nzm = __ballot_sync(0xffffffffu, nz);
-            for (int q = 0; q < 32; ++q) {
-                if (!((nzm >> q) & 1u)) continue;
-                const double tx = __shfl_sync(0xffffffffu, t.x, q);
-                const double ty = __shfl_sync(0xffffffffu, t.y, q);
-                const double tz = __shfl_sync(0xffffffffu, t.z, q);
-                a.x = a.x + tx, a.y = a.y + ty, a.z = a.z + tz;
-            }
+            warp_ordered_add(a, t, nz);
         }
-        if (lane == 0) {
-            warm_edges(P, v, im, a);
-            P.imp[v] = make_double4(a.x, a.y, a.z, im);
-        }
+        warm_edges_warp(P, v, im, a);
+        if (lane == 0) P.imp[v] = make_double4(a.x, a.y, a.z, im);
         __syncwarp();
-    }
+    });
     if (reset_colors)  // coloring state of the contact rows (colors given: keep them)
         for (long long i = gtid(); i < nc; i += gstride()) {
             P.c_stamp[i] = 0;
@@ -1166,8 +1174,8 @@ __device__ void ph_warm(const Params& P, long long nc, bool reset_colors = true)
 
 __device__ void ph_color_rank(const Params& P) {
     const int lane = threadIdx.x & 31;
-    for (long long v = gwarp(); v < P.nv; v += gwarps()) {
-        if (P.vcnt[v] == 0) continue;  // no uncolored entry left at v
+    // vertices with no uncolored entry left are skipped
+    for_warp_vertices(P.nv, [&](int v) { return P.vcnt[v] != 0; }, [&](int v) {
         const int b = P.voff[v], e = P.voff[v + 1];
         int run = 0;
         for (int t0 = b; t0 < e; t0 += 32) {
@@ -1182,14 +1190,14 @@ __device__ void ph_color_rank(const Params& P) {
             if (unc) P.erank[ent] = run + __popc(bal & ((1u << lane) - 1u));
             run += __popc(bal);
         }
-    }
+    });
 }
 
 __device__ void ph_color_conflict(const Params& P, int k) {
     __shared__ unsigned long long seen[TPB / 32][4];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (long long v = gwarp(); v < P.nv; v += gwarps()) {
-        if (P.vcnt[v] == 0) continue;  // no uncolored entry left at v (also: empty segment)
+    // vertices with no uncolored entry left (also: empty segments) are skipped
+    for_warp_vertices(P.nv, [&](int v) { return P.vcnt[v] != 0; }, [&](int v) {
         const int b = P.voff[v], e = P.voff[v + 1];
         if (lane < 4) seen[w][lane] = 0ull;
         __syncwarp();
@@ -1221,7 +1229,7 @@ __device__ void ph_color_conflict(const Params& P, int k) {
             if (unc && tc < 256) atomicOr(&seen[w][tc >> 6], 1ull << (tc & 63));
             __syncwarp();
         }
-    }
+    });
 }
 
 __device__ void ph_color_commit(const Params& P, long long nc, int k) {
@@ -1750,9 +1758,24 @@ __device__ __forceinline__ void pgs_contact_row(const Params& P, int i) {
 // The same row from its color-ordered copy (position pos of c_by_color):
 // static row data is one coalesced read, each dynamic vertex's impulse (with
 // its inverse mass in w) is gathered once and written back once.
-__device__ __forceinline__ void pgs_contact_packed(const Params& P, long long pos) {
-    const int4 id = P.pk_ids[pos];
+// The row's static data (ids, q, diag, multiplier) can be loaded ahead, before
+// the barrier that opens its color (PgsRow): after the barrier only the
+// impulse gathers and the Jacobian load remain on the color's latency chain.
+struct PgsRow {
+    int color;      // the color this prefetch belongs to (-1: none)
+    int edge;       // edge id for an edge row, -1 for a contact row
+    long long pos;  // contact: position in the color-ordered copy
+    int4 ids;       // contact: the row's vertices; edge: (v0, v1, -, -)
+    double q, lam, diag;
+    double3 u;      // edge: the unit direction of er_g
+};
+
+__device__ __forceinline__ void pgs_contact_pre(const Params& P, long long pos, int4 id, double q, double diag,
+                                                double lam0) {
     const int vv[4] = {id.x, id.y, id.z, id.w};
+    double4 a[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) a[m] = vv[m] >= 0 ? P.imp[vv[m]] : make_double4(0, 0, 0, 0);
     const double2* J2 = reinterpret_cast<const double2*>(P.pk_jac + pos * 12);
     double J[12];
 #pragma unroll
@@ -1760,16 +1783,12 @@ __device__ __forceinline__ void pgs_contact_packed(const Params& P, long long po
         const double2 t = J2[k];
         J[2 * k] = t.x, J[2 * k + 1] = t.y;
     }
-    double4 a[4];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) a[m] = vv[m] >= 0 ? P.imp[vv[m]] : make_double4(0, 0, 0, 0);
     double s = 0.0;
 #pragma unroll
     for (int m = 0; m < 4; ++m)
         if (a[m].w > 0.0) s += dot(mk(J[3 * m], J[3 * m + 1], J[3 * m + 2]), mk(a[m].x, a[m].y, a[m].z));
-    const double w = P.pk_q[pos] + s;
-    const double lam0 = P.pk_lam[pos];
-    const double t = lam0 - w / P.pk_diag[pos];
+    const double w = q + s;
+    const double t = lam0 - w / diag;
     const double lam = 0.0 < t ? t : 0.0;
     const double d = lam - lam0;
     if (d != 0.0) {
@@ -1787,40 +1806,45 @@ __device__ __forceinline__ void pgs_contact_packed(const Params& P, long long po
     P.c_lambda[P.c_by_color[pos]] = lam;
 }
 
-__device__ __forceinline__ void pgs_edge_row(const Params& P, int e) {
-    const int2 ed = P.edges[e];
-    const double4 g4 = P.er_g[e];
-    const d3 j0 = edge_jac(g4, 0), j1 = edge_jac(g4, 1);
+// The same row from its color-ordered copy (position pos of c_by_color):
+// static row data is one coalesced read, each dynamic vertex's impulse (with
+// its inverse mass in w) is gathered once and written back once.
+__device__ __forceinline__ void pgs_contact_packed(const Params& P, long long pos) {
+    pgs_contact_pre(P, pos, P.pk_ids[pos], P.pk_q[pos], P.pk_diag[pos], P.pk_lam[pos]);
+}
+
+__device__ __forceinline__ void pgs_edge_pre(const Params& P, int e, int2 ed, double3 u, double diag, double q,
+                                             double lam0) {
+    const d3 j0 = edge_jac(make_double4(u.x, u.y, u.z, diag), 0), j1 = edge_jac(make_double4(u.x, u.y, u.z, diag), 1);
     const double im0 = P.inv_mass[ed.x], im1 = P.inv_mass[ed.y];
+    double4 a0 = make_double4(0, 0, 0, 0), a1 = make_double4(0, 0, 0, 0);
+    if (im0 > 0.0) a0 = P.imp[ed.x];
+    if (im1 > 0.0) a1 = P.imp[ed.y];
     double s = 0.0;
-    if (im0 > 0.0) {
-        const double4 a = P.imp[ed.x];
-        s += dot(j0, mk(a.x, a.y, a.z));
-    }
-    if (im1 > 0.0) {
-        const double4 a = P.imp[ed.y];
-        s += dot(j1, mk(a.x, a.y, a.z));
-    }
-    const double w = P.er_q[e] + s;
-    const double lam0 = P.edge_lambda[e];
-    const double t = lam0 - w / g4.w;
+    if (im0 > 0.0) s += dot(j0, mk(a0.x, a0.y, a0.z));
+    if (im1 > 0.0) s += dot(j1, mk(a1.x, a1.y, a1.z));
+    const double w = q + s;
+    const double t = lam0 - w / diag;
     const double lam = 0.0 < t ? t : 0.0;
     const double d = lam - lam0;
     if (d != 0.0) {
         if (im0 > 0.0) {
-            double4 a = P.imp[ed.x];
             const double sc = im0 * d;
-            a.x = a.x + sc * j0.x, a.y = a.y + sc * j0.y, a.z = a.z + sc * j0.z;
-            P.imp[ed.x] = a;
+            a0.x = a0.x + sc * j0.x, a0.y = a0.y + sc * j0.y, a0.z = a0.z + sc * j0.z;
+            P.imp[ed.x] = a0;
         }
         if (im1 > 0.0) {
-            double4 a = P.imp[ed.y];
             const double sc = im1 * d;
-            a.x = a.x + sc * j1.x, a.y = a.y + sc * j1.y, a.z = a.z + sc * j1.z;
-            P.imp[ed.y] = a;
+            a1.x = a1.x + sc * j1.x, a1.y = a1.y + sc * j1.y, a1.z = a1.z + sc * j1.z;
+            P.imp[ed.y] = a1;
         }
     }
     P.edge_lambda[e] = lam;
+}
+
+__device__ __forceinline__ void pgs_edge_row(const Params& P, int e) {
+    const double4 g4 = P.er_g[e];
+    pgs_edge_pre(P, e, P.edges[e], make_double3(g4.x, g4.y, g4.z), g4.w, P.er_q[e], P.edge_lambda[e]);
 }
 
 // rows of color c: contact rows first, then edge rows (any order inside a
@@ -1833,6 +1857,109 @@ __device__ __forceinline__ void pgs_color_range(const Params& P, int c, int ncol
     *e0 = 0;
     if (P.cfg.edge_constraints && c < ncol_edge) *e0 = P.er_color_off[c], e1 = P.er_color_off[c + 1];
     *n = *nci + (e1 - *e0);
+}
+
+// The color ranges of one sweep, tabled in the CTA's scratch (shared) memory
+// when they fit: the sweep's control flow then reads no global memory.
+struct PgsRanges {
+    const int4* tab;  // (c0, nci, e0, ne) per color, or nullptr
+    int ncol_contact, ncol_edge;
+    __device__ __forceinline__ void get(const Params& P, int c, long long* c0, long long* nci, long long* e0,
+                                        long long* n) const {
+        if (tab) {
+            const int4 r = tab[c];
+            *c0 = r.x, *nci = r.y, *e0 = r.z, *n = (long long)r.y + r.w;
+        } else {
+            pgs_color_range(P, c, ncol_contact, ncol_edge, c0, nci, e0, n);
+        }
+    }
+    __device__ __forceinline__ long long rows(const Params& P, int c) const {
+        long long c0, nci, e0, n;
+        get(P, c, &c0, &nci, &e0, &n);
+        return n;
+    }
+};
+
+__device__ __forceinline__ PgsRanges pgs_ranges(const Params& P, int ncol, int ncol_contact, int ncol_edge,
+                                                long long nc) {
+    PgsRanges R{nullptr, ncol_contact, ncol_edge};
+    if (ncol <= (int)(SCRATCH_BYTES / sizeof(int4)) && nc < 0x7fffffffLL) {
+        int4* tab = reinterpret_cast<int4*>(smem_scratch());
+        for (int c = threadIdx.x; c < ncol; c += TPB) {
+            long long c0, nci, e0, n;
+            pgs_color_range(P, c, ncol_contact, ncol_edge, &c0, &nci, &e0, &n);
+            tab[c] = make_int4((int)c0, (int)nci, (int)e0, (int)(n - nci));
+        }
+        __syncthreads();
+        R.tab = tab;
+    }
+    return R;
+}
+
+// the static data of this thread's first row of color c (rows dealt as in
+// ph_pgs_color), loaded ahead of the barrier that opens the color
+__device__ __forceinline__ void pgs_prefetch(const Params& P, const PgsRanges& R, int c, int nctas, PgsRow& r) {
+    r.color = c;
+    r.edge = -2;  // no row
+    long long c0, nci, e0, n;
+    R.get(P, c, &c0, &nci, &e0, &n);
+    const long long k = blockIdx.x + (long long)threadIdx.x * nctas;
+    if (k >= n) return;
+    if (k < nci) {
+        r.edge = -1;
+        r.pos = c0 + k;
+        r.ids = P.pk_ids[r.pos];
+        r.q = P.pk_q[r.pos];
+        r.diag = P.pk_diag[r.pos];
+        r.lam = P.pk_lam[r.pos];
+    } else {
+        const int e = P.er_by_color[e0 + (k - nci)];
+        r.edge = e;
+        const int2 ed = P.edges[e];
+        r.ids = make_int4(ed.x, ed.y, -1, -1);
+        const double4 g4 = P.er_g[e];
+        r.u = make_double3(g4.x, g4.y, g4.z);
+        r.diag = g4.w;
+        r.q = P.er_q[e];
+        r.lam = P.edge_lambda[e];
+    }
+}
+
+// one large color on the first nctas CTAs, its first row per thread prefetched
+__device__ __forceinline__ void ph_pgs_color_pre(const Params& P, const PgsRanges& R, int c, int nctas,
+                                                 const PgsRow& r) {
+    long long c0, nci, e0, n;
+    R.get(P, c, &c0, &nci, &e0, &n);
+    const long long stride = (long long)nctas * TPB;
+    long long k = blockIdx.x + (long long)threadIdx.x * nctas;
+    if (k < n) {
+        if (r.color == c && r.edge != -2) {
+            if (r.edge == -1) pgs_contact_pre(P, r.pos, r.ids, r.q, r.diag, r.lam);
+            else pgs_edge_pre(P, r.edge, make_int2(r.ids.x, r.ids.y), r.u, r.diag, r.q, r.lam);
+        } else if (k < nci) {
+            pgs_contact_packed(P, c0 + k);
+        } else {
+            pgs_edge_row(P, P.er_by_color[e0 + (k - nci)]);
+        }
+    }
+    for (k += stride; k < n; k += stride) {
+        if (k < nci) pgs_contact_packed(P, c0 + k);
+        else pgs_edge_row(P, P.er_by_color[e0 + (k - nci)]);
+    }
+}
+
+// ph_pgs_tail over tabled ranges
+__device__ void ph_pgs_tail_r(const Params& P, const PgsRanges& R, int cfirst, int cend) {
+    if (blockIdx.x != 0) return;
+    for (int c = cfirst; c < cend; ++c) {
+        long long c0, nci, e0, n;
+        R.get(P, c, &c0, &nci, &e0, &n);
+        for (long long k = threadIdx.x; k < n; k += TPB) {
+            if (k < nci) pgs_contact_packed(P, c0 + k);
+            else pgs_edge_row(P, P.er_by_color[e0 + (k - nci)]);
+        }
+        __syncthreads();
+    }
 }
 
 __device__ void ph_pgs_color(const Params& P, int c, int ncol_contact, int ncol_edge, int nctas) {

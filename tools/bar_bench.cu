@@ -109,14 +109,58 @@ __device__ __forceinline__ void flipbar(Bar* b) {
     else __syncthreads();
 }
 
+__device__ __forceinline__ void red_release(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+// V7: monotonic counter, posted (red.release) arrival, ld.acquire poll
+// V8: the same with a relaxed poll and one fence.acq_rel after it
+// V9: flip-bit with atom.add.release and an ld.acquire poll (no fences)
+template <int V>
+__device__ __forceinline__ void cntbar(Bar* b, unsigned& target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (V == 9) {
+            const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+            const unsigned old = atom_add_release(&b->count, inc);
+            while (((old ^ ld_acquire(&b->count)) & 0x80000000u) == 0u) {
+            }
+        } else {
+            target += gridDim.x;
+            red_release(&b->count, 1u);
+            if (V == 7) {
+                while ((int)(ld_acquire(&b->count) - target) < 0) {
+                }
+            } else {
+                while ((int)(ld_relaxed(&b->count) - target) < 0) {
+                }
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            }
+        }
+    }
+    __syncthreads();
+}
+
 template <int V>
 __global__ void k(Bar* b, int n, unsigned long long* ns, float* sink) {
+    unsigned target = 0;
     float acc = threadIdx.x;
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (int i = 0; i < n; ++i) {
         acc = acc * 1.0001f + 1.f;
         if (V == 4) cg::this_grid().sync();
+        else if (V >= 7) cntbar<V>(b, target);
         else if (V >= 5) flipbar<V>(b);
         else bar<V>(b);
     }
@@ -169,7 +213,188 @@ void runc(int nblocks, int cl, Bar* b, unsigned long long* ns, float* sink) {
     cudaGetLastError();
 }
 
+// V9 on a barrier word at a chosen offset of a large buffer (L2 slice / die)
+__global__ void kaddr(unsigned* w, int n, unsigned long long* ns) {
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int i = 0; i < n; ++i) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+            const unsigned old = atom_add_release(w, inc);
+            while (((old ^ ld_acquire(w)) & 0x80000000u) == 0u) {
+            }
+        }
+        __syncthreads();
+    }
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ns = t1 - t0;
+}
+
+// V9 on the driver's cooperative-launch barrier word (CG: one cg grid sync first)
+template <int CG>
+__global__ void kws(int n, unsigned long long* ns, unsigned long long* addr) {
+    unsigned long long t0, t1;
+    if (CG == 1) cg::this_grid().sync();
+    unsigned* w = &cg::details::get_grid_workspace()->barrier;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int i = 0; i < n; ++i) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+            const unsigned old = atom_add_release(w, inc);
+            while (((old ^ ld_acquire(w)) & 0x80000000u) == 0u) {
+            }
+        }
+        __syncthreads();
+    }
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ns = t1 - t0, *addr = (unsigned long long)w;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gen(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned atom_add_release_gen(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+// generic-address flip-bit (G bit 1: generic atom, bit 2: generic poll)
+template <int G>
+__global__ void kgen(unsigned* w, int n, unsigned long long* ns) {
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int i = 0; i < n; ++i) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+            const unsigned old = (G & 1) ? atom_add_release_gen(w, inc) : atom_add_release(w, inc);
+            while (((old ^ ((G & 2) ? ld_acquire_gen(w) : ld_acquire(w))) & 0x80000000u) == 0u) {
+            }
+        }
+        __syncthreads();
+    }
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ns = t1 - t0;
+}
+// flip-bit variants: S = nanosleep ns between polls (0: none), W: wait for the
+// atomic's return before the first poll
+template <int S, int W>
+__global__ void kflip(unsigned* w, int n, unsigned long long* ns) {
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int i = 0; i < n; ++i) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+            unsigned old = atom_add_release(w, inc);
+            if (W) old = __shfl_sync(1u, old, 0);
+            while (((old ^ ld_acquire(w)) & 0x80000000u) == 0u) {
+                if (S) __nanosleep(S);
+            }
+        }
+        __syncthreads();
+    }
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ns = t1 - t0;
+}
+template <int S, int W>
+void runflip(int nb, unsigned* w, unsigned long long* ns) {
+    int n = 2000;
+    void* args[] = {&w, &n, &ns};
+    float best = 1e9;
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaMemset(w, 0, 4);
+        cudaLaunchCooperativeKernel((const void*)kflip<S, W>, dim3(nb), dim3(256), args, 0, 0);
+        cudaDeviceSynchronize();
+        unsigned long long h = 0;
+        cudaMemcpy(&h, ns, 8, cudaMemcpyDeviceToHost);
+        best = fminf(best, h / 1e3f / n);
+    }
+    printf("flip sleep %d wait %d blocks %d: %.3f us/barrier\n", S, W, nb, best);
+}
+
+template <int G>
+void rungen(int nb, unsigned* w, unsigned long long* ns) {
+    int n = 2000;
+    void* args[] = {&w, &n, &ns};
+    float best = 1e9;
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaMemset(w, 0, 4);
+        cudaLaunchCooperativeKernel((const void*)kgen<G>, dim3(nb), dim3(256), args, 0, 0);
+        cudaDeviceSynchronize();
+        unsigned long long h = 0;
+        cudaMemcpy(&h, ns, 8, cudaMemcpyDeviceToHost);
+        best = fminf(best, h / 1e3f / n);
+    }
+    printf("generic %d blocks %d: %.3f us/barrier\n", G, nb, best);
+}
+
 int main() {
+    {
+        unsigned* w;
+        unsigned long long* ns4;
+        cudaMalloc(&w, 4096);
+        cudaMalloc(&ns4, 8);
+        for (int nb : {148, 296, 592}) {
+            runflip<0, 0>(nb, w, ns4);
+            runflip<0, 1>(nb, w, ns4);
+            runflip<32, 0>(nb, w, ns4);
+            runflip<32, 1>(nb, w, ns4);
+            runflip<100, 1>(nb, w, ns4);
+            runflip<200, 1>(nb, w, ns4);
+            runflip<500, 1>(nb, w, ns4);
+        }
+        for (int nb : {296, 592}) {
+            rungen<0>(nb, w, ns4);
+            rungen<1>(nb, w, ns4);
+            rungen<2>(nb, w, ns4);
+            rungen<3>(nb, w, ns4);
+        }
+    }
+    {
+        unsigned long long *ns3, *ad;
+        cudaMalloc(&ns3, 8);
+        cudaMalloc(&ad, 8);
+        for (int nb : {296, 592}) {
+            int n = 2000;
+            void* args[] = {&n, &ns3, &ad};
+            for (int rep = 0; rep < 6; ++rep) {
+                cudaError_t e = cudaLaunchCooperativeKernel(rep & 1 ? (const void*)kws<1> : (const void*)kws<0>, dim3(nb), dim3(256), args, 0, 0);
+                e = cudaDeviceSynchronize();
+                unsigned long long h = 0, a = 0;
+                cudaMemcpy(&h, ns3, 8, cudaMemcpyDeviceToHost);
+                cudaMemcpy(&a, ad, 8, cudaMemcpyDeviceToHost);
+                printf("driver-word cg-first %d blocks %d: %s %.3f us/barrier\n", rep & 1, nb, cudaGetErrorString(e), h / 1e3 / n); (void)a;
+            }
+        }
+    }
+    {
+        unsigned* big;
+        unsigned long long* ns2;
+        cudaMalloc(&big, 64 << 20);
+        cudaMalloc(&ns2, 8);
+        for (int nb : {296, 592}) {
+            for (long long off : {0LL, 32LL, 128LL, 4096LL, 65536LL, 1LL << 20, 3LL << 20, 5LL << 20, 7LL << 20, 11LL << 20, 13LL << 20, 17LL << 20, 33LL << 20}) {
+                unsigned* w = big + off / 4;
+                int n = 2000;
+                void* args[] = {&w, &n, &ns2};
+                float best = 1e9;
+                for (int rep = 0; rep < 3; ++rep) {
+                    cudaMemset(w, 0, 4);
+                    cudaLaunchCooperativeKernel((const void*)kaddr, dim3(nb), dim3(256), args, 0, 0);
+                    cudaDeviceSynchronize();
+                    unsigned long long h = 0;
+                    cudaMemcpy(&h, ns2, 8, cudaMemcpyDeviceToHost);
+                    best = fminf(best, h / 1e3f / n);
+                }
+                printf("addr-offset %10lld blocks %d: %.3f us/barrier\n", off, nb, best);
+            }
+        }
+    }
     Bar* b;
     unsigned long long* ns;
     float* sink;
@@ -183,6 +408,9 @@ int main() {
         run<3>(nb, b, ns, sink);
         run<4>(nb, b, ns, sink);
         run<5>(nb, b, ns, sink);
+        run<7>(nb, b, ns, sink);
+        run<8>(nb, b, ns, sink);
+        run<9>(nb, b, ns, sink);
         for (int cl : {1, 2, 4, 8}) runc<5>(nb, cl, b, ns, sink);
         for (int cl : {2, 4, 8}) runc<6>(nb, cl, b, ns, sink);
     }
