@@ -296,6 +296,15 @@ __device__ __forceinline__ void unpack_weights(int ka, int kb, double4 w, double
 }
 
 // vertex ids of the pair's simplices from its stored ids (a first)
+// split_ids for a compile-time pair class (register arrays)
+template <int KA, int KB>
+__device__ __forceinline__ void split_ids_t(int4 id, int (&va)[3], int (&vb)[3]) {
+    const int v[4] = {id.x, id.y, id.z, id.w};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) va[i] = i <= KA ? v[i] : -1;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) vb[i] = i <= KB ? v[(KA + 1 + i) & 3] : -1;
+}
 __device__ __forceinline__ void split_ids(int ka, int kb, int4 id, int* va, int* vb) {
     const int v[4] = {id.x, id.y, id.z, id.w};
     int k = 0;

@@ -1042,6 +1042,7 @@ cudaError_t coop_refresh(cudaStream_t s, const Params& P, int nblocks, double bo
     // TW_REFRESH_MINB=2: the 128-register instance (register-budget experiment)
     static const int minb = std::getenv("TW_REFRESH_MINB") ? std::atoi(std::getenv("TW_REFRESH_MINB")) : 4;
     if (minb == 2) return coop((const void*)k_stage_refresh<2>, s, std::min(nblocks, resolve_blocks_per_sm(2) * 148), args);
+    if (minb == 3) return coop((const void*)k_stage_refresh<3>, s, std::min(nblocks, 3 * 148), args);
     return coop((const void*)k_stage_refresh<4>, s, nblocks, args);
 }
 cudaError_t coop_ccd(cudaStream_t s, const Params& P, int nblocks) {

@@ -238,6 +238,51 @@ __device__ __forceinline__ void flip(Closest& r) {
     r.dir = neg(r.dir);
 }
 
+// pair_closest for a compile-time pair class (the kinds a proximity key
+// holds: VV, VE, VT, EE). The vertex ids stay in registers (no runtime-indexed
+// arrays, so no local memory); same calls and arithmetic as pair_closest.
+template <int KA, int KB, typename LoadX>
+__device__ __forceinline__ int pair_closest_t(const int (&ia)[3], const int (&ib)[3], const LoadX& X, Closest& r) {
+#pragma unroll
+    for (int i = 0; i <= KA; ++i)
+#pragma unroll
+        for (int j = 0; j <= KB; ++j)
+            if (ia[i] == ib[j]) return -1;
+    if constexpr (KA == KV && KB == KV) {
+        closest_vv(X(ia[0]), X(ib[0]), r);
+        return 1;
+    } else if constexpr (KA == KV && KB == KE) {
+        closest_ve(X(ia[0]), X(ib[0]), X(ib[1]), r);
+        return 1;
+    } else if constexpr (KA == KV && KB == KT) {
+        return closest_vt(X(ia[0]), X(ib[0]), X(ib[1]), X(ib[2]), r) ? 1 : 0;
+    } else if constexpr (KA == KE && KB == KE) {
+        const bool swp = (ib[0] < ia[0]) || (ib[0] == ia[0] && ib[1] < ia[1]);
+        if (!closest_ee(X(swp ? ib[0] : ia[0]), X(swp ? ib[1] : ia[1]), X(swp ? ia[0] : ib[0]),
+                        X(swp ? ia[1] : ib[1]), r))
+            return 0;
+        if (swp) flip(r);
+        return 1;
+    } else {
+        return -1;
+    }
+}
+
+// Runs f(PairClass<KA, KB>{}) for the runtime class of a proximity key.
+template <int A, int B>
+struct PairClass {
+    static constexpr int ka = A, kb = B;
+};
+template <typename F>
+__device__ __forceinline__ bool with_pair_class(int ka, int kb, F&& f) {
+    if (ka == KV && kb == KT) f(PairClass<KV, KT>{});
+    else if (ka == KE && kb == KE) f(PairClass<KE, KE>{});
+    else if (ka == KV && kb == KE) f(PairClass<KV, KE>{});
+    else if (ka == KV && kb == KV) f(PairClass<KV, KV>{});
+    else return false;
+    return true;
+}
+
 // simplex_pair_closest (distance.cpp:218-253) for the canonical pair kinds the
 // proximity set holds (a = V or E, b = V/E/T) plus the flipped kinds.
 // ids: vertex ids of a (ia[0..2]) and b (ib[0..2]). Returns 1 value, 0

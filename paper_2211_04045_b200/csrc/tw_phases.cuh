@@ -303,6 +303,29 @@ __device__ __forceinline__ void simplex_ids(const Params& P, int k, int idx, int
 
 // The exact narrow-phase test of the reference search (proximity.cpp:162-167):
 // canonical candidate, non-adjacent, has a closest point, distance < d_max.
+template <int K>
+__device__ __forceinline__ void simplex_ids_t(const Params& P, int idx, int (&v)[3]) {
+    v[0] = v[1] = v[2] = -1;
+    if constexpr (K == KV) {
+        v[0] = idx;
+    } else if constexpr (K == KE) {
+        const int2 e = P.edges[idx];
+        v[0] = e.x, v[1] = e.y;
+    } else {
+        const int4 t = P.tris[idx];
+        v[0] = t.x, v[1] = t.y, v[2] = t.z;
+    }
+}
+template <int KA, int KB>
+__device__ __forceinline__ bool candidate_keep_t(const Params& P, int ia, int ib, Closest& c) {
+    if (KA == KE && ib <= ia) return false;              // EE: a is the lower edge index
+    if (KA == KV && KB == KV && ib <= ia) return false;  // VV: a < b
+    int va[3], vb[3];
+    simplex_ids_t<KA>(P, ia, va);
+    simplex_ids_t<KB>(P, ib, vb);
+    const int h = pair_closest_t<KA, KB>(va, vb, XLoad{P.x}, c);
+    return h == 1 && c.dist < P.cfg.d_max;
+}
 __device__ __forceinline__ bool candidate_keep(const Params& P, int ka, int ia, const int* va,
                                                int kb, int ib, Closest& c) {
     if (ka == KE && ib <= ia) return false;             // EE: a is the lower edge index
@@ -562,11 +585,17 @@ __device__ void ph_cand_eval(const Params& P) {
         const int2 e = P.cand[i];
         int ka, ia, kb, cls;
         query_of(P, e.x, &ka, &ia, &kb, &cls);
-        int va[3];
-        simplex_ids(P, ka, ia, va);
         Closest c;
         ++evals;
-        if (candidate_keep(P, ka, ia, va, kb, e.y, c)) {
+        bool keep = false;
+        if (!with_pair_class(ka, kb, [&](auto pc) {
+                keep = candidate_keep_t<decltype(pc)::ka, decltype(pc)::kb>(P, ia, e.y, c);
+            })) {
+            int va[3];
+            simplex_ids(P, ka, ia, va);
+            keep = candidate_keep(P, ka, ia, va, kb, e.y, c);
+        }
+        if (keep) {
             const int pos = atomicAdd(&P.qcount[e.x], 1);
             if (pos < P.K) {
                 P.qslot[(long long)e.x * P.K + pos] = e.y;
@@ -721,12 +750,54 @@ __device__ void ph_emit_pairs(const Params& P) {
 
 // A3b: the pair records, balanced over the output: CTA b writes pairs
 // [b P / nb, (b+1) P / nb), each decoded from its key.
+// one pair record for a compile-time pair class
+template <int KA, int KB>
+__device__ __forceinline__ bool emit_record_t(const Params& P, long long p, uint64_t key, int& touching,
+                                              bool first_search) {
+    int va[3], vb[3];
+    simplex_ids_t<KA>(P, key_ia(key), va);
+    simplex_ids_t<KB>(P, key_ib(key), vb);
+    Closest c;
+    pair_closest_t<KA, KB>(va, vb, XLoad{P.x}, c);
+    const int4 ids = KA == KE ? make_int4(va[0], va[1], vb[0], vb[1]) : make_int4(va[0], vb[0], vb[1], vb[2]);
+    bool all_static = true;
+#pragma unroll
+    for (int k = 0; k <= KA; ++k) all_static &= P.inv_mass[va[k]] == 0.0;
+#pragma unroll
+    for (int k = 0; k <= KB; ++k) all_static &= P.inv_mass[vb[k]] == 0.0;
+    uint8_t fl = PF_ACTIVE | (all_static ? PF_ALL_STATIC : 0) | (c.degenerate ? PF_DEGENERATE : 0);
+    const double4 dd = make_double4(c.dir.x, c.dir.y, c.dir.z, c.dist);
+    const double4 w = pack_weights(KA, KB, c);
+    if (!all_static && dd.w < P.cfg.delta) {  // contact_pred's own early exits, checked first
+        int a3[3] = {va[0], va[1], va[2]}, b3[3] = {vb[0], vb[1], vb[2]};
+        if (contact_pred(P, KA, KB, a3, b3, dd, w, fl)) fl |= PF_CONTACT;
+    }
+    P.pids[p] = ids;
+    P.pdd[p] = dd;
+    if (P.pw_all || (fl & PF_CONTACT)) P.pw[p] = w;  // weights are read for contact rows only
+    P.pflag[p] = fl;
+#pragma unroll
+    for (int k = 0; k <= KA; ++k) vertex_min(P, va[k], c.dist);
+#pragma unroll
+    for (int k = 0; k <= KB; ++k) vertex_min(P, vb[k], c.dist);
+    if (first_search && c.dist < 1e-10) touching = 1;
+    return (fl & PF_CONTACT) != 0;
+}
+
+// A3b: the pair records, balanced over the output: CTA b writes pairs
+// [b P / nb, (b+1) P / nb), each decoded from its key.
 __device__ void ph_emit_records(const Params& P, bool first_search) {
     const long long np = P.g->np;
     int touching = 0;
     for_pair_tiles(P, np, [&](long long p) -> bool {
         const uint64_t key = P.pkey[p];
-        const int ka = key_ka(key), kb = key_kb(key), ia = key_ia(key), ib = key_ib(key);
+        const int ka = key_ka(key), kb = key_kb(key);
+        bool contact = false;
+        if (with_pair_class(ka, kb, [&](auto pc) {
+                contact = emit_record_t<decltype(pc)::ka, decltype(pc)::kb>(P, p, key, touching, first_search);
+            }))
+            return contact;
+        const int ia = key_ia(key), ib = key_ib(key);
         int va[3], vb[3];
         simplex_ids(P, ka, ia, va);
         simplex_ids(P, kb, ib, vb);
@@ -742,7 +813,7 @@ __device__ void ph_emit_records(const Params& P, bool first_search) {
         if (contact_pred(P, ka, kb, va, vb, dd, w, fl)) fl |= PF_CONTACT;
         P.pids[p] = ids;
         P.pdd[p] = dd;
-        if (P.pw_all || (fl & PF_CONTACT)) P.pw[p] = w;  // weights are read for contact rows only
+        if (P.pw_all || (fl & PF_CONTACT)) P.pw[p] = w;
         P.pflag[p] = fl;
         for (int k = 0; k <= ka; ++k) vertex_min(P, va[k], c.dist);
         for (int k = 0; k <= kb; ++k) vertex_min(P, vb[k], c.dist);
@@ -2195,6 +2266,68 @@ __device__ void ph_arch_merge(const Params& P, long long nnew, int sel, long lon
 }
 
 // ============================================================ refresh (H)
+// one pair of ph_refresh for a compile-time pair class (KA < 0: runtime class)
+template <int KA, int KB>
+__device__ __forceinline__ bool refresh_pair(const Params& P, long long p, uint64_t key, uint8_t old_fl, double bound,
+                                             bool next_search, long long& nact) {
+    const int ka = KA >= 0 ? KA : key_ka(key), kb = KA >= 0 ? KB : key_kb(key);
+    int va[3], vb[3];
+    Closest c;
+    int h;
+    if constexpr (KA >= 0) {
+        split_ids_t<KA, KB>(P.pids[p], va, vb);
+        h = pair_closest_t<KA, KB>(va, vb, XLoad{P.x}, c);
+    } else {
+        split_ids(ka, kb, P.pids[p], va, vb);
+        h = pair_closest(ka, va, kb, vb, XLoad{P.x}, c);
+    }
+    uint8_t fl = old_fl & PF_ALL_STATIC;
+    double4 dd;
+    double4 w;
+    if (h != 1) {
+        dd = P.pdd[p];
+        w = P.pw[p];
+        fl |= old_fl & PF_DEGENERATE;
+    } else {
+        d3 dir = c.dir;
+        if (c.degenerate) {
+            const double4 old = P.pdd[p];
+            const d3 od = mk(old.x, old.y, old.z);
+            if (!is_zero(od)) dir = od;
+        }
+        dd = make_double4(dir.x, dir.y, dir.z, c.dist);
+        w = pack_weights(ka, kb, c);
+        P.pdd[p] = dd;
+        if (c.degenerate) fl |= PF_DEGENERATE;
+        if (c.dist < bound) fl |= PF_ACTIVE;
+        else if (c.dist >= bound + kFarMargin) fl |= PF_FAR;
+    }
+    if (fl & PF_ACTIVE) {
+        ++nact;
+        if (!next_search) {
+            if constexpr (KA >= 0) {
+#pragma unroll
+                for (int k = 0; k <= KA; ++k) vertex_min(P, va[k], dd.w);
+#pragma unroll
+                for (int k = 0; k <= KB; ++k) vertex_min(P, vb[k], dd.w);
+            } else {
+                for (int k = 0; k <= ka; ++k) vertex_min(P, va[k], dd.w);
+                for (int k = 0; k <= kb; ++k) vertex_min(P, vb[k], dd.w);
+            }
+        }
+    }
+    // contact_pred's own early exits (active, not all static, inside delta) checked first
+    if (!next_search && (fl & PF_ACTIVE) && !(fl & PF_ALL_STATIC) && dd.w < P.cfg.delta) {
+        int a3[3] = {va[0], va[1], va[2]}, b3[3] = {vb[0], vb[1], vb[2]};
+        if (contact_pred(P, ka, kb, a3, b3, dd, w, fl)) fl |= PF_CONTACT;
+    }
+    // weights are read for contact rows only (ph_rows_build); the stage
+    // entries return them for every pair
+    if (h == 1 && (P.pw_all || (fl & PF_CONTACT))) P.pw[p] = w;
+    P.pflag[p] = fl;
+    return (fl & PF_CONTACT) != 0;
+}
+
 // refresh_distances (proximity.cpp:190-202) with the pre-shrink bound, the
 // vertex bound of the next step (proximity.cpp:204-211) and, when no search
 // follows, the contact predicate of the next linearization. The erase of
@@ -2207,45 +2340,12 @@ __device__ void ph_refresh(const Params& P, double bound, bool next_search) {
         if (old_fl & PF_FAR) return false;  // provably still inactive: nothing observable changes
         ++nev;
         const uint64_t key = P.pkey[p];
-        const int ka = key_ka(key), kb = key_kb(key);
-        int va[3], vb[3];
-        split_ids(ka, kb, P.pids[p], va, vb);
-        Closest c;
-        const int h = pair_closest(ka, va, kb, vb, XLoad{P.x}, c);
-        uint8_t fl = old_fl & PF_ALL_STATIC;
-        double4 dd;
-        double4 w;
-        if (h != 1) {
-            dd = P.pdd[p];
-            w = P.pw[p];
-            fl |= P.pflag[p] & PF_DEGENERATE;
-        } else {
-            d3 dir = c.dir;
-            if (c.degenerate) {
-                const double4 old = P.pdd[p];
-                const d3 od = mk(old.x, old.y, old.z);
-                if (!is_zero(od)) dir = od;
-            }
-            dd = make_double4(dir.x, dir.y, dir.z, c.dist);
-            w = pack_weights(ka, kb, c);
-            P.pdd[p] = dd;
-            if (c.degenerate) fl |= PF_DEGENERATE;
-            if (c.dist < bound) fl |= PF_ACTIVE;
-            else if (c.dist >= bound + kFarMargin) fl |= PF_FAR;
-        }
-        if (fl & PF_ACTIVE) {
-            ++nact;
-            if (!next_search) {
-                for (int k = 0; k <= ka; ++k) vertex_min(P, va[k], dd.w);
-                for (int k = 0; k <= kb; ++k) vertex_min(P, vb[k], dd.w);
-            }
-        }
-        if (!next_search && contact_pred(P, ka, kb, va, vb, dd, w, fl)) fl |= PF_CONTACT;
-        // weights are read for contact rows only (ph_rows_build); the stage
-        // entries return them for every pair
-        if (h == 1 && (P.pw_all || (fl & PF_CONTACT))) P.pw[p] = w;
-        P.pflag[p] = fl;
-        return (fl & PF_CONTACT) != 0;
+        bool contact = false;
+        if (!with_pair_class(key_ka(key), key_kb(key), [&](auto pc) {
+                contact = refresh_pair<decltype(pc)::ka, decltype(pc)::kb>(P, p, key, old_fl, bound, next_search, nact);
+            }))
+            contact = refresh_pair<-1, -1>(P, p, key, old_fl, bound, next_search, nact);
+        return contact;
     });
     const long long na = block_sum(nact), ev = block_sum(nev);
     if (threadIdx.x == 0) {
