@@ -2268,17 +2268,17 @@ __device__ void ph_arch_merge(const Params& P, long long nnew, int sel, long lon
 // ============================================================ refresh (H)
 // one pair of ph_refresh for a compile-time pair class (KA < 0: runtime class)
 template <int KA, int KB>
-__device__ __forceinline__ bool refresh_pair(const Params& P, long long p, uint64_t key, uint8_t old_fl, double bound,
-                                             bool next_search, long long& nact) {
+__device__ __forceinline__ bool refresh_pair(const Params& P, long long p, uint64_t key, int4 id, uint8_t old_fl,
+                                             double bound, bool next_search, long long& nact) {
     const int ka = KA >= 0 ? KA : key_ka(key), kb = KA >= 0 ? KB : key_kb(key);
     int va[3], vb[3];
     Closest c;
     int h;
     if constexpr (KA >= 0) {
-        split_ids_t<KA, KB>(P.pids[p], va, vb);
+        split_ids_t<KA, KB>(id, va, vb);
         h = pair_closest_t<KA, KB>(va, vb, XLoad{P.x}, c);
     } else {
-        split_ids(ka, kb, P.pids[p], va, vb);
+        split_ids(ka, kb, id, va, vb);
         h = pair_closest(ka, va, kb, vb, XLoad{P.x}, c);
     }
     uint8_t fl = old_fl & PF_ALL_STATIC;
@@ -2336,15 +2336,18 @@ __device__ void ph_refresh(const Params& P, double bound, bool next_search) {
     const long long np = P.g->np;
     long long nact = 0, nev = 0;
     for_pair_tiles(P, np, [&](long long p) -> bool {
+        // the pair's flag, key and vertex ids in one load round
         const uint8_t old_fl = P.pflag[p];
+        const uint64_t key = P.pkey[p];
+        const int4 id = P.pids[p];
         if (old_fl & PF_FAR) return false;  // provably still inactive: nothing observable changes
         ++nev;
-        const uint64_t key = P.pkey[p];
         bool contact = false;
         if (!with_pair_class(key_ka(key), key_kb(key), [&](auto pc) {
-                contact = refresh_pair<decltype(pc)::ka, decltype(pc)::kb>(P, p, key, old_fl, bound, next_search, nact);
+                contact = refresh_pair<decltype(pc)::ka, decltype(pc)::kb>(P, p, key, id, old_fl, bound, next_search,
+                                                                           nact);
             }))
-            contact = refresh_pair<-1, -1>(P, p, key, old_fl, bound, next_search, nact);
+            contact = refresh_pair<-1, -1>(P, p, key, id, old_fl, bound, next_search, nact);
         return contact;
     });
     const long long na = block_sum(nact), ev = block_sum(nev);
