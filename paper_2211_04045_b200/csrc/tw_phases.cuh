@@ -243,6 +243,22 @@ __device__ void ph_refit(const Params& P) {
     }
 }
 
+// Euclidean refinement of the inflated-box test: with the query box inflated
+// by dinfl (rounded outwards), lo - qhi + dinfl and qlo + dinfl - hi are lower
+// bounds of the axis gaps between the un-inflated boxes, hence of the gaps
+// between the simplices; a box pair whose gap vector is longer than d_max
+// holds no pair closer than d_max. The float slack per axis (1 um + 3e-7 of
+// the query box's largest coordinate: several ulps of the float rounding of
+// the differences) and 1e-5 relative on the square keep the test
+// conservative, so only candidates the exact filter would reject are dropped
+// (the pair set is unchanged).
+__device__ __forceinline__ bool box_near(float4 qlo, float4 qhi, float4 lo, float4 hi, float dinf, float d2) {
+    const float gx = fmaxf(0.f, fmaxf(lo.x - qhi.x, qlo.x - hi.x) + dinf);
+    const float gy = fmaxf(0.f, fmaxf(lo.y - qhi.y, qlo.y - hi.y) + dinf);
+    const float gz = fmaxf(0.f, fmaxf(lo.z - qhi.z, qlo.z - hi.z) + dinf);
+    return gx * gx + gy * gy + gz * gz <= d2;
+}
+
 __device__ __forceinline__ bool box_hit(float4 qlo, float4 qhi, float4 lo, float4 hi) {
     return qlo.x <= hi.x && qlo.y <= hi.y && qlo.z <= hi.z && lo.x <= qhi.x && lo.y <= qhi.y &&
            lo.z <= qhi.z;
@@ -455,6 +471,11 @@ __device__ void ph_traverse(const Params& P) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     int* stack = sstack[warp];
+    const double dinfl_all = P.cfg.d_max * (1.0 + 1e-6) + 1e-12;
+    // Euclidean pruning (box_near) for the proximity search; off for the
+    // swept boxes of the certification
+    const float dinf_f = P.ccd_x1 ? 0.f : __double2float_rd(dinfl_all);
+    const float d2_f = P.ccd_x1 ? __int_as_float(0x7f800000) : (float)(P.cfg.d_max * P.cfg.d_max * (1.0 + 1e-5));
     for (;;) {
         long long base = 0;
         if (lane == 0) base = (long long)atomicAdd(&P.g->work_q, 32ull);
@@ -466,6 +487,7 @@ __device__ void ph_traverse(const Params& P) {
         const Bvh& B = P.bvh[cls];
         P.qcount[q] = 0;
         float4 qlo = make_float4(1.f, 1.f, 1.f, 0.f), qhi = make_float4(0.f, 0.f, 0.f, 0.f);  // empty box
+        float dinf_q = 0.f;
         if (ia >= 0) {
             int va[3];
             simplex_ids(P, ka, ia, va);
@@ -486,11 +508,14 @@ __device__ void ph_traverse(const Params& P) {
             }
             // float box of the query inflated by d_max (certification: 1e-12 on
             // both boxes), rounded outwards
-            const double dinfl = P.ccd_x1 ? 1e-12 : P.cfg.d_max * (1.0 + 1e-6) + 1e-12;
+            const double dinfl = P.ccd_x1 ? 1e-12 : dinfl_all;
             qlo = make_float4(__double2float_rd(lo3[0] - dinfl), __double2float_rd(lo3[1] - dinfl),
                               __double2float_rd(lo3[2] - dinfl), 0.f);
             qhi = make_float4(__double2float_ru(hi3[0] + dinfl), __double2float_ru(hi3[1] + dinfl),
                               __double2float_ru(hi3[2] + dinfl), 0.f);
+            const float mag = fmaxf(fmaxf(fmaxf(fabsf(qlo.x), fabsf(qhi.x)), fmaxf(fabsf(qlo.y), fabsf(qhi.y))),
+                                    fmaxf(fabsf(qlo.z), fabsf(qhi.z)));
+            dinf_q = dinf_f - (1e-6f + 3e-7f * mag);  // the gap lower bounds, less the float slack
         }
         // canonical partners only: EE (a = lower edge index) and VV (a < b)
         const bool ordered = (ka == KE) || (ka == KV && kb == KV);
@@ -535,10 +560,13 @@ __device__ void ph_traverse(const Params& P) {
             // subtrees whose largest index is <= ia are skipped
             const int need = ordered ? ia : -0x7fffffff - 1;
             auto visit = [&](float4 l0, float4 h0, float4 l1, float4 h1) {
-                const bool hit0 = box_hit(qlo, qhi, l0, h0) && __float_as_int(h0.w) > need;
-                const bool hit1 = box_hit(qlo, qhi, l1, h1) && __float_as_int(h1.w) > need;
-                const bool any0 = __any_sync(0xffffffffu, hit0), any1 = __any_sync(0xffffffffu, hit1);
                 const int r0 = __float_as_int(l0.w), r1 = __float_as_int(l1.w);
+                // leaves (ref < 0, warp-uniform) also pass the Euclidean test
+                bool hit0 = box_hit(qlo, qhi, l0, h0) && __float_as_int(h0.w) > need;
+                bool hit1 = box_hit(qlo, qhi, l1, h1) && __float_as_int(h1.w) > need;
+                if (r0 < 0) hit0 = hit0 && box_near(qlo, qhi, l0, h0, dinf_q, d2_f);
+                if (r1 < 0) hit1 = hit1 && box_near(qlo, qhi, l1, h1, dinf_q, d2_f);
+                const bool any0 = __any_sync(0xffffffffu, hit0), any1 = __any_sync(0xffffffffu, hit1);
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     if (!(k ? any1 : any0)) continue;
