@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_resolve(Params P) {
                         while (next < ncol && R.rows(P, next) == 0) ++next;
                         // the next large color's static row data, in flight across the barrier
                         if (next < ncol && R.rows(P, next) > tail_rows) pgs_prefetch(P, R, next, nsub, pre);
+                        // ph_pgs_color (a large color or a run of small ones)
                         SUBSYNC(nsub);
                         c = next;
                     }
