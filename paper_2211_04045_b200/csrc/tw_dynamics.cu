@@ -306,16 +306,29 @@ __device__ __forceinline__ d3 hess_row(const DynParams& P, int v, const double4*
     const d3 zv = l4(z[v]);
     d3 out = scl(P.sdiag[v], zv);
     if (dyn) {
-        for (int k = P.vedge_off[v]; k < P.vedge_off[v + 1]; ++k) {
-            const double a = P.inc_a[k];
-            const double4 ub = P.inc_u[k];
-            if (a == 0.0 && ub.w == 0.0) continue;
-            const int o = P.inc_o[k];
+        // K z_v - K z_o per incident edge (the second only when the other end
+        // is dynamic), added in incidence order; two incidences per round so
+        // their loads and neighbour gathers overlap
+        const int k1 = P.vedge_off[v + 1];
+        int k = P.vedge_off[v];
+        auto term = [&](double a, const double4& ub, int o, const d3& zo) {
+            if (a == 0.0 && ub.w == 0.0) return;
             const d3 u = l4(ub);
-            // K z_v - K z_o (the second only when the other end is dynamic)
             d3 t = zv;
-            if (o >= 0) t = sub(zv, l4(z[o]));
+            if (o >= 0) t = sub(zv, zo);
             out = add(out, add(scl(a, t), scl(ub.w * dot(u, t), u)));
+        };
+        for (; k + 1 < k1; k += 2) {
+            const double a0 = P.inc_a[k], a1 = P.inc_a[k + 1];
+            const double4 u0 = P.inc_u[k], u1 = P.inc_u[k + 1];
+            const int o0 = P.inc_o[k], o1 = P.inc_o[k + 1];
+            const d3 z0 = o0 >= 0 ? l4(z[o0]) : zv, z1 = o1 >= 0 ? l4(z[o1]) : zv;
+            term(a0, u0, o0, z0);
+            term(a1, u1, o1, z1);
+        }
+        if (k < k1) {
+            const int o0 = P.inc_o[k];
+            term(P.inc_a[k], P.inc_u[k], o0, o0 >= 0 ? l4(z[o0]) : zv);
         }
         for (int k = P.vh_off[v]; k < P.vh_off[v + 1]; ++k) {
             const int h = P.vh[k] >> 2, i = P.vh[k] & 3;
@@ -385,7 +398,12 @@ __device__ __forceinline__ void grid_total2(const double* part, int nb, double* 
     __shared__ double ra, rb;
     if (threadIdx.x < 32) {
         double a = 0.0, b = 0.0;
-        for (int i = threadIdx.x; i < nb; i += 32) a += ((volatile const double*)part)[2 * i], b += ((volatile const double*)part)[2 * i + 1];
+        // L2 loads (the barrier's acquire ordered them after the writers);
+        // one (a, b) pair per 16-byte load
+        for (int i = threadIdx.x; i < nb; i += 32) {
+            const double2 ab = __ldcg(reinterpret_cast<const double2*>(part) + i);
+            a += ab.x, b += ab.y;
+        }
         for (int o = 16; o > 0; o >>= 1) {
             a += __shfl_down_sync(0xffffffffu, a, o);
             b += __shfl_down_sync(0xffffffffu, b, o);
