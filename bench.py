@@ -287,7 +287,7 @@ class FrameRunner:
     (tw_step_device on HBM state reset from pristine copies outside the timed
     region) and end to end (tw_step with pinned host buffers)."""
 
-    def __init__(self, ctx, scene, args, jitter=None):
+    def __init__(self, ctx, scene, args, jitter=None, energy=None):
         import torch
 
         from paper_2211_04045_b200 import capi
@@ -297,7 +297,7 @@ class FrameRunner:
         self.mesh = capi.Mesh.from_scene(ctx, self.sc)
         from paper_2211_04045_b200 import scenes
 
-        self.dyn = capi.Dynamics(ctx, self.mesh, self.sc.x, **scenes.FRAME_ENERGY)
+        self.dyn = capi.Dynamics(ctx, self.mesh, self.sc.x, **{**scenes.FRAME_ENERGY, **(energy or {})})
         self.kw = dict(RESOLVE_KW, coloring_mode=args.coloring)
         self.d_x0 = torch.from_numpy(self.sc.x).cuda()
         self.d_v0 = torch.from_numpy(self.v0).cuda()
@@ -537,25 +537,33 @@ def run_configs(ctx, args, peak):
                                             "kind": "reference", "sample": f"one full resolve on the reference "
                                             f"build: {secs:.1f} s, {rs['steps']} steps, {rs['searches']} searches"}
         mesh.close()
-    fr = FrameRunner(ctx, "reef", args)
-    for _ in range(2):
-        fr.reset()
-        fr.step_device()
-    ms = 0.0
-    for i in range(n):
-        fr.reset()
-        flush.fill_(i & 0xFF)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        st = fr.step_device()
-        b.record(stream)
-        torch.cuda.synchronize()
-        ms += a.elapsed_time(b)
-    out["cfg2_reef_knot_frame"] = {"vertices": fr.sc.nv, "triangles": int(len(fr.sc.triangles)),
-                                   "steps_per_s": round(n / (ms / 1e3), 2), "ms": round(ms / n, 3),
-                                   "resolve_alg1_steps": st["resolve_steps"], "searches": st["searches"],
-                                   "pcg_ms": round(st["pcg_ms"], 3), "resolve_ms": round(st["resolve_ms"], 3)}
-    fr.close()
+    # configs[1] the reef frame; and the bow frame with Coulomb friction
+    # (mu = 0.3: step() runs friction_filter on the target, dynamics.cpp:338,
+    # with the search at d_max so the filter sees every pair)
+    for key, scene, energy in (("cfg2_reef_knot_frame", "reef", None),
+                               ("bow_knot_frame_friction_mu0.3", "bow", {"mu": 0.3})):
+        fr = FrameRunner(ctx, scene, args, energy=energy)
+        for _ in range(2):
+            fr.reset()
+            fr.step_device()
+        ms = fric = 0.0
+        for i in range(n):
+            fr.reset()
+            flush.fill_(i & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st = fr.step_device()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms += a.elapsed_time(b)
+            fric += st["friction_ms"]
+        out[key] = {"vertices": fr.sc.nv, "triangles": int(len(fr.sc.triangles)),
+                    "steps_per_s": round(n / (ms / 1e3), 2), "ms": round(ms / n, 3),
+                    "resolve_alg1_steps": st["resolve_steps"], "searches": st["searches"],
+                    "pcg_ms": round(st["pcg_ms"], 3), "resolve_ms": round(st["resolve_ms"], 3)}
+        if energy:
+            out[key].update({"friction_ms": round(fric / n, 3), "pairs_filtered": st["num_pairs"]})
+        fr.close()
     return out
 
 

@@ -274,7 +274,7 @@ typedef struct {
     double repulsion_radius;    /* 1e-3 m */
     double dt;                  /* 0.01 s */
     int32_t newton_iters;       /* 1 */
-    double mu;                  /* 0: friction_filter (mu > 0) returns TW_EUNSUPPORTED */
+    double mu;                  /* 0; mu > 0 runs friction_filter on the target */
     double pcg_tol;             /* 1e-6 relative */
     int32_t pcg_max_iters;      /* 400 */
 } tw_energy_model;
@@ -286,13 +286,14 @@ typedef struct {
     int32_t resolve_converged;
     int32_t pcg_iterations;  /* summed over Newton iterations */
     int32_t pcg_converged;
-    int32_t num_pairs;       /* pairs of the last target's search (cutoff min(d_max, repulsion_radius)) */
+    int32_t num_pairs;       /* pairs of the last target's search (cutoff min(d_max, repulsion_radius); d_max when mu > 0) */
     int32_t repulsive_pairs; /* pairs closer than repulsion_radius */
     double device_ms;        /* CUDA-event time of the whole step on the device */
     double resolve_ms;       /* of which resolve */
     double wall_ms;
     double target_ms;        /* of which the Newton targets (search + gradient/Hessian + PCG) */
     double pcg_ms;           /* of which the PCG kernels */
+    double friction_ms;      /* friction_filter (mu > 0) */
 } tw_step_stats;
 
 typedef struct tw_dyn tw_dyn;
@@ -306,9 +307,17 @@ void tw_dyn_destroy(tw_dyn* dyn);
 int32_t tw_dyn_num_hinges(const tw_dyn* dyn);
 /* proximity_search(x, d_max) + gradient_and_hessian + add_repulsion +
  * newton_target (dynamics.cpp:334-337) with the inertia target built from
- * (x0, v0): writes the Newton target y_out and (nullable) the gradient. */
+ * (x0, v0), then friction_filter when mu > 0 (dynamics.cpp:338): writes the
+ * target y_out and (nullable) the gradient. */
 int tw_newton_target(tw_ctx* ctx, tw_mesh* mesh, tw_dyn* dyn, double d_max, const double* x0, const double* v0,
                      const double* x, double* y_out, double* grad_out, tw_step_stats* stats);
+/* friction_filter (dynamics.cpp:272-324) with the pair set of
+ * proximity_search(x, d_max): the target y_target (nv * 3) filtered by the
+ * inelastic, Coulomb-capped pair impulses of the dyn's model, in pair order
+ * (bit-identical to the sequential loop). step() / tw_newton_target apply it
+ * when mu > 0, as dynamics.cpp:338 does. */
+int tw_friction_filter(tw_ctx* ctx, tw_mesh* mesh, tw_dyn* dyn, double d_max, const double* x, const double* y_target,
+                       double* y_out);
 /* step() (dynamics.cpp:326-349): x, v (nv * 3) in/out, host buffers. */
 int tw_step(tw_ctx* ctx, tw_mesh* mesh, tw_dyn* dyn, const tw_resolve_config* cfg, double* x, double* v,
             tw_step_stats* stats);

@@ -7,6 +7,7 @@ package (paper_2211_04045_b200) never imports it.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 
@@ -351,3 +352,69 @@ def ccd_certify_path(scene, path):
         tot += v
         cert += c
     return tot, cert
+
+
+def _simplex(m, kind, idx):
+    if kind == KIND_V:
+        return [int(idx)]
+    if kind == KIND_E:
+        return [int(v) for v in m.edges[idx]]
+    return [int(v) for v in m.triangles[idx]]
+
+
+def friction_filter(m, x, y_target, d_max, mu, dt=0.01, repulsion_radius=1e-3):
+    """friction_filter(model, mesh, x, y_target, proximity_search(x, d_max))
+    restated from dynamics.cpp:272-324 (Python scalars: IEEE double, no
+    contraction, the reference's association), on the oracle's search and
+    closest points. Pure-Python loop: small scenes only."""
+    x = _f64(x, (-1, 3))
+    y = _f64(y_target, (-1, 3)).copy()
+    inv = [float(v) for v in _f64(m.inv_mass)]
+    pairs = search(m, x, d_max)
+    xs = [list(map(float, r)) for r in x]
+
+    def is_zero(v):
+        return all(abs(c) <= 1e-12 for c in v)
+
+    for i in range(len(pairs)):
+        if pairs.flags[i] & PF_ALL_STATIC:  # :278
+            continue
+        key = int(pairs.keys[i])
+        ka, kb = key >> 62, (key >> 60) & 3
+        va, vb = _simplex(m, ka, (key >> 30) & 0x3FFFFFFF), _simplex(m, kb, key & 0x3FFFFFFF)
+        res = closest(ka, va, kb, vb, y)  # penetration at the target state, :279
+        if res is None:
+            continue
+        depth = repulsion_radius - float(res["distance"])
+        if depth <= 0.0:
+            continue
+        n = [float(c) for c in res["direction"]]
+        if is_zero(n):
+            n = [float(c) for c in pairs.dir[i]]  # p.closest.direction, :284
+        if is_zero(n):
+            continue
+        vid = va + vb
+        sw = [float(w) for w in res["weights_a"][:len(va)]] + [-float(w) for w in res["weights_b"][:len(vb)]]
+        kappa = 0.0
+        v_rel = [0.0, 0.0, 0.0]
+        for a, v in enumerate(vid):  # :299-302
+            kappa += sw[a] * sw[a] * inv[v]
+            v_rel = [v_rel[c] + (sw[a] * (float(y[v, c]) - xs[v][c])) / dt for c in range(3)]
+        if kappa <= 0.0:
+            continue
+        vn = (v_rel[0] * n[0] + v_rel[1] * n[1]) + v_rel[2] * n[2]  # :307-318
+        hi = depth / dt
+        jn = 0.0 if -vn < 0.0 else (hi if hi < -vn else -vn)  # std::clamp
+        impulse = [jn * c for c in n]
+        vt = [v_rel[c] - vn * n[c] for c in range(3)]
+        vt_norm = math.sqrt((vt[0] * vt[0] + vt[1] * vt[1]) + vt[2] * vt[2])
+        if vt_norm > 1e-12:
+            cap = mu * jn
+            dvt = vt_norm if vt_norm < cap else cap  # std::min(cap, vt_norm)
+            impulse = [impulse[c] - dvt * (vt[c] / vt_norm) for c in range(3)]
+        dv = [c / kappa for c in impulse]
+        for a, v in enumerate(vid):  # :320-321
+            s = dt * inv[v] * sw[a]
+            for c in range(3):
+                y[v, c] = float(y[v, c]) + s * dv[c]
+    return y

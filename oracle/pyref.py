@@ -87,6 +87,7 @@ def lib():
                                     C.c_uint64, C.c_int64, P, P, P, P, P, P, P]
         L.ref_step.argtypes = [P, P, C.POINTER(EnergyParams), C.POINTER(Config), P, P, P]
         L.ref_newton_target.argtypes = [P, P, C.POINTER(EnergyParams), C.c_double, P, P, P, P, P]
+        L.ref_friction_filter.argtypes = [P, P, C.POINTER(EnergyParams), C.c_double, P, P, P]
         L.ref_incremental_energy.restype = C.c_double
         L.ref_incremental_energy.argtypes = [P, P, C.POINTER(EnergyParams), P]
         L.ref_normal_flow_target.argtypes = [P, P, C.c_double, C.c_double, P]
@@ -229,6 +230,17 @@ def newton_target(mesh: RefMesh, rest_x, x, d_max=4e-3, **energy):
     if rc != 0:
         raise RuntimeError(_err())
     return y, g, it.value, bool(conv.value)
+
+
+def friction_filter(mesh: RefMesh, rest_x, x, y_target, d_max=4e-3, **energy):
+    """The reference's friction_filter on the pair set of proximity_search(x, d_max)."""
+    ep = energy_params(**energy)
+    x, yt = _f64(x), _f64(y_target)
+    y = np.zeros_like(x)
+    rc = lib().ref_friction_filter(mesh.h, _p(_f64(rest_x)), C.byref(ep), d_max, _p(x), _p(yt), _p(y))
+    if rc != 0:
+        raise RuntimeError(_err())
+    return y
 
 
 def incremental_energy(mesh: RefMesh, rest_x, x, **energy):

@@ -280,6 +280,26 @@ int ref_newton_target(void* mp, const double* rest_x, const EnergyParams* ep, do
     }
 }
 
+// friction_filter(model, mesh, x, y_target, proximity_search(x, d_max))
+// (dynamics.cpp:272-324), the reference's own function.
+int ref_friction_filter(void* mp, const double* rest_x, const EnergyParams* ep, double d_max,
+                        const double* x, const double* y_target, double* y_out) {
+    auto* m = static_cast<MeshState*>(mp);
+    try {
+        EnergyModel model = to_model(ep);
+        MeshState rest = *m;
+        rest.positions = to_pos(m->num_vertices(), rest_x);
+        model.prepare(rest);
+        const Positions xs = to_pos(m->num_vertices(), x);
+        const ProximitySet set = proximity_search(xs, *m, d_max);
+        const Positions y = friction_filter(model, *m, xs, to_pos(m->num_vertices(), y_target), set);
+        from_pos(y, y_out);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 double ref_incremental_energy(void* mp, const double* rest_x, const EnergyParams* ep,
                               const double* x) {
     auto* m = static_cast<MeshState*>(mp);

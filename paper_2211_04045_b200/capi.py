@@ -68,7 +68,7 @@ EXPORTS = [
     "tw_stage_advance", "tw_ccd_certify", "tw_default_energy_model", "tw_dyn_create", "tw_dyn_destroy",
     "tw_dyn_num_hinges", "tw_newton_target", "tw_step", "tw_step_device", "tw_stage_lcp",
     "tw_stage_linearize_ex", "tw_stage_build_rows", "tw_stage_constraint_value", "tw_stage_fill_diag",
-    "tw_normal_flow_target", "tw_last_path", "tw_ctx_set_grid_share",
+    "tw_normal_flow_target", "tw_last_path", "tw_ctx_set_grid_share", "tw_friction_filter",
 ]
 
 
@@ -89,6 +89,7 @@ class StepStats(C.Structure):
         ("pcg_iterations", C.c_int32), ("pcg_converged", C.c_int32), ("num_pairs", C.c_int32),
         ("repulsive_pairs", C.c_int32), ("device_ms", C.c_double), ("resolve_ms", C.c_double),
         ("wall_ms", C.c_double), ("target_ms", C.c_double), ("pcg_ms", C.c_double),
+        ("friction_ms", C.c_double),
     ]
 
 _LIB = None
@@ -139,6 +140,7 @@ def lib():
         L.tw_dyn_num_hinges.argtypes = [P]
         L.tw_newton_target.argtypes = [P, P, P, C.c_double, P, P, P, P, P, C.POINTER(StepStats)]
         L.tw_step.argtypes = [P, P, P, C.POINTER(Config), P, P, C.POINTER(StepStats)]
+        L.tw_friction_filter.argtypes = [P, P, P, C.c_double, P, P, P]
         L.tw_step_device.argtypes = [P, P, P, C.POINTER(Config), P, P, C.POINTER(StepStats)]
         _LIB = L
     return _LIB
@@ -559,7 +561,8 @@ def _step_stats(st):
 
 
 def newton_target(ctx: Context, mesh: Mesh, dyn: Dynamics, x0, v0, x=None, d_max=4e-3):
-    """search + gradient_and_hessian + add_repulsion + newton_target: (y, grad, stats)."""
+    """search + gradient_and_hessian + add_repulsion + newton_target (+ friction_filter
+    when mu > 0): (y, grad, stats)."""
     x0 = np.ascontiguousarray(x0, np.float64).reshape(-1, 3)
     v0 = np.ascontiguousarray(v0, np.float64).reshape(-1, 3)
     x = x0 if x is None else np.ascontiguousarray(x, np.float64).reshape(-1, 3)
@@ -571,6 +574,16 @@ def newton_target(ctx: Context, mesh: Mesh, dyn: Dynamics, x0, v0, x=None, d_max
         raise NotImplementedError(lib().tw_last_error(ctx.h).decode())
     ctx.check(rc)
     return y, g, _step_stats(st)
+
+
+def friction_filter(ctx: Context, mesh: Mesh, dyn: Dynamics, x, y_target, d_max=4e-3):
+    """friction_filter(model, mesh, x, y_target, proximity_search(x, d_max))
+    (dynamics.cpp:272-324) on the device: the filtered target."""
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    yt = np.ascontiguousarray(y_target, np.float64).reshape(-1, 3)
+    y = np.zeros_like(yt)
+    ctx.check(lib().tw_friction_filter(ctx.h, mesh.h, dyn.h, d_max, _p(x), _p(yt), _p(y)))
+    return y
 
 
 def step(ctx: Context, mesh: Mesh, dyn: Dynamics, x, v, **kw):

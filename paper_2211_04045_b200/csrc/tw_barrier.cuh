@@ -2,8 +2,8 @@
 //
 // One arrival per CTA: CTA 0 adds 2^31 - (n - 1), every other CTA adds 1, so
 // the arrival that completes the count flips bit 31 and the waiters watch for
-// the flip. The arrival is a release atomic and the poll an acquire load (no
-// separate fences). The first poll is issued only once the arrival has
+// the flip. The arrival is a release atomic; waiters poll relaxed and fence
+// once after the flip (bar_poll_relaxed). The first poll is issued only once the arrival has
 // returned (a data dependency on its result): polls that race the arrivals
 // queue at the same L2 line and slow the last arrival down. Measured on B200
 // (tools/bar_bench.cu, 2,000 barriers, 256-thread CTAs): 1.16 us per barrier at
@@ -26,6 +26,18 @@ __device__ __forceinline__ unsigned bar_poll(const unsigned* w) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
     return v;
 }
+
+// Relaxed poll: an acquire load compiles to LDG.STRONG.GPU + CCTL.IVALL, i.e.
+// every poll invalidates the whole L1 of the SM -- including the lines the
+// co-resident CTAs still working on the phase are gathering from. Waiters
+// poll relaxed and order their later reads with one fence after the flip
+// (the fence-based acquire pattern of the PTX memory model).
+__device__ __forceinline__ unsigned bar_poll_relaxed(const unsigned* w) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
+    return v;
+}
+__device__ __forceinline__ void bar_acquire_fence() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 __device__ __forceinline__ bool bar_flipped(unsigned old, unsigned now) { return ((old ^ now) & 0x80000000u) != 0u; }
 

@@ -367,8 +367,9 @@ __device__ __forceinline__ void dyn_sync(DynGlobals* g) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned old = bar_arrive(&g->bar, blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u);
-        while (!bar_flipped(old, bar_poll(&g->bar))) {
+        while (!bar_flipped(old, bar_poll_relaxed(&g->bar))) {
         }
+        bar_acquire_fence();
     }
     __syncthreads();
 }
@@ -648,6 +649,268 @@ __global__ void k_velocity(int nv, const double* inv_mass, const double* x, cons
     vel[i] = inv_mass[i / 3] == 0.0 ? 0.0 : (x[i] - x0[i]) / dt;
 }
 
+// ------------------------------------------------------- friction filter
+// friction_filter (dynamics.cpp:272-324) is a Gauss-Seidel pass over the pair
+// set in pair order: every pair reads y at its vertices and, when it
+// penetrates the repulsion radius at that y, writes y back. In the sorted pair
+// set nearly every pair shares a vertex with the one before it, so the pass is
+// one long dependency chain -- but only the writers carry data along it (a
+// pair that leaves y unchanged is invisible to the pairs after it). The device
+// therefore runs it speculatively and verifies exactly:
+//
+//  1. every pair is evaluated at the input y0 in parallel; the ones that reach
+//     the write (depth > 0, a normal, kappa > 0) form the writer set W;
+//  2. the sequential pass is replayed over W alone as a dataflow (below),
+//     logging every write as (vertex, pair, y after);
+//  3. every pair outside W is re-evaluated at the state it would see in that
+//     replay (per vertex, the last logged write of an earlier pair, else y0);
+//     pairs that would write join W and the replay restarts from y0.
+// When step 3 adds nothing, no pair outside W writes in the replay's
+// history, so by induction over the pair order the full sequential pass
+// visits exactly the states of the replay: the result is bit-identical.
+//
+// The replay is a dataflow over W's shared vertices: every (vertex, pair,
+// slot) incidence sorted by vertex names the pair to wait for (pred, <= 4
+// per pair); a pair runs once its predecessors have published their done
+// flag (release store; relaxed polls and one fence) and touches only its own
+// vertices. A vertex joins the order only when a write can change it:
+// dynamic vertices, and static ones with a -0.0 coordinate (the write adds
+// (dt * 0 * sw) * dv = +-0, which leaves every other bit pattern unchanged).
+constexpr uint8_t FR_ALL_STATIC = 2;  // the pair flag bit PF_ALL_STATIC (tw_engine.cuh)
+
+struct FrParams {
+    long long np;
+    double dt, mu, r_rep;
+    const double* inv_mass;
+    const double* x;        // N x 3: the Newton point
+    double* y;              // N x 3: target in, filtered target out
+    const double* y0;       // N x 3: the input target (replays restart from it)
+    const uint64_t* pkey;
+    const int4* pids;
+    const double4* pdd;     // search direction at x (the fallback normal), distance
+    const uint8_t* pflag;
+    uint8_t* cand;          // per pair: in the writer set W
+    unsigned long long* ent;  // (vertex << 32 | pair << 2 | slot)
+    int* pred;              // 4 per pair: the pair to wait for at that slot, -1 none
+    int* done;
+    int* misc;              // [0] entries, [1] ticket, [2] |W|, [3] added to W, [4] log entries
+    unsigned long long* log_key;  // (vertex << 32 | pair) per logged write
+    double4* log_val;             // y after that write
+    const unsigned long long* slog_key;  // the log sorted by key, with the entry index
+    const int* slog_idx;
+    int nlog;
+};
+
+__device__ __forceinline__ void fr_verts(uint64_t key, int4 ids, int (&v)[4]) {
+    v[0] = ids.x, v[1] = ids.y, v[2] = ids.z, v[3] = ids.w;
+}
+
+__device__ __forceinline__ bool fr_tracked(const FrParams& F, int v) {
+    if (F.inv_mass[v] > 0.0) return true;
+    const double* p = F.y0 + 3 * (size_t)v;  // static vertices: only the input can hold a -0.0
+    return (p[0] == 0.0 && signbit(p[0])) || (p[1] == 0.0 && signbit(p[1])) || (p[2] == 0.0 && signbit(p[2]));
+}
+
+// The body of the reference loop for pair i (dynamics.cpp:278-318) at the
+// state Y: false when the pair leaves y alone, else the signed weights and dv
+// of its write (:320-321).
+template <int KA, int KB, typename LoadY>
+__device__ __forceinline__ bool fr_eval(const FrParams& F, long long i, const int (&vid)[4], const LoadY& Y,
+                                        double (&sw)[4], d3& dv) {
+    constexpr int m = (KA + 1) + (KB + 1);
+    const int ia[3] = {vid[0], KA >= 1 ? vid[1] : -1, KA >= 2 ? vid[2] : -1};
+    const int ib[3] = {vid[KA + 1], KB >= 1 ? vid[KA + 2] : -1, KB >= 2 ? vid[KA + 3] : -1};
+    Closest res;
+    closest_init(res);
+    if (pair_closest_t<KA, KB>(ia, ib, Y, res) != 1) return false;  // penetration at the target state
+    const double depth = F.r_rep - res.dist;
+    if (depth <= 0.0) return false;
+    d3 n = res.dir;
+    if (is_zero(n)) {
+        const double4 c = F.pdd[i];
+        n = mk(c.x, c.y, c.z);
+    }
+    if (is_zero(n)) return false;
+#pragma unroll
+    for (int a = 0; a <= KA; ++a) sw[a] = res.wa[a];
+#pragma unroll
+    for (int b = 0; b <= KB; ++b) sw[KA + 1 + b] = -res.wb[b];
+    double kappa = 0.0;
+    d3 v_rel = mk(0, 0, 0);
+#pragma unroll
+    for (int a = 0; a < m; ++a) {
+        const int v = vid[a];
+        kappa += sw[a] * sw[a] * F.inv_mass[v];
+        v_rel = add(v_rel, dvd(scl(sw[a], sub(Y(v), ld3(F.x, v))), F.dt));
+    }
+    if (kappa <= 0.0) return false;
+    // inelastic normal impulse capped by the depth rate, Coulomb-capped tangential part
+    const double vn = dot(v_rel, n);
+    const double jn = clampd(-vn, 0.0, depth / F.dt);
+    d3 impulse = scl(jn, n);
+    const d3 vt = sub(v_rel, scl(vn, n));
+    const double vt_norm = nrm(vt);
+    if (vt_norm > 1e-12) {
+        const double dvt = mind(F.mu * jn, vt_norm);
+        impulse = sub(impulse, scl(dvt, dvd(vt, vt_norm)));
+    }
+    dv = dvd(impulse, kappa);
+    return true;
+}
+
+template <typename F_>
+__device__ __forceinline__ bool fr_class(uint64_t key, F_&& f) {
+    return with_pair_class(key_ka(key), key_kb(key), f);
+}
+
+// 1. W = the pairs that write at y0
+__global__ void k_fr_eval0(FrParams F) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= F.np) return;
+    bool w = false;
+    if (!(F.pflag[i] & FR_ALL_STATIC)) {  // dynamics.cpp:278
+        const uint64_t key = F.pkey[i];
+        int vid[4];
+        fr_verts(key, F.pids[i], vid);
+        auto Y = [&](int v) { return ld3(F.y0, v); };
+        fr_class(key, [&](auto c) {
+            double sw[4];
+            d3 dv;
+            w = fr_eval<decltype(c)::ka, decltype(c)::kb>(F, i, vid, Y, sw, dv);
+        });
+    }
+    F.cand[i] = w;
+    if (w) atomicAdd(F.misc + 2, 1);
+}
+
+// 2a. dependency order of W (pred reset for every pair)
+__global__ void k_fr_entries(FrParams F) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= F.np) return;
+    reinterpret_cast<int4*>(F.pred)[i] = make_int4(-1, -1, -1, -1);
+    F.done[i] = 0;
+    if (!F.cand[i]) return;
+    const uint64_t key = F.pkey[i];
+    int v[4];
+    fr_verts(key, F.pids[i], v);
+    const int n = (key_ka(key) + 1) + (key_kb(key) + 1);
+    for (int k = 0; k < n; ++k)
+        if (fr_tracked(F, v[k]))
+            F.ent[atomicAdd(F.misc, 1)] = ((unsigned long long)(unsigned)v[k] << 32) | ((unsigned long long)i << 2) | k;
+}
+
+__global__ void k_fr_pred(FrParams F, int n) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n || j == 0) return;
+    const unsigned long long e = F.ent[j], p = F.ent[j - 1];
+    if ((e >> 32) == (p >> 32)) F.pred[(e & 0xffffffffu)] = (int)((p & 0xffffffffu) >> 2);
+}
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// y is written by other CTAs during the replay: read it at L2 (never a stale L1 line)
+__device__ __forceinline__ d3 ldy(const double* y, int v) {
+    return mk(__ldcg(y + 3 * v), __ldcg(y + 3 * v + 1), __ldcg(y + 3 * v + 2));
+}
+
+template <int KA, int KB>
+__device__ __forceinline__ void fr_apply(const FrParams& F, long long i, const int (&vid)[4]) {
+    constexpr int m = (KA + 1) + (KB + 1);
+    double sw[4];
+    d3 dv;
+    auto Y = [&](int v) { return ldy(F.y, v); };
+    if (!fr_eval<KA, KB>(F, i, vid, Y, sw, dv)) return;
+#pragma unroll
+    for (int a = 0; a < m; ++a) {
+        const int v = vid[a];
+        if (!fr_tracked(F, v)) continue;  // a +-0 write to an unchanged static vertex
+        const d3 o = add(ldy(F.y, v), scl(F.dt * F.inv_mass[v] * sw[a], dv));
+        __stcg(F.y + 3 * v, o.x), __stcg(F.y + 3 * v + 1, o.y), __stcg(F.y + 3 * v + 2, o.z);
+        const int e = atomicAdd(F.misc + 4, 1);
+        F.log_key[e] = ((unsigned long long)(unsigned)v << 32) | (unsigned long long)i;
+        F.log_val[e] = make_double4(o.x, o.y, o.z, 0.0);
+    }
+}
+
+// 2b. the replay over W. Warps take 32 consecutive pairs from a ticket counter
+// in pair order, so the earliest unfinished pair of W always belongs to a
+// running warp whose predecessors are all finished: the pass cannot stall.
+__global__ void __launch_bounds__(DTPB) k_friction(FrParams F) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(F.misc + 1, 32);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= F.np) return;
+        const long long i = (long long)base + lane;
+        bool pending = i < F.np && F.cand[i];
+        int4 pr = make_int4(-1, -1, -1, -1);
+        uint64_t key = 0;
+        int vid[4] = {-1, -1, -1, -1};
+        if (pending) {
+            pr = reinterpret_cast<const int4*>(F.pred)[i];
+            key = F.pkey[i];
+            fr_verts(key, F.pids[i], vid);
+        }
+        while (__any_sync(0xffffffffu, pending)) {
+            if (pending && (pr.x < 0 || ld_relaxed(F.done + pr.x)) && (pr.y < 0 || ld_relaxed(F.done + pr.y)) &&
+                (pr.z < 0 || ld_relaxed(F.done + pr.z)) && (pr.w < 0 || ld_relaxed(F.done + pr.w))) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                fr_class(key, [&](auto c) { fr_apply<decltype(c)::ka, decltype(c)::kb>(F, i, vid); });
+                st_release(F.done + i, 1);
+                pending = false;
+            }
+        }
+    }
+}
+
+__global__ void k_iota(int* a, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = i;
+}
+
+// the state pair i sees at vertex v in the replay: the last logged write of
+// an earlier pair, else the input
+__device__ __forceinline__ d3 fr_state(const FrParams& F, int v, long long i) {
+    const unsigned long long t = ((unsigned long long)(unsigned)v << 32) | (unsigned long long)i;
+    int lo = 0, hi = F.nlog;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (F.slog_key[mid] < t) lo = mid + 1;
+        else hi = mid;
+    }
+    if (lo > 0 && (F.slog_key[lo - 1] >> 32) == (unsigned long long)(unsigned)v) {
+        const double4 o = F.log_val[F.slog_idx[lo - 1]];
+        return mk(o.x, o.y, o.z);
+    }
+    return ld3(F.y0, v);
+}
+
+// 3. pairs outside W that would write in the replay's history join W
+__global__ void k_fr_verify(FrParams F) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= F.np || F.cand[i] || (F.pflag[i] & FR_ALL_STATIC)) return;
+    const uint64_t key = F.pkey[i];
+    int vid[4];
+    fr_verts(key, F.pids[i], vid);
+    auto Y = [&](int v) { return fr_state(F, v, i); };
+    bool w = false;
+    fr_class(key, [&](auto c) {
+        double sw[4];
+        d3 dv;
+        w = fr_eval<decltype(c)::ka, decltype(c)::kb>(F, i, vid, Y, sw, dv);
+    });
+    if (w) {
+        F.cand[i] = 1;
+        atomicAdd(F.misc + 3, 1);
+    }
+}
 
 // ---------------------------------------------------------- normal flow
 // normal_flow_target (normal_flow.cpp:38-81): area-weighted unit normals
@@ -723,9 +986,12 @@ struct tw_dyn {
     DevMem rest, hv, hk, vh_off, vh;
     DevMem inc_u, inc_a, inc_o, hx, hvel, x0, v0, xk, y, e_u, e_ab, rp_ids, rp_sw, rp_dir, rp_count, rs_key, rs_key2, vr_off, sort_tmp;
     DevMem sdiag, grad, pre, b, d, r, z, p, q, best, part, glob;
+    DevMem fr_pred, fr_done, fr_misc, fr_cand, fr_y0;  // friction_filter replay state
+    DevMem fr_log_key, fr_log_key2, fr_log_val, fr_log_idx, fr_log_idx2;
     long long rp_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // step timing (the resolve uses the context's own events)
     cudaEvent_t evt0 = nullptr, evp0 = nullptr, evp1 = nullptr;  // target / PCG timing
+    cudaEvent_t evf0 = nullptr, evf1 = nullptr;                  // friction_filter timing
 };
 
 namespace {
@@ -913,6 +1179,122 @@ int search_at_x(tw_ctx* ctx, tw_mesh* m, double d_max, long long* np) {
     return TW_OK;
 }
 
+// friction_filter (dynamics.cpp:272-324) on d_y (N x 3, in place) with the
+// pair set the context holds from the search at d_xk (np pairs, key order):
+// the writer-set speculation of k_fr_eval0 / k_friction / k_fr_verify.
+template <typename K>
+cudaError_t sort_keys(tw_dyn* D, K* in, K* out, int n, cudaStream_t s) {
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, in, out, n, 0, 64, s);
+    cudaError_t e = D->sort_tmp.ensure(tb);
+    if (e == cudaSuccess) e = cub::DeviceRadixSort::SortKeys(D->sort_tmp.p, tb, in, out, n, 0, 64, s);
+    return e;
+}
+
+int friction_device(tw_dyn* D, const double* d_xk, double* d_y, long long np) {
+    tw_ctx* ctx = D->ctx;
+    tw_mesh* m = D->mesh;
+    cudaStream_t s = ctx->stream;
+    if (np <= 0) return TW_OK;
+    if (np >= (1ll << 30)) return fail(ctx, TW_ECAPACITY, "friction_filter: too many pairs");
+    const size_t nv = (size_t)std::max(1, m->nv);
+    CK(D->fr_pred.ensure((size_t)np * 16));
+    CK(D->fr_done.ensure((size_t)np * 4));
+    CK(D->fr_cand.ensure((size_t)np));
+    CK(D->fr_misc.ensure(32));
+    CK(D->fr_y0.ensure(nv * 24));
+    CK(cudaMemcpyAsync(D->fr_y0.p, d_y, (size_t)m->nv * 24, cudaMemcpyDeviceToDevice, s));
+    FrParams F;
+    std::memset(&F, 0, sizeof F);
+    F.np = np, F.dt = D->model.dt, F.mu = D->model.mu, F.r_rep = D->model.repulsion_radius;
+    F.inv_mass = m->d_inv_mass.as<double>();
+    F.x = d_xk, F.y = d_y, F.y0 = D->fr_y0.as<double>();
+    F.pkey = ctx->pkey.as<uint64_t>();
+    F.pids = ctx->pids.as<int4>();
+    F.pdd = ctx->pdd.as<double4>();
+    F.pflag = ctx->pflag.as<uint8_t>();
+    F.cand = D->fr_cand.as<uint8_t>();
+    F.pred = D->fr_pred.as<int>();
+    F.done = D->fr_done.as<int>();
+    F.misc = D->fr_misc.as<int>();
+    const unsigned pb = (unsigned)((np + DTPB - 1) / DTPB);
+    CK(cudaMemsetAsync(D->fr_misc.p, 0, 32, s));
+    k_fr_eval0<<<pb, DTPB, 0, s>>>(F);
+    ++ctx->launches;
+    DSYNC("k_fr_eval0");
+    static int occ = -1;
+    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_friction, DTPB, 0);
+    int misc[8];
+    CK(cudaMemcpyAsync(misc, D->fr_misc.p, 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int round = 0;; ++round) {
+        const long long nw = misc[2];  // |W|
+        if (nw == 0) return TW_OK;     // nothing writes at y0 and (verified) nothing after
+        // buffers sized by |W|: <= 4 incidences and <= 4 logged writes per pair
+        CK(D->rs_key.ensure((size_t)nw * 4 * 8));
+        CK(D->rs_key2.ensure((size_t)nw * 4 * 8));
+        CK(D->fr_log_key.ensure((size_t)nw * 4 * 8));
+        CK(D->fr_log_key2.ensure((size_t)nw * 4 * 8));
+        CK(D->fr_log_val.ensure((size_t)nw * 4 * 32));
+        CK(D->fr_log_idx.ensure((size_t)nw * 4 * 4));
+        CK(D->fr_log_idx2.ensure((size_t)nw * 4 * 4));
+        F.ent = D->rs_key.as<unsigned long long>();
+        F.log_key = D->fr_log_key.as<unsigned long long>();
+        F.log_val = D->fr_log_val.as<double4>();
+        if (round) CK(cudaMemcpyAsync(d_y, D->fr_y0.p, (size_t)m->nv * 24, cudaMemcpyDeviceToDevice, s));
+        // misc[0] entries, [1] ticket, [3] added, [4] log entries restart; [2] = |W| stays
+        CK(cudaMemsetAsync(F.misc, 0, 8, s));
+        CK(cudaMemsetAsync(F.misc + 3, 0, 8, s));
+        k_fr_entries<<<pb, DTPB, 0, s>>>(F);
+        ++ctx->launches;
+        DSYNC("k_fr_entries");
+        CK(cudaMemcpyAsync(misc, D->fr_misc.p, 32, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int nent = misc[0];
+        if (nent > 1) {
+            CK(sort_keys(D, D->rs_key.as<unsigned long long>(), D->rs_key2.as<unsigned long long>(), nent, s));
+            ctx->launches += 4;
+            F.ent = D->rs_key2.as<unsigned long long>();
+            k_fr_pred<<<(nent + DTPB - 1) / DTPB, DTPB, 0, s>>>(F, nent);
+            ++ctx->launches;
+            DSYNC("k_fr_pred");
+        }
+        const int grid = (int)std::max(1ll, std::min<long long>(pb, (long long)ctx->sm_count * std::max(1, occ)));
+        k_friction<<<grid, DTPB, 0, s>>>(F);
+        ++ctx->launches;
+        DSYNC("k_friction");
+        CK(cudaMemcpyAsync(misc, D->fr_misc.p, 32, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int nlog = misc[4];
+        F.nlog = nlog;
+        if (nlog > 0) {  // the log sorted by (vertex, pair), carrying the entry index
+            size_t tb = 0;
+            auto* k1 = D->fr_log_key.as<unsigned long long>();
+            auto* k2 = D->fr_log_key2.as<unsigned long long>();
+            int* i1 = D->fr_log_idx.as<int>();
+            int* i2 = D->fr_log_idx2.as<int>();
+            k_iota<<<(nlog + DTPB - 1) / DTPB, DTPB, 0, s>>>(i1, nlog);
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k2, i1, i2, nlog, 0, 64, s);
+            CK(D->sort_tmp.ensure(tb));
+            CK(cub::DeviceRadixSort::SortPairs(D->sort_tmp.p, tb, k1, k2, i1, i2, nlog, 0, 64, s));
+            ctx->launches += 5;
+            F.slog_key = k2;
+            F.slog_idx = i2;
+        }
+        k_fr_verify<<<pb, DTPB, 0, s>>>(F);
+        ++ctx->launches;
+        DSYNC("k_fr_verify");
+        CK(cudaMemcpyAsync(misc, D->fr_misc.p, 32, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (misc[3] == 0) break;  // verified: no pair outside W writes
+        misc[2] += misc[3];
+        CK(cudaMemcpyAsync(F.misc + 2, misc + 2, 4, cudaMemcpyHostToDevice, s));
+        if (round > 64) return fail(ctx, TW_ECAPACITY, "friction_filter: writer set did not settle");
+    }
+    CK(cudaGetLastError());
+    return TW_OK;
+}
+
 // search + gradient/Hessian + repulsion + PCG at d_xk (N x 3, device) with
 // inertia data D->x0 / D->v0; the target goes to d_y. stats: pcg iterations /
 // convergence / pairs.
@@ -933,10 +1315,14 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
     // in key order), so searching with min(d_max, radius) yields exactly the
     // repulsive pairs of step()'s d_max search -- in the same order -- at a
     // fraction of the broad-phase cost; no repulsion, no search.
+    // friction_filter (mu > 0) reads every pair of the d_max set -- a pair
+    // farther than the radius at x can penetrate it at the target -- so then
+    // the search runs at d_max (the repulsive pairs are the same either way).
     long long np = 0;
     const bool repel = D->model.repulsion_stiffness > 0.0 && D->model.repulsion_radius > 0.0;
-    if (repel) {
-        const int rc0 = search_at_x(ctx, m, std::min(d_max, D->model.repulsion_radius), &np);
+    const bool friction = D->model.mu > 0.0;
+    if (repel || friction) {
+        const int rc0 = search_at_x(ctx, m, friction ? d_max : std::min(d_max, D->model.repulsion_radius), &np);
         if (rc0) return rc0;
     }
     int rc = TW_OK;
@@ -1021,6 +1407,12 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
     CK(cudaStreamSynchronize(s));
     k_target<<<std::max(1, nb), DTPB, 0, s>>>(nv, m->d_inv_mass.as<double>(), d_xk, P.best, G.bnorm == 0.0, d_y);
     ++ctx->launches;
+    if (friction) {  // dynamics.cpp:338
+        CK(cudaEventRecord(D->evf0, s));
+        rc = friction_device(D, d_xk, d_y, np);
+        if (rc) return rc;
+        CK(cudaEventRecord(D->evf1, s));
+    }
     float tms = 0.f, pms = 0.f;
     CK(cudaEventElapsedTime(&tms, D->evt0, D->evp1));
     CK(cudaEventElapsedTime(&pms, D->evp0, D->evp1));
@@ -1031,6 +1423,12 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
         st->pcg_converged = st->pcg_converged && G.converged;
         st->num_pairs = (int32_t)np;
         st->repulsive_pairs = counts[0];
+        if (friction) {
+            float fms = 0.f;
+            CK(cudaEventSynchronize(D->evf1));
+            CK(cudaEventElapsedTime(&fms, D->evf0, D->evf1));
+            st->friction_ms += fms;
+        }
     }
     CK(cudaGetLastError());
     return TW_OK;
@@ -1039,7 +1437,6 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
 int dyn_check(tw_ctx* ctx, tw_mesh* m, tw_dyn* D) {
     if (!ctx || !m || !D) return fail(ctx, TW_EINVAL, "dynamics: null argument");
     if (D->mesh != m) return fail(ctx, TW_EINVAL, "dynamics: model prepared on another mesh");
-    if (D->model.mu > 0.0) return fail(ctx, TW_EUNSUPPORTED, "dynamics: friction_filter (mu > 0) is not provided");
     return TW_OK;
 }
 
@@ -1168,7 +1565,8 @@ int tw_dyn_create(tw_ctx* ctx, tw_mesh* m, const tw_energy_model* model, const d
     int rc = ensure_state(D);
     if (!rc && (cudaEventCreate(&D->ev0) != cudaSuccess || cudaEventCreate(&D->ev1) != cudaSuccess ||
                 cudaEventCreate(&D->evt0) != cudaSuccess || cudaEventCreate(&D->evp0) != cudaSuccess ||
-                cudaEventCreate(&D->evp1) != cudaSuccess))
+                cudaEventCreate(&D->evp1) != cudaSuccess || cudaEventCreate(&D->evf0) != cudaSuccess ||
+                cudaEventCreate(&D->evf1) != cudaSuccess))
         rc = fail(ctx, TW_ECUDA, "dynamics: event creation failed");
     if (rc) {
         tw_dyn_destroy(D);
@@ -1184,9 +1582,11 @@ void tw_dyn_destroy(tw_dyn* D) {
     DevMem* all[] = {&D->inc_u, &D->inc_a, &D->inc_o, &D->hx, &D->hvel, &D->rest, &D->hv, &D->hk, &D->vh_off, &D->vh, &D->x0, &D->v0, &D->xk, &D->y, &D->e_u,
                      &D->e_ab, &D->rp_ids, &D->rp_sw, &D->rp_dir, &D->rp_count, &D->rs_key, &D->rs_key2,
                      &D->vr_off, &D->sort_tmp, &D->sdiag, &D->grad, &D->pre, &D->b, &D->d, &D->r, &D->z,
-                     &D->p, &D->q, &D->best, &D->part, &D->glob};
+                     &D->p, &D->q, &D->best, &D->part, &D->glob, &D->fr_pred, &D->fr_done, &D->fr_misc,
+                     &D->fr_cand, &D->fr_y0, &D->fr_log_key, &D->fr_log_key2, &D->fr_log_val, &D->fr_log_idx,
+                     &D->fr_log_idx2};
     for (DevMem* d : all) d->release();
-    for (cudaEvent_t e : {D->ev0, D->ev1, D->evt0, D->evp0, D->evp1})
+    for (cudaEvent_t e : {D->ev0, D->ev1, D->evt0, D->evp0, D->evp1, D->evf0, D->evf1})
         if (e) cudaEventDestroy(e);
     delete D;
 }
@@ -1213,6 +1613,32 @@ int tw_newton_target(tw_ctx* ctx, tw_mesh* m, tw_dyn* D, double d_max, const dou
     CK(cudaMemcpyAsync(y_out, D->y.p, bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (st) *st = local;
+    return TW_OK;
+}
+
+int tw_friction_filter(tw_ctx* ctx, tw_mesh* m, tw_dyn* D, double d_max, const double* x, const double* y_target,
+                       double* y_out) {
+    int rc = dyn_check(ctx, m, D);
+    if (rc) return rc;
+    if (!x || !y_target || !y_out) return fail(ctx, TW_EINVAL, "friction_filter: null argument");
+    if (!(d_max > 0.0)) return fail(ctx, TW_EINVAL, "friction_filter: d_max must be > 0");
+    CK(cudaSetDevice(ctx->device));
+    const int nv = m->nv;
+    const size_t bytes = (size_t)nv * 24;
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemcpyAsync(D->xk.p, x, bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(D->y.p, y_target, bytes, cudaMemcpyHostToDevice, s));
+    CK(ctx->x.ensure((size_t)std::max(1, nv) * 32));
+    k_pack_x4<<<std::max(1, (nv + DTPB - 1) / DTPB), DTPB, 0, s>>>(nv, D->xk.as<double>(), m->d_inv_mass.as<double>(),
+                                                                 ctx->x.as<double4>());
+    ++ctx->launches;
+    long long np = 0;
+    rc = search_at_x(ctx, m, d_max, &np);
+    if (rc) return rc;
+    rc = friction_device(D, D->xk.as<double>(), D->y.as<double>(), np);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(y_out, D->y.p, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     return TW_OK;
 }
 

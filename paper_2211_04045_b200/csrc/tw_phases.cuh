@@ -24,7 +24,7 @@ __device__ __forceinline__ void flip_wait(Globals* g, unsigned* w, unsigned inc)
     const unsigned old = bar_arrive(w, inc);
     volatile int* err = &g->error;
     unsigned long long t0 = 0;
-    for (unsigned it = 0; !bar_flipped(old, bar_poll(w)); ++it) {
+    for (unsigned it = 0; !bar_flipped(old, bar_poll_relaxed(w)); ++it) {
         if ((it & 63u) == 63u) {
             if (*err) break;
             const unsigned long long t = global_ns();
@@ -35,6 +35,7 @@ __device__ __forceinline__ void flip_wait(Globals* g, unsigned* w, unsigned inc)
             }
         }
     }
+    bar_acquire_fence();
 }
 
 __device__ __forceinline__ bool grid_sync(Globals* g) {

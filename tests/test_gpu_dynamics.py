@@ -175,17 +175,6 @@ def test_step_is_intersection_free(ctx):
         x = xn
 
 
-def test_friction_is_rejected(ctx):
-    from paper_2211_04045_b200 import capi
-
-    m, x, v, mesh, dyn, rm = _setup(ctx, "drape", "default")
-    d2 = capi.Dynamics(ctx, mesh, x, mu=0.3)
-    with pytest.raises(NotImplementedError):
-        capi.step(ctx, mesh, d2, x, v)
-    with pytest.raises(ValueError):
-        capi.Dynamics(ctx, mesh, x, dt=0.0)
-
-
 def test_concurrent_contexts_are_deterministic():
     """Two contexts sharing the device (tw_ctx_set_grid_share, own streams,
     threads) step independent frames at the same time and return bit for bit
