@@ -832,9 +832,11 @@ __device__ __forceinline__ void fr_apply(const FrParams& F, long long i, const i
         if (!fr_tracked(F, v)) continue;  // a +-0 write to an unchanged static vertex
         const d3 o = add(ldy(F.y, v), scl(F.dt * F.inv_mass[v] * sw[a], dv));
         __stcg(F.y + 3 * v, o.x), __stcg(F.y + 3 * v + 1, o.y), __stcg(F.y + 3 * v + 2, o.z);
-        const int e = atomicAdd(F.misc + 4, 1);
-        F.log_key[e] = ((unsigned long long)(unsigned)v << 32) | (unsigned long long)i;
-        F.log_val[e] = make_double4(o.x, o.y, o.z, 0.0);
+        if (F.log_key) {
+            const int e = atomicAdd(F.misc + 4, 1);
+            F.log_key[e] = ((unsigned long long)(unsigned)v << 32) | (unsigned long long)i;
+            F.log_val[e] = make_double4(o.x, o.y, o.z, 0.0);
+        }
     }
 }
 
@@ -868,6 +870,12 @@ __global__ void __launch_bounds__(DTPB) k_friction(FrParams F) {
             }
         }
     }
+}
+
+// every pair that is not all-static joins W (the plain dataflow: no verification needed)
+__global__ void k_fr_all(FrParams F) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < F.np) F.cand[i] = !(F.pflag[i] & FR_ALL_STATIC);
 }
 
 __global__ void k_iota(int* a, int n) {
@@ -1227,20 +1235,35 @@ int friction_device(tw_dyn* D, const double* d_xk, double* d_y, long long np) {
     int misc[8];
     CK(cudaMemcpyAsync(misc, D->fr_misc.p, 32, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    // A cascade (a write pushes the next pair into the radius, whose write
+    // pushes the next ...) adds few pairs per round; after kMaxRounds the
+    // replay runs over every pair instead, which needs no verification.
+    static const int kMaxRounds = getenv("TW_FR_MAX_ROUNDS") ? std::atoi(getenv("TW_FR_MAX_ROUNDS")) : 8;
+    bool all = false;
     for (int round = 0;; ++round) {
+        if (round == kMaxRounds) {
+            k_fr_all<<<pb, DTPB, 0, s>>>(F);
+            ++ctx->launches;
+            all = true;
+            misc[2] = (int)std::min<long long>(np, 0x7fffffff);
+        }
         const long long nw = misc[2];  // |W|
         if (nw == 0) return TW_OK;     // nothing writes at y0 and (verified) nothing after
         // buffers sized by |W|: <= 4 incidences and <= 4 logged writes per pair
         CK(D->rs_key.ensure((size_t)nw * 4 * 8));
         CK(D->rs_key2.ensure((size_t)nw * 4 * 8));
-        CK(D->fr_log_key.ensure((size_t)nw * 4 * 8));
-        CK(D->fr_log_key2.ensure((size_t)nw * 4 * 8));
-        CK(D->fr_log_val.ensure((size_t)nw * 4 * 32));
-        CK(D->fr_log_idx.ensure((size_t)nw * 4 * 4));
-        CK(D->fr_log_idx2.ensure((size_t)nw * 4 * 4));
         F.ent = D->rs_key.as<unsigned long long>();
-        F.log_key = D->fr_log_key.as<unsigned long long>();
-        F.log_val = D->fr_log_val.as<double4>();
+        if (!all) {  // the write log (the full replay needs none)
+            CK(D->fr_log_key.ensure((size_t)nw * 4 * 8));
+            CK(D->fr_log_key2.ensure((size_t)nw * 4 * 8));
+            CK(D->fr_log_val.ensure((size_t)nw * 4 * 32));
+            CK(D->fr_log_idx.ensure((size_t)nw * 4 * 4));
+            CK(D->fr_log_idx2.ensure((size_t)nw * 4 * 4));
+            F.log_key = D->fr_log_key.as<unsigned long long>();
+            F.log_val = D->fr_log_val.as<double4>();
+        } else {
+            F.log_key = nullptr;
+        }
         if (round) CK(cudaMemcpyAsync(d_y, D->fr_y0.p, (size_t)m->nv * 24, cudaMemcpyDeviceToDevice, s));
         // misc[0] entries, [1] ticket, [3] added, [4] log entries restart; [2] = |W| stays
         CK(cudaMemsetAsync(F.misc, 0, 8, s));
@@ -1265,6 +1288,7 @@ int friction_device(tw_dyn* D, const double* d_xk, double* d_y, long long np) {
         DSYNC("k_friction");
         CK(cudaMemcpyAsync(misc, D->fr_misc.p, 32, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        if (all) break;
         const int nlog = misc[4];
         F.nlog = nlog;
         if (nlog > 0) {  // the log sorted by (vertex, pair), carrying the entry index
@@ -1289,7 +1313,6 @@ int friction_device(tw_dyn* D, const double* d_xk, double* d_y, long long np) {
         if (misc[3] == 0) break;  // verified: no pair outside W writes
         misc[2] += misc[3];
         CK(cudaMemcpyAsync(F.misc + 2, misc + 2, 4, cudaMemcpyHostToDevice, s));
-        if (round > 64) return fail(ctx, TW_ECAPACITY, "friction_filter: writer set did not settle");
     }
     CK(cudaGetLastError());
     return TW_OK;

@@ -121,6 +121,32 @@ def test_friction_filter_is_deterministic(ctx):
     mesh.close()
 
 
+def test_friction_full_replay_fallback():
+    """TW_FR_MAX_ROUNDS=0: the replay runs over every pair (the fallback for a
+    writer set that does not settle) -- same bits as the reference."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np; sys.path[:0] = ['tests', 'oracle', '.']\n"
+        "import pyref as R, test_gpu_friction as T\n"
+        "from paper_2211_04045_b200 import capi\n"
+        "ctx = capi.Context(0)\n"
+        "for name in ('drape_dense', 'drape_neg_zero'):\n"
+        "    m, x, yt = T.SCENES[name]()\n"
+        "    mesh, dyn, rm = T._meshes(ctx, m, x, mu=0.3)\n"
+        "    y = capi.friction_filter(ctx, mesh, dyn, x, yt)\n"
+        "    yr = R.friction_filter(rm, x, x, yt, d_max=4e-3, mu=0.3)\n"
+        "    assert np.array_equal(y.view(np.uint64), yr.view(np.uint64)), name\n"
+        "print('ok')\n")
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "TW_FR_MAX_ROUNDS": "0"})
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
 def test_friction_filter_knot(ctx):
     """A 200-segment knot frame (two plies, 8K vertices): the tightening target
     penetrates where the knot is tightest."""
