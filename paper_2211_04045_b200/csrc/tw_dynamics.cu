@@ -30,10 +30,12 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <utility>
 #include <vector>
@@ -694,6 +696,9 @@ struct FrParams {
     int* pred;              // 4 per pair: the pair to wait for at that slot, -1 none
     int* done;
     int* misc;              // [0] entries, [1] ticket, [2] |W|, [3] added to W, [4] log entries
+    int* rank;              // per pair: its position among W's pairs (exclusive scan of cand)
+    int* wlist;             // W's pairs in pair order
+    int nw;
     unsigned long long* log_key;  // (vertex << 32 | pair) per logged write
     double4* log_val;             // y after that write
     const unsigned long long* slog_key;  // the log sorted by key, with the entry index
@@ -840,33 +845,61 @@ __device__ __forceinline__ void fr_apply(const FrParams& F, long long i, const i
     }
 }
 
-// 2b. the replay over W. Warps take 32 consecutive pairs from a ticket counter
-// in pair order, so the earliest unfinished pair of W always belongs to a
-// running warp whose predecessors are all finished: the pass cannot stall.
+__global__ void k_fr_compact(FrParams F) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < F.np && F.cand[i]) F.wlist[F.rank[i]] = (int)i;
+}
+
+// 2b. the replay over W (compacted: a warp holds 32 consecutive pairs of W,
+// which mostly chain through their shared query vertex). Warps take them from
+// a ticket counter in pair order, so the earliest unfinished pair of W always
+// belongs to a running warp whose predecessors are all finished: the pass
+// cannot stall. A predecessor in the same warp is waited for through the
+// warp's done ballot (its writes are ordered by __syncwarp, y at L2); one in
+// another warp through its done flag.
 __global__ void __launch_bounds__(DTPB) k_friction(FrParams F) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         int base = 0;
         if (lane == 0) base = atomicAdd(F.misc + 1, 32);
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= F.np) return;
-        const long long i = (long long)base + lane;
-        bool pending = i < F.np && F.cand[i];
-        int4 pr = make_int4(-1, -1, -1, -1);
+        if (base >= F.nw) return;
+        const int t = base + lane;
+        bool fin = t >= F.nw;
+        long long i = 0;
+        int pq[4] = {-1, -1, -1, -1};  // >= 0: pair index (another warp); <= -2: -2 - lane (this warp)
         uint64_t key = 0;
         int vid[4] = {-1, -1, -1, -1};
-        if (pending) {
-            pr = reinterpret_cast<const int4*>(F.pred)[i];
+        if (!fin) {
+            i = F.wlist[t];
+            const int4 pr = reinterpret_cast<const int4*>(F.pred)[i];
+            const int pp[4] = {pr.x, pr.y, pr.z, pr.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (pp[k] >= 0) {
+                    const int r = F.rank[pp[k]];
+                    pq[k] = r >= base ? -2 - (r - base) : pp[k];
+                }
             key = F.pkey[i];
             fr_verts(key, F.pids[i], vid);
         }
-        while (__any_sync(0xffffffffu, pending)) {
-            if (pending && (pr.x < 0 || ld_relaxed(F.done + pr.x)) && (pr.y < 0 || ld_relaxed(F.done + pr.y)) &&
-                (pr.z < 0 || ld_relaxed(F.done + pr.z)) && (pr.w < 0 || ld_relaxed(F.done + pr.w))) {
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                fr_class(key, [&](auto c) { fr_apply<decltype(c)::ka, decltype(c)::kb>(F, i, vid); });
-                st_release(F.done + i, 1);
-                pending = false;
+        for (;;) {
+            __syncwarp();
+            const unsigned donem = __ballot_sync(0xffffffffu, fin);
+            if (donem == 0xffffffffu) break;
+            if (!fin) {
+                bool ready = true, remote = false;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (pq[k] <= -2) ready = ready && ((donem >> (-2 - pq[k])) & 1u);
+                    else if (pq[k] >= 0) ready = ready && ld_relaxed(F.done + pq[k]), remote = true;
+                }
+                if (ready) {
+                    if (remote) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    fr_class(key, [&](auto c) { fr_apply<decltype(c)::ka, decltype(c)::kb>(F, i, vid); });
+                    st_release(F.done + i, 1);
+                    fin = true;
+                }
             }
         }
     }
@@ -995,7 +1028,7 @@ struct tw_dyn {
     DevMem inc_u, inc_a, inc_o, hx, hvel, x0, v0, xk, y, e_u, e_ab, rp_ids, rp_sw, rp_dir, rp_count, rs_key, rs_key2, vr_off, sort_tmp;
     DevMem sdiag, grad, pre, b, d, r, z, p, q, best, part, glob;
     DevMem fr_pred, fr_done, fr_misc, fr_cand, fr_y0;  // friction_filter replay state
-    DevMem fr_log_key, fr_log_key2, fr_log_val, fr_log_idx, fr_log_idx2;
+    DevMem fr_log_key, fr_log_key2, fr_log_val, fr_log_idx, fr_log_idx2, fr_rank, fr_wlist;
     long long rp_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // step timing (the resolve uses the context's own events)
     cudaEvent_t evt0 = nullptr, evp0 = nullptr, evp1 = nullptr;  // target / PCG timing
@@ -1190,6 +1223,10 @@ int search_at_x(tw_ctx* ctx, tw_mesh* m, double d_max, long long* np) {
 // friction_filter (dynamics.cpp:272-324) on d_y (N x 3, in place) with the
 // pair set the context holds from the search at d_xk (np pairs, key order):
 // the writer-set speculation of k_fr_eval0 / k_friction / k_fr_verify.
+struct ScanAdd {
+    __device__ __forceinline__ int operator()(int a, int b) const { return a + b; }
+};
+
 template <typename K>
 cudaError_t sort_keys(tw_dyn* D, K* in, K* out, int n, cudaStream_t s) {
     size_t tb = 0;
@@ -1209,6 +1246,8 @@ int friction_device(tw_dyn* D, const double* d_xk, double* d_y, long long np) {
     CK(D->fr_pred.ensure((size_t)np * 16));
     CK(D->fr_done.ensure((size_t)np * 4));
     CK(D->fr_cand.ensure((size_t)np));
+    CK(D->fr_rank.ensure((size_t)np * 4));
+    CK(D->fr_wlist.ensure((size_t)np * 4));
     CK(D->fr_misc.ensure(32));
     CK(D->fr_y0.ensure(nv * 24));
     CK(cudaMemcpyAsync(D->fr_y0.p, d_y, (size_t)m->nv * 24, cudaMemcpyDeviceToDevice, s));
@@ -1282,7 +1321,20 @@ int friction_device(tw_dyn* D, const double* d_xk, double* d_y, long long np) {
             ++ctx->launches;
             DSYNC("k_fr_pred");
         }
-        const int grid = (int)std::max(1ll, std::min<long long>(pb, (long long)ctx->sm_count * std::max(1, occ)));
+        {  // W in pair order: rank = exclusive scan of cand, wlist[rank] = pair
+            size_t tb = 0;
+            int* rk = D->fr_rank.as<int>();
+            cub::DeviceScan::ExclusiveScan(nullptr, tb, F.cand, rk, ScanAdd{}, 0, (int)np, s);
+            CK(D->sort_tmp.ensure(tb));
+            CK(cub::DeviceScan::ExclusiveScan(D->sort_tmp.p, tb, F.cand, rk, ScanAdd{}, 0, (int)np, s));
+            F.rank = rk;
+            F.wlist = D->fr_wlist.as<int>();
+            F.nw = (int)nw;
+            k_fr_compact<<<pb, DTPB, 0, s>>>(F);
+            ctx->launches += 3;
+        }
+        const unsigned wb = (unsigned)((nw + DTPB - 1) / DTPB);
+        const int grid = (int)std::max(1ll, std::min<long long>(wb, (long long)ctx->sm_count * std::max(1, occ)));
         k_friction<<<grid, DTPB, 0, s>>>(F);
         ++ctx->launches;
         DSYNC("k_friction");
@@ -1310,6 +1362,9 @@ int friction_device(tw_dyn* D, const double* d_xk, double* d_y, long long np) {
         DSYNC("k_fr_verify");
         CK(cudaMemcpyAsync(misc, D->fr_misc.p, 32, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        if (getenv("TW_FR_STATS"))
+            fprintf(stderr, "friction round %d: |W| %lld, incidences %d, logged writes %d, added %d\n", round, nw,
+                    nent, nlog, misc[3]);
         if (misc[3] == 0) break;  // verified: no pair outside W writes
         misc[2] += misc[3];
         CK(cudaMemcpyAsync(F.misc + 2, misc + 2, 4, cudaMemcpyHostToDevice, s));
@@ -1607,7 +1662,7 @@ void tw_dyn_destroy(tw_dyn* D) {
                      &D->vr_off, &D->sort_tmp, &D->sdiag, &D->grad, &D->pre, &D->b, &D->d, &D->r, &D->z,
                      &D->p, &D->q, &D->best, &D->part, &D->glob, &D->fr_pred, &D->fr_done, &D->fr_misc,
                      &D->fr_cand, &D->fr_y0, &D->fr_log_key, &D->fr_log_key2, &D->fr_log_val, &D->fr_log_idx,
-                     &D->fr_log_idx2};
+                     &D->fr_log_idx2, &D->fr_rank, &D->fr_wlist};
     for (DevMem* d : all) d->release();
     for (cudaEvent_t e : {D->ev0, D->ev1, D->evt0, D->evp0, D->evp1, D->evf0, D->evf1})
         if (e) cudaEventDestroy(e);

@@ -29,3 +29,13 @@ for n_along in (1870,):
           f"{np.array_equal(y.view(np.uint64), y2.view(np.uint64))}", flush=True)
     dyn.close()
     mesh.close()
+
+# per-phase timing of one filter call (TW_FR_STATS prints the rounds)
+if os.environ.get("TW_FR_PROFILE"):
+    fr, v0 = S.knot_frame(n_along=1870)
+    mesh = capi.Mesh.from_scene(ctx, fr)
+    dyn = capi.Dynamics(ctx, mesh, fr.x, mu=0.3)
+    capi.friction_filter(ctx, mesh, dyn, fr.x, fr.x + 0.01 * v0)
+    t = time.perf_counter()
+    capi.search(ctx, mesh, fr.x, 4e-3)
+    print(f"search alone {1e3 * (time.perf_counter() - t):.1f} ms", flush=True)
