@@ -15,7 +15,8 @@ import weakref
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtwoway_b200.so")
+# TW_LIB_PATH: an alternative in-tree build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("TW_LIB_PATH") or os.path.join(_HERE, "libtwoway_b200.so")
 
 TW_OK, TW_EINVAL, TW_EUNSUPPORTED, TW_ECAPACITY, TW_ECUDA, TW_ETIMEOUT = range(6)
 SOLVERS = {"pgs": 0, "jacobi": 1, "al20": 2, "al100": 3}

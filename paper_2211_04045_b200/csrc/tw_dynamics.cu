@@ -1466,7 +1466,6 @@ int newton_target_device(tw_dyn* D, double d_max, const double* d_xk, double* d_
     const bool want2 = vpt_env && std::atoi(vpt_env) == 2;
     const bool fit1 = b1 <= ctx->sm_count * occ[0] / parts, fit2 = b2 <= ctx->sm_count * occ[1] / parts;
     const int vpt = getenv("TW_PCG_GLOBAL") ? 0 : (want2 && fit2) ? 2 : fit1 ? 1 : fit2 ? 2 : 0;
-    const bool use_reg = vpt != 0;
     const int pb = vpt == 1 ? b1 : vpt == 2 ? b2 : std::max(1, pcg_blocks(ctx, nv) / parts);
     P.nblocks = pb;
     CK(D->part.ensure((size_t)pb * 32));

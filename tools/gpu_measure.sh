@@ -20,3 +20,9 @@ timeout 300 python tools/prof_search.py > gpurun_out/plain2.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_stage -c 2 \
     -o gpurun_out/prof_search -f python tools/prof_search.py > gpurun_out/ncu_search.log 2>&1
 echo "ncu search rc=$?"; tail -2 gpurun_out/ncu_search.log
+# Summarise on the box (the .ncu-rep files exceed gpurun's 64 MiB merge limit):
+# profiles are staged under gpurun_out/profiles_staged and copied into
+# profiles/ here; the reports are then removed from gpurun_out.
+TW_PROF_DIR=gpurun_out/profiles_staged python tools/make_profiles.py ${PROF_TAG:-r02} > gpurun_out/make_profiles.log 2>&1
+echo "make_profiles rc=$?"; tail -2 gpurun_out/make_profiles.log
+rm -f gpurun_out/*.ncu-rep

@@ -22,7 +22,7 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-PROF = os.path.join(ROOT, "profiles")
+PROF = os.environ.get("TW_PROF_DIR") or os.path.join(ROOT, "profiles")  # staged on the GPU box
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 
 METRICS = [
