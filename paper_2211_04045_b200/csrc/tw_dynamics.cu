@@ -706,7 +706,8 @@ struct FrParams {
     int nlog;
 };
 
-__device__ __forceinline__ void fr_verts(uint64_t key, int4 ids, int (&v)[4]) {
+// the pair's vertex ids in the reference's vid order (a's, then b's; -1 padded)
+__device__ __forceinline__ void fr_verts(int4 ids, int (&v)[4]) {
     v[0] = ids.x, v[1] = ids.y, v[2] = ids.z, v[3] = ids.w;
 }
 
@@ -776,7 +777,7 @@ __global__ void k_fr_eval0(FrParams F) {
     if (!(F.pflag[i] & FR_ALL_STATIC)) {  // dynamics.cpp:278
         const uint64_t key = F.pkey[i];
         int vid[4];
-        fr_verts(key, F.pids[i], vid);
+        fr_verts(F.pids[i], vid);
         auto Y = [&](int v) { return ld3(F.y0, v); };
         fr_class(key, [&](auto c) {
             double sw[4];
@@ -797,7 +798,7 @@ __global__ void k_fr_entries(FrParams F) {
     if (!F.cand[i]) return;
     const uint64_t key = F.pkey[i];
     int v[4];
-    fr_verts(key, F.pids[i], v);
+    fr_verts(F.pids[i], v);
     const int n = (key_ka(key) + 1) + (key_kb(key) + 1);
     for (int k = 0; k < n; ++k)
         if (fr_tracked(F, v[k]))
@@ -881,7 +882,7 @@ __global__ void __launch_bounds__(DTPB) k_friction(FrParams F) {
                     pq[k] = r >= base ? -2 - (r - base) : pp[k];
                 }
             key = F.pkey[i];
-            fr_verts(key, F.pids[i], vid);
+            fr_verts(F.pids[i], vid);
         }
         for (;;) {
             __syncwarp();
@@ -939,7 +940,7 @@ __global__ void k_fr_verify(FrParams F) {
     if (i >= F.np || F.cand[i] || (F.pflag[i] & FR_ALL_STATIC)) return;
     const uint64_t key = F.pkey[i];
     int vid[4];
-    fr_verts(key, F.pids[i], vid);
+    fr_verts(F.pids[i], vid);
     auto Y = [&](int v) { return fr_state(F, v, i); };
     bool w = false;
     fr_class(key, [&](auto c) {
